@@ -1,0 +1,182 @@
+/*
+ * ddh.h -- C ABI of the B200-native DDH-MBIR hot path (libddh.so).
+ *
+ * Dynamic DH-MBIR (Sheikh, Pellizzari, Kisner, Buzzard, Bouman, arXiv
+ * 2305.03284) estimates, for every time step n of a stream of single-shot
+ * digital-holography (DH) frames y_n, the pupil phase error phi_n and the
+ * image reflectance r_n of the model
+ *
+ *     y_n = A_{phi_n} g_n + w_n,   A_phi = D_a D(e^{j phi}) F_c^{-1},   g_n ~ CN(0, D(r_n))
+ *
+ * (Eq. 1; Gamma = I and F vs F^{-1} per DESIGN.md
+ * readings R3/R5).  Citations "P:<line>" are lines of PAPER.md; "R<k>" are
+ * the readings listed in DESIGN.md (where the paper is silent).
+ *
+ * Conventions shared by every entry point
+ *   - Grid: N x N, row-major, index (i = row, j = column), centre (N/2, N/2).
+ *     N is one of 64, 128, 256, 512, 1024.
+ *   - Frames: complex64 = two little-endian IEEE float32 (re, im), layout
+ *     [T][S][N][N] (frame-major, then stream, then row, then column).
+ *   - Fields (phi, r): float32 [S][N][N] or [T][S][N][N].
+ *   - Unless an argument says "host", pointers are CUDA device pointers on
+ *     the ctx's device (e.g. torch tensors' data_ptr()).  The CALLER owns all
+ *     input/output buffers and keeps them alive until ddh_sync() returns; the
+ *     ctx owns its per-stream state and workspace.
+ *   - Execution is asynchronous on the CUDA stream given to ddh_create unless
+ *     an entry point says "synchronous".
+ *   - Every function returns a ddh_status and never throws.  DDH_E_INVAL
+ *     leaves the ctx unchanged.  A CUDA error is sticky (DDH_E_CUDA from then
+ *     on; the ctx can only be destroyed).  ddh_last_error() explains the last
+ *     failure.
+ *   - A degenerate frame (||y - mean(y)|| = 0, Eq. 4 undefined) does not fail
+ *     the call: its status byte is 1 and that stream's (r, phi) are left
+ *     unchanged; the frame counter still advances.
+ */
+#ifndef DDH_H_
+#define DDH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DDH_OK = 0,
+  DDH_E_INVAL = 1,  /* bad argument / unsupported configuration      */
+  DDH_E_CUDA = 2,   /* CUDA runtime error (sticky)                    */
+  DDH_E_NOMEM = 3,  /* device or host allocation failed               */
+  DDH_E_STATE = 4   /* ctx unusable (after a sticky error)            */
+} ddh_status;
+
+/* flags */
+#define DDH_F_NO_TIPTILT 1u /* skip RemoveTipTilt (Fig. 1) in ddh_step  */
+
+typedef struct ddh_ctx ddh_ctx; /* opaque */
+
+/* Algorithm and layout parameters.  Fill with ddh_default_params() first. */
+typedef struct {
+  int32_t n;        /* grid side N: 64, 128, 256, 512 or 1024                         */
+  int32_t streams;  /* S independent sensor streams owned by this ctx (>= 1)           */
+  int32_t device;   /* CUDA device ordinal                                             */
+  float aperture_diam;          /* D_a: circle of diameter D px, strictly inside,
+                                   centred at (N/2, N/2); <= 0 selects aperture_mask     */
+  const uint8_t *aperture_mask; /* host [N][N] {0,1}, used when aperture_diam <= 0; every
+                                   row must be empty or one contiguous run of ones       */
+  double noise_var; /* sigma^2 of the reconstruction in normalised-data units (R19), > 0  */
+  double lambda;    /* Eq. 3 weight lambda in [0,1], default 0.45                 */
+  double alpha;     /* Eq. 3 weight alpha in [0,1], default 0.025                 */
+  int32_t n_k;      /* EM iterations per time step N_k >= 1 (Fig. 1)                */
+  double r_min;     /* floor on r (replaces r <- 0 of Fig. 1, R14), > 0, default 1e-4      */
+  double r_sigma;   /* qGGMRF scale sigma_r; <= 0 disables the r prior (R6/R7), def. 0.5  */
+  double r_T;       /* qGGMRF threshold T > 0, default 1                                  */
+  double r_q;       /* qGGMRF tail exponent q in [1,2], default 1.2                       */
+  double phi_sigma; /* GMRF scale sigma_phi; <= 0 disables the phi prior (R11), def. 0.5 */
+  int32_t icd_sweeps;   /* 4-colour ICD sweeps per M-step >= 1, default 1 (R8)             */
+  int32_t boot_period;  /* bootstrap reset period P_b >= 1, default 200            */
+  double boot_alpha;    /* bootstrap back-projection weight alpha_b > 0, default 1 (R15)   */
+  int32_t chunk_streams;/* streams per launch group (L2-resident workspace); 0 = auto       */
+  uint32_t flags;       /* DDH_F_*                                                        */
+} ddh_params;
+
+/* Defaults: N=256, S=1, device 0, D=N, sigma^2=0.1, lambda=0.45, alpha=0.025,
+ * N_k=1, r_min=1e-4, sigma_r=0.5, T=1, q=1.2, sigma_phi=0.5, 1 sweep,
+ * P_b=200, alpha_b=1, chunk auto, flags 0.  Errors: DDH_E_INVAL if p is NULL. */
+ddh_status ddh_default_params(ddh_params *p);
+
+/* Create a ctx for S streams on p->device: validates p, allocates the state
+ * r = r_min, phi = 0, frame counter n = 0 (Fig. 1 P:163 with R14), and the
+ * workspace.  cuda_stream: a cudaStream_t (NULL = legacy default stream) on
+ * which all work of this ctx is enqueued.  *out receives the ctx (caller frees
+ * it with ddh_destroy).  Synchronous.
+ * Errors: DDH_E_INVAL (params out of range, unsupported N, non-interval mask),
+ * DDH_E_NOMEM, DDH_E_CUDA. */
+ddh_status ddh_create(const ddh_params *p, void *cuda_stream, ddh_ctx **out);
+
+/* Free a ctx and everything it owns (synchronises its stream first). */
+ddh_status ddh_destroy(ddh_ctx *c);
+
+/* Bootstrap on the first frame (R15): every stream is cold-
+ * started (r = r_min, phi = 0), y0 is normalised (Eq. 4), then k_b EM
+ * iterations run; before iteration k with k mod boot_period == 0 the
+ * reflectance is reset to max(boot_alpha |A_phi^H y|^2, r_min).  The frame is
+ * consumed (frame counter += 1).  k_b == 0 is a no-op (Fig. 1 cold start).
+ * y0: device complex64 [S][N][N].  status: device uint8 [S] or NULL (0 ok,
+ * 1 degenerate frame: the stream stays cold).  Errors: DDH_E_INVAL (k_b < 0,
+ * NULL y0), DDH_E_CUDA. */
+ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *status);
+
+/* The hot path: T time steps of DDH_MBIR (Fig. 1) for all S streams.
+ * For each t: y <- Normalize(y_t) (Eq. 4); phi <- RemoveTipTilt(phi) (
+ * LS plane incl. piston, R17); r <- max((1-lambda) r + lambda alpha
+ * |A_phi^H y|^2, r_min) (Eq. 3); then N_k EM iterations (E-step, qGGMRF r-ICD,
+ * GMRF phi-ICD; R1-R12), two 2-D FFTs each (R13); WriteData.
+ * y: device complex64 [T][S][N][N].  phi_out, r_out: device float32
+ * [T][S][N][N] or NULL (the state always advances).  status: device uint8
+ * [T][S] or NULL.  Errors: DDH_E_INVAL (T < 0 or NULL y with T > 0),
+ * DDH_E_CUDA. */
+ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float *r_out,
+                    uint8_t *status);
+
+/* Same as ddh_step with HOST buffers (the end-to-end path): for each t the
+ * frame batch y_t is copied host->device, stepped, and phi/r/status of that
+ * step copied device->host.  y_host: host complex64 [T][S][N][N] (pinned
+ * memory recommended); phi_out/r_out/status: host [T][S][N][N] / [T][S] or
+ * NULL.  Synchronous.  Errors as ddh_step, plus DDH_E_NOMEM. */
+ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out,
+                         float *r_out, uint8_t *status);
+
+/* Conventional single-shot DH-MBIR on each of T frame
+ * batches independently: cold start, `iters` EM iterations with bootstrap
+ * resets every boot_period.  The ctx state is left equal to the last frame's
+ * result.  Arguments as ddh_step.  Errors: DDH_E_INVAL (iters < 1). */
+ddh_status ddh_static(ddh_ctx *c, const void *y, int32_t T, int32_t iters, float *phi_out,
+                      float *r_out, uint8_t *status);
+
+/* Copy the state out / in (checkpoint / resume; SPEC state continuity).
+ * r, phi: device float32 [S][N][N] (either may be NULL); frame_index: host
+ * int64 (may be NULL).  Errors: DDH_E_CUDA. */
+ddh_status ddh_get_state(ddh_ctx *c, float *r, float *phi, int64_t *frame_index);
+ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t frame_index);
+
+/* Peak Strehl ratio of B phase estimates against truth:
+ * S_b = max |F_c^{-1}(a e^{j psi_b})|^2 / max |F_c^{-1}(a)|^2,
+ * psi_b = phi_hat_b - phi_true_b minus its LS plane over the aperture (R26).
+ * phi_hat, phi_true: device float32 [B][N][N].  strehl_out: HOST double [B].
+ * Synchronous.  Errors: DDH_E_INVAL (B < 0, NULL), DDH_E_CUDA. */
+ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B,
+                      double *strehl_out);
+
+/* Wait for all work enqueued by this ctx. */
+ddh_status ddh_sync(ddh_ctx *c);
+
+/* Human-readable description of the last error of c (or of the last failed
+ * ddh_create when c is NULL).  Never NULL; owned by the library. */
+const char *ddh_last_error(const ddh_ctx *c);
+
+/* Number of CUDA kernels this ctx has launched so far (instrumentation). */
+uint64_t ddh_kernel_launches(const ddh_ctx *c);
+
+/* Frames processed so far (the n of Fig. 1). */
+int64_t ddh_frame_index(const ddh_ctx *c);
+
+/* ---- stage entry points for parity tests (same kernels as the hot path) ---- */
+
+/* Centred unitary 2-D DFT F_c (inverse = 0) or F_c^{-1} (inverse = 1) of B
+ * fields (R4): in, out device complex64 [B][N][N] (may alias). */
+ddh_status ddh_test_fft2c(ddh_ctx *c, const void *in, void *out, int32_t B, int32_t inverse);
+
+/* One r M-step (colour-ordered qGGMRF ICD, icd_sweeps sweeps; R6-R9) of B
+ * fields: r_in, q, r_out device float32 [B][N][N] (r_out must not alias). */
+ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t B, float *r_out);
+
+/* One phi M-step (colour-ordered GMRF ICD; R10-R11) of B fields given the
+ * phase-correlation terms c, theta: device float32 [B][N][N]. */
+ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta,
+                           int32_t B, float *phi_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDH_H_ */

@@ -248,7 +248,7 @@ def phi_prior_coeffs(phi, ii, jj):
         sb += np.where(valid, b, 0.0)
     return nb, sb
 
-def r_update_pixels(r_cur, q, B, S, r_min):
+def r_update_pixels(r_cur, q, B, S, r_min, return_gap=False):
     """Exact minimiser of the surrogate over x >= r_min for a vector of pixels
     (R9).  Stationary points solve 2 B x^3 - 2 S x^2 + x - q = 0; the roots are
     the eigenvalues of the companion matrix of the monic cubic (LAPACK).
@@ -268,10 +268,17 @@ def r_update_pixels(r_cur, q, B, S, r_min):
     fmin = f.min(axis=1, keepdims=True)
     near = f <= fmin + 1e-12 * (1.0 + np.abs(fmin))
     dist = np.where(near, np.abs(cand - r_cur[:, None]), np.inf)
-    return cand[np.arange(m), dist.argmin(axis=1)]
+    best = cand[np.arange(m), dist.argmin(axis=1)]
+    if not return_gap:
+        return best
+    # diagnostic for the parity protocol: cost gap to the best
+    # candidate that is far (> 1e-3 relative) from the chosen one
+    far = np.abs(cand - best[:, None]) > 1e-3 * np.maximum(best[:, None], r_min)
+    gap = np.where(far, f - fmin, np.inf).min(axis=1) / (1.0 + np.abs(fmin[:, 0]))
+    return best, gap
 
 
-def r_icd(r: np.ndarray, q: np.ndarray, p: OracleParams) -> np.ndarray:
+def r_icd(r: np.ndarray, q: np.ndarray, p: OracleParams, gaps: Optional[np.ndarray] = None) -> np.ndarray:
     """r M-step: colour-ordered ICD with the qGGMRF prior (north_star; R6-R9).
 
     For each colour (i mod 2, j mod 2) in order (0,0),(0,1),(1,0),(1,1), every
@@ -290,7 +297,11 @@ def r_icd(r: np.ndarray, q: np.ndarray, p: OracleParams) -> np.ndarray:
             ii = ii.ravel()
             jj = jj.ravel()
             B, S = r_prior_coeffs(r, ii, jj, p)
-            r[ii, jj] = r_update_pixels(r[ii, jj], q[ii, jj], B, S, p.r_min)
+            if gaps is None:
+                r[ii, jj] = r_update_pixels(r[ii, jj], q[ii, jj], B, S, p.r_min)
+            else:
+                r[ii, jj], g = r_update_pixels(r[ii, jj], q[ii, jj], B, S, p.r_min, return_gap=True)
+                gaps[ii, jj] = np.minimum(gaps[ii, jj], g)
     return r
 
 
@@ -344,13 +355,13 @@ def phi_icd(phi: np.ndarray, c: np.ndarray, theta: np.ndarray, p: OracleParams) 
     return phi
 
 
-def em_update(r, phi, yhat, u, a, p: OracleParams):
+def em_update(r, phi, yhat, u, a, p: OracleParams, gaps=None):
     """One EM iteration EM(r, phi; y) given u = A_phi^H y:
     E-step, r M-step (uses q only) and phi M-step (uses f = F_c^{-1} mu only).
     The two M-steps read only E-step quantities, so their order is
     irrelevant (R12).  Exactly two 2-D FFTs per iteration (R13)."""
     mu, _C, q = e_step(u, r, p.noise_var)
-    r_new = r_icd(r, q, p)
+    r_new = r_icd(r, q, p, gaps)
     f = ifft2c(mu)
     c, theta = phase_correlation(yhat, f, a, p.noise_var)
     phi_new = phi_icd(phi, c, theta, p)
@@ -362,7 +373,7 @@ def em_update(r, phi, yhat, u, a, p: OracleParams):
 # ---------------------------------------------------------------------------
 
 
-def ddh_step(r, phi, y, p: OracleParams, a=None):
+def ddh_step(r, phi, y, p: OracleParams, a=None, gaps=None):
     """One time step of DDH_MBIR (Fig. 1):
     y <- Normalize(y); phi <- RemoveTipTilt(phi);
     r <- (1-lam) r + lam alpha |A_phi^H y|^2 (Eq. 3); N_k x EM(r, phi; y).
@@ -380,11 +391,11 @@ def ddh_step(r, phi, y, p: OracleParams, a=None):
     for k in range(p.n_k):
         if k > 0:
             u = adjoint(phi, yhat, a)
-        r, phi = em_update(r, phi, yhat, u, a, p)
+        r, phi = em_update(r, phi, yhat, u, a, p, gaps)
     return r, phi, 0
 
 
-def bootstrap(y0, p: OracleParams, k_b: int, a=None):
+def bootstrap(y0, p: OracleParams, k_b: int, a=None, gaps=None):
     """Bootstrap on the first frame (R15): cold start
     r = r_min, phi = 0, then K_b EM iterations; before iteration k with
     k mod P_b == 0 the reflectance is reset to the back-projection
@@ -403,7 +414,7 @@ def bootstrap(y0, p: OracleParams, k_b: int, a=None):
         u = adjoint(phi, yhat, a)
         if k % p.boot_period == 0:
             r = np.maximum(p.boot_alpha * np.abs(u) ** 2, p.r_min)
-        r, phi = em_update(r, phi, yhat, u, a, p)
+        r, phi = em_update(r, phi, yhat, u, a, p, gaps)
     return r, phi, 0
 
 

@@ -1,0 +1,663 @@
+// ddh_api.cpp -- host side of libddh.so: the C ABI declared in include/ddh.h.
+//
+// Owns per-stream state (r, phi ping-pong) and the launch-group workspace,
+// validates parameters and sequences the kernels of ddh_kernels.cu:
+//   per frame batch t, per launch group (chunk of streams):
+//     K0 ; N_k x [ K1 ; K2a ; icd_sweeps x K2b ; K3a ; icd_sweeps x K3b ]
+// (Fig. 1; Eq. 3 only in the first iteration; RemoveTipTilt's plane
+// is subtracted by K1/K3b of the first iteration).  Everything is enqueued on
+// the ctx stream; nothing here computes on the host except the aperture's
+// constant tables (row intervals, 3x3 normal-matrix inverse, twiddles).
+#include "../../include/ddh.h"
+#include "ddh_kernels.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using ddh::IcdArgs;
+using ddh::StepArgs;
+using ddh::StrehlArgs;
+
+struct ddh_ctx {
+  ddh_params p{};
+  cudaStream_t st = nullptr;
+  int n = 0, S = 0, sc = 0, nb0 = 0, nb1 = 0, strehl_nb = 0;
+  size_t P = 0;
+  // state
+  float *r = nullptr;
+  float *phi[2] = {nullptr, nullptr};
+  int cur = 0;
+  int64_t frame = 0;
+  // launch-group workspace
+  float2 *cbuf = nullptr;
+  float *rinit = nullptr, *q = nullptr, *cc = nullptr, *theta = nullptr;
+  float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
+  double *part0 = nullptr, *part1 = nullptr;
+  float *pmax = nullptr;
+  // constants
+  int2 *rowspan = nullptr;
+  float2 *tw = nullptr;
+  double minv[9] = {};
+  double strehl_den = 1.0;
+  // host-buffer path
+  float2 *y_stage = nullptr;
+  float *phi_stage = nullptr, *r_stage = nullptr;
+  uint8_t *status_stage = nullptr;
+  // bookkeeping
+  uint64_t launches = 0;
+  bool sticky = false;
+  std::string err;
+};
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_create_err;
+
+ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (s == DDH_E_CUDA) c->sticky = true;
+  } else {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    g_create_err = msg;
+  }
+  return s;
+}
+
+#define DDH_CK(c, call)                                                                      \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail((c), DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+#define DDH_LAUNCH(c, call)  \
+  do {                       \
+    DDH_CK(c, call);         \
+    (c)->launches++;         \
+  } while (0)
+
+bool valid_n(int n) { return n == 64 || n == 128 || n == 256 || n == 512 || n == 1024; }
+
+ddh_status check_usable(ddh_ctx *c) {
+  if (!c) return DDH_E_INVAL;
+  if (c->sticky) return DDH_E_STATE;
+  return DDH_OK;
+}
+
+template <class T>
+cudaError_t dalloc(T **p, size_t count) {
+  return cudaMalloc((void **)p, std::max<size_t>(count, 1) * sizeof(T));
+}
+
+StepArgs base_args(ddh_ctx *c, int s0, int sc) {
+  StepArgs a{};
+  a.n = c->n;
+  a.sc = sc;
+  a.nb0 = c->nb0;
+  a.nb1 = c->nb1;
+  a.r_state = c->r + (size_t)s0 * c->P;
+  a.cbuf = c->cbuf;
+  a.rinit = c->rinit;
+  a.q = c->q;
+  a.cc = c->cc;
+  a.theta = c->theta;
+  a.part0 = c->part0;
+  a.part1 = c->part1;
+  a.rowspan = c->rowspan;
+  a.tw = c->tw;
+  a.s2 = (float)c->p.noise_var;
+  a.r_min = (float)c->p.r_min;
+  a.P = (float)c->P;
+  std::memcpy(a.minv, c->minv, sizeof(a.minv));
+  return a;
+}
+
+IcdArgs ricd_args(ddh_ctx *c) {
+  IcdArgs a{};
+  a.n = c->n;
+  a.nb0 = c->nb0;
+  a.nb1 = c->nb1;
+  a.prior = c->p.r_sigma > 0 ? 1 : 0;
+  a.r_min = (float)c->p.r_min;
+  if (a.prior) {
+    a.b0 = (float)(1.0 / (2.0 * c->p.r_sigma * c->p.r_sigma));
+    a.inv_Tsig = (float)(1.0 / (c->p.r_T * c->p.r_sigma));
+    a.two_minus_q = (float)(2.0 - c->p.r_q);
+  }
+  return a;
+}
+
+IcdArgs phiicd_args(ddh_ctx *c) {
+  IcdArgs a{};
+  a.n = c->n;
+  a.nb0 = c->nb0;
+  a.nb1 = c->nb1;
+  a.prior = c->p.phi_sigma > 0 ? 1 : 0;
+  if (a.prior) a.b0 = (float)(1.0 / (c->p.phi_sigma * c->p.phi_sigma));
+  std::memcpy(a.minv, c->minv, sizeof(a.minv));
+  return a;
+}
+
+// r M-step: icd_sweeps sweeps of K2b from r_in into r_final (+ copy).
+ddh_status run_ricd(ddh_ctx *c, const float *r_in, const float *q, float *r_final, float *copy,
+                    const double *part1, int sc) {
+  IcdArgs a = ricd_args(c);
+  a.q = q;
+  a.part1 = part1;
+  const int sw = c->p.icd_sweeps;
+  const float *in = r_in;
+  for (int k = 0; k < sw; ++k) {
+    const bool last = (k == sw - 1);
+    float *out = last ? r_final : c->rtmp[k & 1];
+    a.in = in;
+    a.out = out;
+    a.copy = last ? copy : nullptr;
+    DDH_LAUNCH(c, ddh::launch_ricd(a, sc, c->st));
+    in = out;
+  }
+  return DDH_OK;
+}
+
+// phi M-step: icd_sweeps sweeps of K3b (plane subtracted in the first sweep).
+ddh_status run_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta, float *phi_final,
+                      float *copy, const double *part0, const double *part1, int apply_plane, int sc) {
+  IcdArgs a = phiicd_args(c);
+  a.q = cc;
+  a.theta = theta;
+  a.part0 = part0;
+  a.part1 = part1;
+  const int sw = c->p.icd_sweeps;
+  const float *in = phi_in;
+  for (int k = 0; k < sw; ++k) {
+    const bool last = (k == sw - 1);
+    float *out = last ? phi_final : c->ptmp[k & 1];
+    a.in = in;
+    a.out = out;
+    a.copy = last ? copy : nullptr;
+    a.apply_plane = (k == 0) ? apply_plane : 0;
+    DDH_LAUNCH(c, ddh::launch_phiicd(a, sc, c->st));
+    in = out;
+  }
+  return DDH_OK;
+}
+
+enum class Mode { Step, Boot };
+
+// One frame batch (all streams) through the loop body.  y: device frames
+// [S][N][N] of this time step.  Outputs (may be null) are [S][N][N] / [S].
+// Mode::Step: DDH step (Fig. 1).  Mode::Boot: cold start + `iters` iterations
+// with resets every boot_period (bootstrap / static DH-MBIR).
+ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status, Mode mode,
+                     int iters) {
+  const size_t P = c->P;
+  const int cur0 = c->cur;
+  const bool plane = (mode == Mode::Step) && !(c->p.flags & DDH_F_NO_TIPTILT);
+  for (int s0 = 0; s0 < c->S; s0 += c->sc) {
+    const int sc = std::min(c->sc, c->S - s0);
+    const size_t so = (size_t)s0 * P;
+    int cur = cur0;
+    if (mode == Mode::Boot) {  // cold start r = r_min, phi = 0 (Fig. 1, R14)
+      DDH_LAUNCH(c, ddh::launch_fill(c->r + so, (float)c->p.r_min, (size_t)sc * P, c->st));
+      DDH_CK(c, cudaMemsetAsync(c->phi[cur] + so, 0, (size_t)sc * P * sizeof(float), c->st));
+    }
+    StepArgs a = base_args(c, s0, sc);
+    a.y = y + so;
+    a.phi_in = c->phi[cur] + so;
+    a.want_y = 1;
+    a.apply_plane = plane ? 1 : 0;
+    DDH_LAUNCH(c, ddh::launch_k0(a, c->st));
+    for (int it = 0; it < iters; ++it) {
+      const bool first = (it == 0), last = (it == iters - 1);
+      a.phi_in = c->phi[cur] + so;
+      a.apply_plane = (plane && first) ? 1 : 0;
+      if (mode == Mode::Step) {
+        a.warm = first ? 1 : 0;
+        a.oml = (float)(1.0 - c->p.lambda);
+        a.la = (float)(c->p.lambda * c->p.alpha);
+      } else {
+        a.warm = (it % c->p.boot_period == 0) ? 1 : 0;
+        a.oml = 0.f;
+        a.la = (float)c->p.boot_alpha;
+      }
+      a.status = (first && status) ? status + s0 : nullptr;
+      DDH_LAUNCH(c, ddh::launch_k1(a, c->st));
+      DDH_LAUNCH(c, ddh::launch_k2a(a, c->st));
+      ddh_status rs = run_ricd(c, c->rinit, c->q, c->r + so, (last && r_out) ? r_out + so : nullptr, c->part1, sc);
+      if (rs != DDH_OK) return rs;
+      DDH_LAUNCH(c, ddh::launch_k3a(a, c->st));
+      rs = run_phiicd(c, c->phi[cur] + so, c->cc, c->theta, c->phi[cur ^ 1] + so,
+                      (last && phi_out) ? phi_out + so : nullptr, c->part0, c->part1, a.apply_plane, sc);
+      if (rs != DDH_OK) return rs;
+      cur ^= 1;
+    }
+  }
+  c->cur = cur0 ^ (iters & 1);
+  return DDH_OK;
+}
+
+double inv3(const double G[9], double out[9]) {
+  const double a = G[0], b = G[1], cc = G[2], d = G[3], e = G[4], f = G[5], g = G[6], h = G[7], i = G[8];
+  const double A = e * i - f * h, B = -(d * i - f * g), C = d * h - e * g;
+  const double det = a * A + b * B + cc * C;
+  if (!(std::fabs(det) > 0)) return 0.0;
+  out[0] = A / det;
+  out[1] = -(b * i - cc * h) / det;
+  out[2] = (b * f - cc * e) / det;
+  out[3] = B / det;
+  out[4] = (a * i - cc * g) / det;
+  out[5] = -(a * f - cc * d) / det;
+  out[6] = C / det;
+  out[7] = -(a * h - b * g) / det;
+  out[8] = (a * e - b * d) / det;
+  return det;
+}
+
+void free_ctx(ddh_ctx *c) {
+  if (!c) return;
+  void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
+                  c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->pmax, c->rowspan, c->tw,
+                  c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+}
+
+}  // namespace
+
+extern "C" {
+
+ddh_status ddh_default_params(ddh_params *p) {
+  if (!p) return DDH_E_INVAL;
+  std::memset(p, 0, sizeof(*p));
+  p->n = 256;
+  p->streams = 1;
+  p->device = 0;
+  p->aperture_diam = 256.f;
+  p->aperture_mask = nullptr;
+  p->noise_var = 0.1;
+  p->lambda = 0.45;
+  p->alpha = 0.025;
+  p->n_k = 1;
+  p->r_min = 1e-4;
+  p->r_sigma = 0.5;
+  p->r_T = 1.0;
+  p->r_q = 1.2;
+  p->phi_sigma = 0.5;
+  p->icd_sweeps = 1;
+  p->boot_period = 200;
+  p->boot_alpha = 1.0;
+  p->chunk_streams = 0;
+  p->flags = 0;
+  return DDH_OK;
+}
+
+ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
+  if (!pp || !out) return fail(nullptr, DDH_E_INVAL, "ddh_create: NULL argument");
+  *out = nullptr;
+  const ddh_params &p = *pp;
+  if (!valid_n(p.n)) return fail(nullptr, DDH_E_INVAL, "ddh_create: n must be 64, 128, 256, 512 or 1024");
+  if (p.streams < 1) return fail(nullptr, DDH_E_INVAL, "ddh_create: streams must be >= 1");
+  if (!(p.noise_var > 0)) return fail(nullptr, DDH_E_INVAL, "ddh_create: noise_var must be > 0");
+  if (!(p.lambda >= 0 && p.lambda <= 1) || !(p.alpha >= 0 && p.alpha <= 1))
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: lambda and alpha must be in [0,1] (P:189)");
+  if (p.n_k < 1) return fail(nullptr, DDH_E_INVAL, "ddh_create: n_k must be >= 1");
+  if (!(p.r_min > 0)) return fail(nullptr, DDH_E_INVAL, "ddh_create: r_min must be > 0");
+  if (p.r_sigma > 0 && (!(p.r_T > 0) || !(p.r_q >= 1 && p.r_q <= 2)))
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: qGGMRF needs r_T > 0 and r_q in [1,2]");
+  if (p.icd_sweeps < 1) return fail(nullptr, DDH_E_INVAL, "ddh_create: icd_sweeps must be >= 1");
+  if (p.boot_period < 1 || !(p.boot_alpha > 0))
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: boot_period >= 1 and boot_alpha > 0 required");
+  if (p.chunk_streams < 0) return fail(nullptr, DDH_E_INVAL, "ddh_create: chunk_streams must be >= 0");
+  if (!(p.aperture_diam > 0) && !p.aperture_mask)
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture_diam <= 0 requires aperture_mask");
+
+  const int n = p.n;
+  // aperture row intervals and plane normal matrix (RemoveTipTilt)
+  std::vector<int2> span(n);
+  double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  size_t count = 0;
+  for (int i = 0; i < n; ++i) {
+    int lo = n, hi = n;
+    bool seen = false, ended = false;
+    for (int j = 0; j < n; ++j) {
+      bool in;
+      if (p.aperture_diam > 0) {
+        const double di = i - n / 2, dj = j - n / 2, rr = 0.5 * (double)p.aperture_diam;
+        in = di * di + dj * dj < rr * rr;
+      } else {
+        in = p.aperture_mask[(size_t)i * n + j] != 0;
+      }
+      if (in) {
+        if (ended) return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture mask rows must be contiguous runs");
+        if (!seen) lo = j;
+        seen = true;
+        hi = j + 1;
+        const double x = j - n / 2, y = i - n / 2;
+        const double b[3] = {1.0, x, y};
+        for (int u = 0; u < 3; ++u)
+          for (int v = 0; v < 3; ++v) G[u * 3 + v] += b[u] * b[v];
+        ++count;
+      } else if (seen) {
+        ended = true;
+      }
+    }
+    if (!seen) lo = hi = 0;
+    span[i] = make_int2(lo, hi);
+  }
+  double minv[9];
+  if (count < 3 || inv3(G, minv) == 0.0)
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture too small for the tip/tilt plane fit");
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || p.device < 0 || p.device >= ndev)
+    return fail(nullptr, DDH_E_CUDA, "ddh_create: CUDA device not available");
+  if (cudaSetDevice(p.device) != cudaSuccess) return fail(nullptr, DDH_E_CUDA, "ddh_create: cudaSetDevice failed");
+
+  ddh_ctx *c = new ddh_ctx();
+  c->p = p;
+  c->p.aperture_mask = nullptr;  // not retained
+  c->st = (cudaStream_t)cuda_stream;
+  c->n = n;
+  c->S = p.streams;
+  c->P = (size_t)n * n;
+  std::memcpy(c->minv, minv, sizeof(minv));
+  c->nb0 = ddh::k0_blocks(n);
+  c->nb1 = n / ddh::row_block_rows(n);
+  c->strehl_nb = n / ddh::col_block_cols(n);
+  // launch group: keep the per-group workspace (~32 B/px) L2-resident
+  int sc = p.chunk_streams;
+  if (sc <= 0) {
+    const double bytes = 32.0 * (double)c->P;
+    int lim = (int)std::max(1.0, std::floor(48.0 * 1024 * 1024 / bytes));
+    sc = 1;
+    while (sc * 2 <= lim) sc *= 2;
+  }
+  c->sc = std::min(sc, c->S);
+  const size_t S = c->S, P = c->P, SC = c->sc;
+
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) {
+    if (e == cudaSuccess) e = r;
+  };
+  A(dalloc(&c->r, S * P));
+  A(dalloc(&c->phi[0], S * P));
+  A(dalloc(&c->phi[1], S * P));
+  A(dalloc(&c->cbuf, SC * P));
+  A(dalloc(&c->rinit, SC * P));
+  A(dalloc(&c->q, SC * P));
+  A(dalloc(&c->cc, SC * P));
+  A(dalloc(&c->theta, SC * P));
+  if (p.icd_sweeps > 1) {
+    A(dalloc(&c->rtmp[0], SC * P));
+    A(dalloc(&c->rtmp[1], SC * P));
+    A(dalloc(&c->ptmp[0], SC * P));
+    A(dalloc(&c->ptmp[1], SC * P));
+  }
+  A(dalloc(&c->part0, SC * c->nb0 * 5));
+  A(dalloc(&c->part1, SC * c->nb1));
+  A(dalloc(&c->pmax, SC * c->strehl_nb));
+  A(dalloc(&c->rowspan, (size_t)n));
+  A(dalloc(&c->tw, (size_t)n));
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? DDH_E_NOMEM : DDH_E_CUDA,
+                std::string("ddh_create: allocation failed: ") + cudaGetErrorString(e));
+  }
+  // twiddles W_N^m = e^{-2 pi i m/N}, FP64 -> FP32
+  std::vector<float2> tw(n);
+  for (int m = 0; m < n; ++m) {
+    const double ang = -2.0 * M_PI * (double)m / (double)n;
+    tw[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+  }
+  A(cudaMemcpy(c->tw, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+  A(cudaMemcpy(c->rowspan, span.data(), n * sizeof(int2), cudaMemcpyHostToDevice));
+  A(ddh::init_kernels(n));
+  // state: n = 0, r = r_min, phi = 0 (Fig. 1; R14)
+  A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));
+  A(cudaMemsetAsync(c->phi[0], 0, S * P * sizeof(float), c->st));
+  A(cudaMemsetAsync(c->phi[1], 0, S * P * sizeof(float), c->st));
+  A(cudaStreamSynchronize(c->st));
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return fail(nullptr, DDH_E_CUDA, std::string("ddh_create: ") + cudaGetErrorString(e));
+  }
+  c->launches = 1;
+  // Strehl denominator max |F_c^{-1}(a)|^2 ("back-propagation through a vacuum")
+  {
+    StrehlArgs s{};
+    s.n = n;
+    s.nb = c->strehl_nb;
+    s.phi_hat = nullptr;
+    s.phi_true = nullptr;
+    s.part0 = c->part0;
+    s.nb0 = c->nb0;
+    std::memcpy(s.minv, c->minv, sizeof(s.minv));
+    s.rowspan = c->rowspan;
+    s.tw = c->tw;
+    s.cbuf = c->cbuf;
+    s.pmax = c->pmax;
+    A(ddh::launch_strehl(s, 1, c->st));
+    std::vector<float> pm(c->strehl_nb);
+    A(cudaMemcpyAsync(pm.data(), c->pmax, pm.size() * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    A(cudaStreamSynchronize(c->st));
+    double m = 0;
+    for (float v : pm) m = std::max(m, (double)v);
+    c->strehl_den = m;
+    c->launches += 2;
+  }
+  if (e != cudaSuccess) {
+    free_ctx(c);
+    return fail(nullptr, DDH_E_CUDA, std::string("ddh_create: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return DDH_OK;
+}
+
+ddh_status ddh_destroy(ddh_ctx *c) {
+  if (!c) return DDH_E_INVAL;
+  cudaSetDevice(c->p.device);
+  cudaStreamSynchronize(c->st);
+  free_ctx(c);
+  return DDH_OK;
+}
+
+ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *status) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (k_b < 0 || (!y0 && k_b > 0)) return fail(c, DDH_E_INVAL, "ddh_bootstrap: bad arguments");
+  if (k_b == 0) return DDH_OK;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  s = run_frame(c, (const float2 *)y0, nullptr, nullptr, status, Mode::Boot, k_b);
+  if (s != DDH_OK) return s;
+  c->frame += 1;
+  return DDH_OK;
+}
+
+ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float *r_out, uint8_t *status) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (T < 0 || (!y && T > 0)) return fail(c, DDH_E_INVAL, "ddh_step: bad arguments");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  const size_t fs = (size_t)c->S * c->P;
+  for (int t = 0; t < T; ++t) {
+    s = run_frame(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
+                  r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr, Mode::Step,
+                  c->p.n_k);
+    if (s != DDH_OK) return s;
+    c->frame += 1;
+  }
+  return DDH_OK;
+}
+
+ddh_status ddh_static(ddh_ctx *c, const void *y, int32_t T, int32_t iters, float *phi_out, float *r_out,
+                      uint8_t *status) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (T < 0 || iters < 1 || (!y && T > 0)) return fail(c, DDH_E_INVAL, "ddh_static: bad arguments");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  const size_t fs = (size_t)c->S * c->P;
+  for (int t = 0; t < T; ++t) {
+    s = run_frame(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
+                  r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr, Mode::Boot,
+                  iters);
+    if (s != DDH_OK) return s;
+    c->frame += 1;
+  }
+  return DDH_OK;
+}
+
+ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
+                         uint8_t *status) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (T < 0 || (!y_host && T > 0)) return fail(c, DDH_E_INVAL, "ddh_step_host: bad arguments");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  const size_t fs = (size_t)c->S * c->P;
+  if (!c->y_stage) {
+    cudaError_t e = dalloc(&c->y_stage, fs);
+    if (e == cudaSuccess) e = dalloc(&c->phi_stage, fs);
+    if (e == cudaSuccess) e = dalloc(&c->r_stage, fs);
+    if (e == cudaSuccess) e = dalloc(&c->status_stage, (size_t)c->S);
+    if (e != cudaSuccess) return fail(c, DDH_E_NOMEM, "ddh_step_host: staging allocation failed");
+  }
+  for (int t = 0; t < T; ++t) {
+    DDH_CK(c, cudaMemcpyAsync(c->y_stage, (const float2 *)y_host + t * fs, fs * sizeof(float2),
+                              cudaMemcpyHostToDevice, c->st));
+    s = run_frame(c, c->y_stage, phi_out ? c->phi_stage : nullptr, r_out ? c->r_stage : nullptr,
+                  status ? c->status_stage : nullptr, Mode::Step, c->p.n_k);
+    if (s != DDH_OK) return s;
+    c->frame += 1;
+    if (phi_out)
+      DDH_CK(c, cudaMemcpyAsync(phi_out + t * fs, c->phi_stage, fs * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    if (r_out)
+      DDH_CK(c, cudaMemcpyAsync(r_out + t * fs, c->r_stage, fs * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+    if (status)
+      DDH_CK(c, cudaMemcpyAsync(status + (size_t)t * c->S, c->status_stage, c->S, cudaMemcpyDeviceToHost, c->st));
+  }
+  DDH_CK(c, cudaStreamSynchronize(c->st));
+  return DDH_OK;
+}
+
+ddh_status ddh_get_state(ddh_ctx *c, float *r, float *phi, int64_t *frame_index) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  const size_t bytes = (size_t)c->S * c->P * sizeof(float);
+  if (r) DDH_CK(c, cudaMemcpyAsync(r, c->r, bytes, cudaMemcpyDeviceToDevice, c->st));
+  if (phi) DDH_CK(c, cudaMemcpyAsync(phi, c->phi[c->cur], bytes, cudaMemcpyDeviceToDevice, c->st));
+  if (frame_index) *frame_index = c->frame;
+  return DDH_OK;
+}
+
+ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t frame_index) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  const size_t bytes = (size_t)c->S * c->P * sizeof(float);
+  if (r) DDH_CK(c, cudaMemcpyAsync(c->r, r, bytes, cudaMemcpyDeviceToDevice, c->st));
+  if (phi) DDH_CK(c, cudaMemcpyAsync(c->phi[c->cur], phi, bytes, cudaMemcpyDeviceToDevice, c->st));
+  c->frame = frame_index;
+  return DDH_OK;
+}
+
+ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, double *out) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!phi_hat || !phi_true || !out))) return fail(c, DDH_E_INVAL, "ddh_strehl: bad arguments");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  std::vector<float> pm((size_t)c->sc * c->strehl_nb);
+  for (int b0 = 0; b0 < B; b0 += c->sc) {
+    const int bn = std::min(c->sc, B - b0);
+    const size_t off = (size_t)b0 * c->P;
+    StepArgs a = base_args(c, 0, bn);
+    a.want_y = 0;
+    a.apply_plane = 1;
+    a.phi_in = phi_hat + off;
+    a.phi_sub = phi_true + off;
+    DDH_LAUNCH(c, ddh::launch_k0(a, c->st));
+    StrehlArgs sa{};
+    sa.n = c->n;
+    sa.nb = c->strehl_nb;
+    sa.phi_hat = phi_hat + off;
+    sa.phi_true = phi_true + off;
+    sa.part0 = c->part0;
+    sa.nb0 = c->nb0;
+    std::memcpy(sa.minv, c->minv, sizeof(sa.minv));
+    sa.rowspan = c->rowspan;
+    sa.tw = c->tw;
+    sa.cbuf = c->cbuf;
+    sa.pmax = c->pmax;
+    DDH_CK(c, ddh::launch_strehl(sa, bn, c->st));
+    c->launches += 2;
+    DDH_CK(c, cudaMemcpyAsync(pm.data(), c->pmax, (size_t)bn * c->strehl_nb * sizeof(float),
+                              cudaMemcpyDeviceToHost, c->st));
+    DDH_CK(c, cudaStreamSynchronize(c->st));
+    for (int b = 0; b < bn; ++b) {
+      double m = 0;
+      for (int k = 0; k < c->strehl_nb; ++k) m = std::max(m, (double)pm[(size_t)b * c->strehl_nb + k]);
+      out[b0 + b] = m / c->strehl_den;
+    }
+  }
+  return DDH_OK;
+}
+
+ddh_status ddh_sync(ddh_ctx *c) {
+  if (!c) return DDH_E_INVAL;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  DDH_CK(c, cudaStreamSynchronize(c->st));
+  return c->sticky ? DDH_E_STATE : DDH_OK;
+}
+
+const char *ddh_last_error(const ddh_ctx *c) {
+  if (c) return c->err.c_str();
+  std::lock_guard<std::mutex> lk(g_err_mu);
+  return g_create_err.c_str();
+}
+
+uint64_t ddh_kernel_launches(const ddh_ctx *c) { return c ? c->launches : 0; }
+
+int64_t ddh_frame_index(const ddh_ctx *c) { return c ? c->frame : -1; }
+
+ddh_status ddh_test_fft2c(ddh_ctx *c, const void *in, void *out, int32_t B, int32_t inverse) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!in || !out))) return fail(c, DDH_E_INVAL, "ddh_test_fft2c: bad arguments");
+  if (B == 0) return DDH_OK;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  DDH_CK(c, ddh::launch_test_fft2c(c->n, (const float2 *)in, (float2 *)out, B, inverse, c->tw, c->st));
+  c->launches += 2;
+  return DDH_OK;
+}
+
+ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t B, float *r_out) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!r_in || !q || !r_out))) return fail(c, DDH_E_INVAL, "ddh_test_ricd: bad arguments");
+  if (B == 0) return DDH_OK;
+  if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_ricd: B > chunk with sweeps > 1");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  return run_ricd(c, r_in, q, r_out, nullptr, nullptr, B);
+}
+
+ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta, int32_t B,
+                           float *phi_out) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!phi_in || !cc || !theta || !phi_out)))
+    return fail(c, DDH_E_INVAL, "ddh_test_phiicd: bad arguments");
+  if (B == 0) return DDH_OK;
+  if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_phiicd: B > chunk with sweeps > 1");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  return run_phiicd(c, phi_in, cc, theta, phi_out, nullptr, nullptr, nullptr, 0, B);
+}
+
+}  // extern "C"

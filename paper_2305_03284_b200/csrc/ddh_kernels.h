@@ -1,0 +1,99 @@
+// ddh_kernels.h -- internal interface between the host library (ddh_api.cpp)
+// and the sm_100a kernels (ddh_kernels.cu).  Not part of the public ABI.
+//
+// Kernel map of one EM iteration:
+//   K0  k0_stats     per-stream sums of y (Eq. 4 mean) and of the phase over
+//                    the aperture (RemoveTipTilt normal equations)
+//   K1  k1_rows_fwd  Normalize-apply (y - mu), plane removal, aperture,
+//                    e^{-j phi}, chi, forward row DFT; partial ||y - mu||^2
+//   K2a k2a_cols     forward column DFT -> u = A^H y (Eq. 3 back-projection =
+//                    first E-step transform, R13); Eq. 3 warm start; E-step;
+//                    chi mu -> inverse column DFT
+//   K2b k2b_ricd     colour-ordered qGGMRF r-ICD (4 colours, halo 4, periodic)
+//   K3a k3a_rows_inv inverse row DFT -> f = F_c^{-1} mu; c = (2/s2) a |y||f|,
+//                    theta = arg(y conj f)
+//   K3b k3b_phiicd   colour-ordered GMRF phi-ICD (4 colours, halo 4, free edge)
+// State pointers passed to kernels are pre-offset to the first stream of the
+// launch group ("chunk"); blockIdx.{y|z} is the stream within the chunk.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ddh {
+
+struct StepArgs {
+  int n;        // N
+  int sc;       // streams in this launch group
+  int nb0;      // K0 blocks per stream
+  int nb1;      // K1 / K3a row blocks per stream
+  const float2 *y;        // frame batch for this chunk: [sc][N][N]
+  const float *phi_sub;   // K0 only: subtract this field (Strehl residual), else null
+  float *r_state;         // [sc][N][N]
+  const float *phi_in;    // [sc][N][N]
+  float2 *cbuf;           // [sc][N][N] spectrum scratch (row DFT out / col IDFT out)
+  float *rinit, *q;       // [sc][N][N] E-step outputs (r after Eq. 3, second moment)
+  float *cc, *theta;      // [sc][N][N] phase-correlation terms
+  double *part0;          // [sc][nb0][5]: sum re y, sum im y, sum phi, sum phi x, sum phi y
+  double *part1;          // [sc][nb1]: sum |y - mu|^2
+  const int2 *rowspan;    // [N] aperture row intervals [lo, hi)
+  const float2 *tw;       // [N] twiddles e^{-2 pi i m / N}
+  uint8_t *status;        // [sc] degenerate-frame flags or null (written by K2a)
+  int want_y;             // K0: accumulate y sums
+  int apply_plane;        // K0: accumulate plane sums; K1/K3b: subtract the plane
+  int warm;               // K2a: apply Eq. 3 (or a bootstrap reset)
+  float oml, la;          // K2a: r0 = max(oml r + la |u|^2, r_min)
+  float s2, r_min;        // noise variance, r floor
+  float P;                // N*N
+  double minv[9];         // inverse of the aperture plane normal matrix
+};
+
+struct IcdArgs {
+  int n;
+  const float *in;       // r_in or phi_in [sc][N][N]
+  const float *q;        // r-ICD: second moment; phi-ICD: c
+  const float *theta;    // phi-ICD only
+  float *out;            // [sc][N][N]
+  float *copy;           // optional second output (user buffer) or null
+  const double *part0;   // plane sums (phi-ICD with apply_plane) or null
+  const double *part1;   // ||y - mu||^2 partials for degenerate detection, or null
+  int nb0, nb1;
+  int apply_plane;
+  double minv[9];
+  int prior;             // prior enabled
+  float r_min;
+  float b0;              // r: 1/(2 sig_r^2) ; phi: 1/sig_phi^2
+  float inv_Tsig;        // r: 1/(T sig_r)
+  float two_minus_q;     // r: 2 - q
+};
+
+struct StrehlArgs {
+  int n, nb;             // nb: column blocks per field (partial maxima per field)
+  const float *phi_hat, *phi_true;  // [B][N][N] (phi_hat null: psi = 0)
+  const double *part0;   // plane sums of psi [B][nb0][5]
+  int nb0;
+  double minv[9];
+  const int2 *rowspan;
+  const float2 *tw;
+  float2 *cbuf;          // [B][N][N]
+  float *pmax;           // [B][nb]
+};
+
+// Returns the first launch error (cudaGetLastError) of the sequence.
+cudaError_t init_kernels(int n);
+int row_block_rows(int n);    // H rows per K1/K3a CTA
+int col_block_cols(int n);    // W columns per K2a CTA
+int icd_tile(int n);          // ICD tile side
+int k0_blocks(int n);         // K0 blocks per stream
+
+cudaError_t launch_k0(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_k1(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_k2a(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_k3a(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_ricd(const IcdArgs &a, int sc, cudaStream_t st);
+cudaError_t launch_phiicd(const IcdArgs &a, int sc, cudaStream_t st);
+cudaError_t launch_fill(float *p, float v, size_t count, cudaStream_t st);
+cudaError_t launch_strehl(const StrehlArgs &a, int B, cudaStream_t st);
+cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
+                              cudaStream_t st);
+
+}  // namespace ddh

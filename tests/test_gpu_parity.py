@@ -1,0 +1,424 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on
+the same seeded synthetic frames (-m gpu).
+
+Tolerances (north_star):
+  * per step, from identical FP32 state: max piston-removed wrapped |dphi|
+    over the aperture <= 1e-3 rad and relative L2 r error <= 1e-4, excluding
+    (and counting) pixels where the oracle's r-surrogate has two far-apart
+    candidates within 1e-6 of each other and their 5x5 neighbourhood
+    ("several results are correct");
+  * end to end: per-frame Strehl within 0.01 absolute;
+  * stages: FFT relative L2 <= 3e-6 (FP32 floor ~ eps log2 N), ICDs <= 1e-5.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle.ddh_oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2305_03284_b200 import build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def DDH(*a, **k):
+    from paper_2305_03284_b200 import DDH as _D
+    return _D(*a, **k)
+
+
+def crandn(g, *shape):
+    return (g.standard_normal(shape) + 1j * g.standard_normal(shape)).astype(np.complex64)
+
+
+def oracle_params(n, diam=None, **kw):
+    p = O.OracleParams(n=n, aperture_diam=float(n if diam is None else diam))
+    for k, v in kw.items():
+        setattr(p, k, v)
+    return p
+
+
+def gpu_kwargs(p: O.OracleParams):
+    return dict(noise_var=p.noise_var, lam=p.lam, alpha=p.alpha, n_k=p.n_k, r_min=p.r_min, r_sigma=p.r_sigma,
+                r_T=p.r_T, r_q=p.r_q, phi_sigma=p.phi_sigma, icd_sweeps=p.icd_sweeps, boot_period=p.boot_period,
+                boot_alpha=p.boot_alpha, flags=0 if p.tiptilt else 1)
+
+
+def tie_mask(gaps, thr=1e-6, rad=2):
+    m = gaps < thr
+    out = m.copy()
+    for di in range(-rad, rad + 1):
+        for dj in range(-rad, rad + 1):
+            out |= np.roll(np.roll(m, di, 0), dj, 1)
+    return out
+
+
+def phi_err(phi_g, phi_o, a):
+    d = np.angle(np.exp(1j * (phi_g.astype(np.float64) - phi_o)))
+    d = d[a > 0]
+    d = np.angle(np.exp(1j * (d - np.angle(np.mean(np.exp(1j * d))))))
+    return float(np.max(np.abs(d)))
+
+
+def r_err(r_g, r_o, excl):
+    keep = ~excl
+    return float(np.linalg.norm((r_g - r_o)[keep]) / np.linalg.norm(r_o[keep]))
+
+
+def frames(n, S, T, cfg="c1", **over):
+    c = dict(synth.CONFIGS[cfg], n=n, diam=n, **over)
+    y, ph = synth.make_batch(c, streams=S, frames=T, workers=1)
+    return y, ph, c
+
+
+# ------------------------------------------------------------------ stages
+
+
+@pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
+def test_fft2c_parity(n):
+    g = np.random.default_rng(n)
+    B = 3 if n <= 256 else 2
+    x = crandn(g, B, n, n)
+    ctx = DDH(n, 1)
+    xt = torch.from_numpy(x).to(DEV)
+    for inv in (False, True):
+        out = ctx.test_fft2c(xt, inverse=inv).cpu().numpy()
+        for b in range(B):
+            ref = O.ifft2c(x[b].astype(np.complex128)) if inv else O.fft2c(x[b].astype(np.complex128))
+            err = np.linalg.norm(out[b] - ref) / np.linalg.norm(ref)
+            assert err < 3e-6, (n, inv, err)
+
+
+def _realistic_rq(n, seed):
+    """(r, q) from an oracle E-step on a synthetic frame (FP32-rounded)."""
+    y, _, c = frames(n, 1, 1, "c1")
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0))
+    a = O.aperture_of(p)
+    g = np.random.default_rng(seed)
+    r = (g.random((n, n)) * 0.5 + 0.01)
+    u = O.adjoint(np.zeros((n, n)), O.normalize(y[0, 0].astype(np.complex128)), a)
+    r = O.warm_start(r, u, 0.45, 0.025, 1e-4)
+    _, _, q = O.e_step(u, r, p.noise_var)
+    return r.astype(np.float32), q.astype(np.float32), p
+
+
+@pytest.mark.parametrize("n,kind", [(64, "random"), (256, "random"), (128, "realistic"), (256, "realistic")])
+def test_ricd_stage_parity(n, kind):
+    g = np.random.default_rng(7 + n)
+    B = 2
+    if kind == "random":
+        r = (g.random((B, n, n)) * 2 + 1e-3).astype(np.float32)
+        q = (g.random((B, n, n)) * 2 + 1e-4).astype(np.float32)
+        p = oracle_params(n)
+    else:
+        rq = [_realistic_rq(n, s) for s in range(B)]
+        r = np.stack([x[0] for x in rq])
+        q = np.stack([x[1] for x in rq])
+        p = rq[0][2]
+    ctx = DDH(n, B, **gpu_kwargs(p))
+    out = ctx.test_ricd(torch.from_numpy(r).to(DEV), torch.from_numpy(q).to(DEV)).cpu().numpy()
+    for b in range(B):
+        gaps = np.full((n, n), np.inf)
+        ref = O.r_icd(r[b].astype(np.float64), q[b].astype(np.float64), p, gaps)
+        excl = tie_mask(gaps)
+        assert excl.mean() < 0.01
+        e = r_err(out[b], ref, excl)
+        assert e < 1e-5, (b, e, int((gaps < 1e-6).sum()))
+        rel = np.abs(out[b] - ref)[~excl] / np.abs(ref[~excl])
+        assert rel.max() < 1e-3
+
+
+def test_ricd_prior_off_is_clamp():
+    n = 64
+    g = np.random.default_rng(3)
+    r = g.random((1, n, n)).astype(np.float32)
+    q = (g.random((1, n, n)) * 1e-3).astype(np.float32)
+    ctx = DDH(n, 1, r_sigma=0.0)
+    out = ctx.test_ricd(torch.from_numpy(r).to(DEV), torch.from_numpy(q).to(DEV)).cpu().numpy()
+    assert np.array_equal(out[0], np.maximum(q[0], np.float32(1e-4)))
+
+
+@pytest.mark.parametrize("n,prior", [(64, True), (256, True), (128, False)])
+def test_phiicd_stage_parity(n, prior):
+    g = np.random.default_rng(11 + n)
+    B = 2
+    phi = (g.standard_normal((B, n, n)) * 2).astype(np.float32)
+    c = (g.random((B, n, n)) * 5).astype(np.float32)
+    c[:, :, : n // 8] = 0.0  # pixels outside an aperture: prior only
+    th = g.uniform(-math.pi, math.pi, (B, n, n)).astype(np.float32)
+    p = oracle_params(n, phi_sigma=0.5 if prior else 0.0)
+    ctx = DDH(n, B, **gpu_kwargs(p))
+    out = ctx.test_phiicd(*(torch.from_numpy(v).to(DEV) for v in (phi, c, th))).cpu().numpy()
+    for b in range(B):
+        ref = O.phi_icd(phi[b].astype(np.float64), c[b].astype(np.float64), th[b].astype(np.float64), p)
+        d = np.angle(np.exp(1j * (out[b] - ref)))
+        assert np.max(np.abs(d)) < 2e-4, np.max(np.abs(d))
+
+
+# -------------------------------------------------------------- one step
+
+
+def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, **frame_over):
+    y, ph, c = frames(n, S, seed_frames, cfg, **frame_over)
+    a = O.aperture_of(p)
+    # a realistic state: oracle bootstrap on frame 0, rounded to FP32
+    orc = O.DDHOracle(p, S)
+    st = orc.bootstrap(y[0], pre_boot)
+    assert not st.any()
+    r32 = orc.r.astype(np.float32)
+    p32 = orc.phi.astype(np.float32)
+    orc.set_state(r32, p32, 1)
+    ctx = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(p))
+    ctx.set_state(torch.from_numpy(r32).to(DEV), torch.from_numpy(p32).to(DEV), 1)
+    yt = torch.from_numpy(y[1:2]).to(DEV)
+    phi_o = torch.empty((1, S, n, n), device=DEV)
+    r_o = torch.empty_like(phi_o)
+    status = torch.empty((1, S), dtype=torch.uint8, device=DEV)
+    ctx.step(yt, phi_o, r_o, status)
+    torch.cuda.synchronize()
+    phi_g = phi_o.cpu().numpy()[0]
+    r_g = r_o.cpu().numpy()[0]
+    assert status.cpu().numpy().sum() == 0
+    # the state matches the per-frame outputs
+    r_s, phi_s, fi = ctx.get_state()
+    assert fi == 2
+    assert np.array_equal(r_s.cpu().numpy(), r_g) and np.array_equal(phi_s.cpu().numpy(), phi_g)
+    worst = (0.0, 0.0)
+    for s in range(S):
+        gaps = np.full((n, n), np.inf)
+        r_ref, phi_ref, st = O.ddh_step(orc.r[s], orc.phi[s], y[1, s], p, a, gaps)
+        excl = tie_mask(gaps)
+        ep = phi_err(phi_g[s], phi_ref, a)
+        er = r_err(r_g[s], r_ref, excl)
+        assert ep <= 1e-3, (s, ep)
+        assert er <= 1e-4, (s, er, int((gaps < 1e-6).sum()))
+        worst = (max(worst[0], ep), max(worst[1], er))
+    return worst
+
+
+@pytest.mark.parametrize("n,S,chunk", [(64, 2, 0), (128, 3, 2), (256, 2, 0)])
+def test_step_parity_priors_on(n, S, chunk):
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0))
+    _step_parity(n, S, p, chunk=chunk)
+
+
+def test_step_parity_priors_off():
+    n = 64
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0), r_sigma=0.0, phi_sigma=0.0)
+    _step_parity(n, 2, p)
+
+
+def test_step_parity_nk2_two_sweeps_no_tiptilt():
+    n = 128
+    p = oracle_params(n, noise_var=0.2, n_k=2, icd_sweeps=2, tiptilt=False)
+    _step_parity(n, 2, p)
+
+
+def test_step_parity_masked_aperture():
+    n = 64
+    p = oracle_params(n, diam=50, noise_var=0.15)
+    _step_parity(n, 2, p)
+
+
+# -------------------------------------------------- bootstrap and static
+
+
+def test_bootstrap_and_static_parity():
+    n, S = 64, 2
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0), boot_period=3)
+    y, _, _ = frames(n, S, 2)
+    a = O.aperture_of(p)
+    ctx = DDH(n, S, **gpu_kwargs(p))
+    ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), 5)
+    r_g, phi_g, fi = ctx.get_state()
+    assert fi == 1
+    for s in range(S):
+        r_ref, phi_ref, _ = O.bootstrap(y[0, s], p, 5, a)
+        # 5 chained iterations from a cold start: FP32 drift stays far inside the per-step bar
+        assert phi_err(phi_g[s].cpu().numpy(), phi_ref, a) < 1e-3
+        assert r_err(r_g[s].cpu().numpy(), r_ref, np.zeros((n, n), bool)) < 1e-3
+    phi_o = torch.empty((2, S, n, n), device=DEV)
+    ctx.static(torch.from_numpy(y).to(DEV), 4, phi_out=phi_o)
+    for t in range(2):
+        for s in range(S):
+            _, phi_ref, _ = O.static_dhmbir(y[t, s], p, 4, a)
+            assert phi_err(phi_o[t, s].cpu().numpy(), phi_ref, a) < 1e-3
+
+
+# ---------------------------------------------------------- end to end
+
+
+def test_end_to_end_c1_strehl_parity():
+    """BASELINE config 1: 64x64, bootstrap then 1 EM iteration per frame,
+    16 frames; both sides run free from their own state."""
+    cfg = synth.CONFIGS["c1"]
+    n, T = cfg["n"], cfg["frames"]
+    y, ph, _ = frames(n, 1, T)
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, cfg["snr_db"]))
+    a = O.aperture_of(p)
+    kb = cfg["k_b"]
+    ctx = DDH(n, 1, **gpu_kwargs(p))
+    ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), kb)
+    phi_o = torch.empty((T - 1, 1, n, n), device=DEV)
+    ctx.step(torch.from_numpy(np.ascontiguousarray(y[1:])).to(DEV), phi_o)
+    strehl_gpu_api = ctx.strehl(phi_o[:, 0].contiguous(), torch.from_numpy(ph[1:, 0]).to(DEV))
+    phi_g = phi_o.cpu().numpy()[:, 0]
+    r, phi, _ = O.bootstrap(y[0, 0], p, kb, a)
+    worst = 0.0
+    for t in range(1, T):
+        r, phi, _ = O.ddh_step(r, phi, y[t, 0], p, a)
+        s_ref = O.strehl(phi, ph[t, 0], a)
+        s_gpu = O.strehl(phi_g[t - 1], ph[t, 0], a)
+        worst = max(worst, abs(s_ref - s_gpu))
+        assert abs(s_gpu - strehl_gpu_api[t - 1]) < 1e-5
+    assert worst <= 0.01, worst
+
+
+def test_strehl_parity():
+    n = 256
+    a = O.aperture(n, n)
+    g = np.random.default_rng(5)
+    B = 3
+    hat = np.stack([synth.screen_from_coeffs(synth.screen_coeffs(n, n, n / 3.0, g)) for _ in range(B)]).astype(np.float32)
+    tru = (g.standard_normal((B, n, n)) * 0.1).astype(np.float32)
+    ctx = DDH(n, 1)
+    out = ctx.strehl(torch.from_numpy(hat).to(DEV), torch.from_numpy(tru).to(DEV))
+    for b in range(B):
+        assert abs(out[b] - O.strehl(hat[b], tru[b], a)) < 1e-5
+    zero = torch.zeros((1, n, n), device=DEV)
+    assert abs(ctx.strehl(zero, zero)[0] - 1.0) < 1e-6
+
+
+# ----------------------------------------------- full BASELINE sizes, sampled
+
+
+def test_c3_full_size_sampled_streams():
+    """BASELINE config 3 shape (256^2, 64 streams, launch groups as bench.py):
+    one cold-start step on all 64 streams; streams 0 and 63 checked against
+    the oracle."""
+    cfg = synth.CONFIGS["c3"]
+    n, S = cfg["n"], cfg["streams"]
+    y, _ = synth.make_batch(cfg, streams=S, frames=1, want_phi=False)
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, cfg["snr_db"]))
+    a = O.aperture_of(p)
+    ctx = DDH(n, S, **gpu_kwargs(p))
+    phi_o = torch.empty((1, S, n, n), device=DEV)
+    r_o = torch.empty_like(phi_o)
+    ctx.step(torch.from_numpy(y).to(DEV), phi_o, r_o)
+    for s in (0, S - 1):
+        gaps = np.full((n, n), np.inf)
+        r_ref, phi_ref, _ = O.ddh_step(np.full((n, n), p.r_min), np.zeros((n, n)), y[0, s], p, a, gaps)
+        assert phi_err(phi_o[0, s].cpu().numpy(), phi_ref, a) <= 1e-3
+        assert r_err(r_o[0, s].cpu().numpy(), r_ref, tie_mask(gaps)) <= 1e-4
+
+
+@pytest.mark.parametrize("cfgname,S", [("c4", 6), ("c5", 1)])
+def test_large_grid_sampled(cfgname, S):
+    cfg = synth.CONFIGS[cfgname]
+    n = cfg["n"]
+    y, _ = synth.make_batch(cfg, streams=S, frames=1, want_phi=False, workers=1)
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, cfg["snr_db"]))
+    a = O.aperture_of(p)
+    ctx = DDH(n, S, **gpu_kwargs(p))
+    phi_o = torch.empty((1, S, n, n), device=DEV)
+    r_o = torch.empty_like(phi_o)
+    ctx.step(torch.from_numpy(y).to(DEV), phi_o, r_o)
+    s = S - 1
+    gaps = np.full((n, n), np.inf)
+    r_ref, phi_ref, _ = O.ddh_step(np.full((n, n), p.r_min), np.zeros((n, n)), y[0, s], p, a, gaps)
+    assert phi_err(phi_o[0, s].cpu().numpy(), phi_ref, a) <= 1e-3
+    assert r_err(r_o[0, s].cpu().numpy(), r_ref, tie_mask(gaps)) <= 1e-4
+
+
+# ------------------------------------------------ edge cases / invariants
+
+
+def test_degenerate_frame_keeps_state():
+    n, S = 64, 2
+    y, _, _ = frames(n, S, 2)
+    ctx = DDH(n, S, noise_var=0.1)
+    ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), 3)
+    r0, phi0, _ = ctx.get_state()
+    yy = y[1:2].copy()
+    yy[0, 1] = 0.7 - 0.2j  # constant frame on stream 1
+    status = torch.empty((1, S), dtype=torch.uint8, device=DEV)
+    ctx.step(torch.from_numpy(yy).to(DEV), status=status)
+    r1, phi1, fi = ctx.get_state()
+    assert status.cpu().tolist() == [[0, 1]]
+    assert torch.equal(r1[1], r0[1]) and torch.equal(phi1[1], phi0[1])
+    assert not torch.equal(phi1[0], phi0[0])
+    assert fi == 2
+
+
+def test_state_continuity_bit_exact():
+    n, S = 64, 2
+    y, _, _ = frames(n, S, 6)
+    yt = torch.from_numpy(y).to(DEV)
+    a = DDH(n, S, noise_var=0.1)
+    b = DDH(n, S, noise_var=0.1)
+    pa = torch.empty((6, S, n, n), device=DEV)
+    pb = torch.empty_like(pa)
+    a.step(yt, pa)
+    b.step(yt[:2].contiguous(), pb[:2])
+    b.step(yt[2:].contiguous(), pb[2:])
+    assert torch.equal(pa, pb)
+
+
+def test_sharding_and_launch_groups_bit_exact():
+    """Streams are independent: the per-stream results do not depend on how
+    streams are grouped into launches or split over contexts (G-GPU sharding
+    emulated by two ctxs on one device)."""
+    n, S = 128, 4
+    y, _, _ = frames(n, S, 3)
+    yt = torch.from_numpy(y).to(DEV)
+    outs = []
+    for chunk in (1, 4):
+        ctx = DDH(n, S, noise_var=0.1, chunk_streams=chunk)
+        po = torch.empty((3, S, n, n), device=DEV)
+        ctx.step(yt, po)
+        outs.append(po)
+    assert torch.equal(outs[0], outs[1])
+    halves = []
+    for h in range(2):
+        ctx = DDH(n, 2, noise_var=0.1)
+        po = torch.empty((3, 2, n, n), device=DEV)
+        ctx.step(yt[:, 2 * h:2 * h + 2].contiguous(), po)
+        halves.append(po)
+    assert torch.equal(torch.cat(halves, 1), outs[0])
+
+
+def test_step_host_matches_device_path():
+    n, S, T = 64, 2, 3
+    y, _, _ = frames(n, S, T)
+    a = DDH(n, S, noise_var=0.1)
+    b = DDH(n, S, noise_var=0.1)
+    pa = torch.empty((T, S, n, n), device=DEV)
+    a.step(torch.from_numpy(y).to(DEV), pa)
+    yh = torch.from_numpy(y).pin_memory()
+    pb = torch.empty((T, S, n, n)).pin_memory()
+    rb = torch.empty((T, S, n, n)).pin_memory()
+    sb = torch.empty((T, S), dtype=torch.uint8).pin_memory()
+    b.step_host(yh, pb, rb, sb)
+    assert torch.equal(pa.cpu(), pb)
+    assert sb.sum().item() == 0
+
+
+def test_kernel_launch_count_and_empty_call():
+    n, S = 64, 1
+    ctx = DDH(n, S, noise_var=0.1)
+    l0 = ctx.kernel_launches
+    ctx.step(torch.empty((0, S, n, n), dtype=torch.complex64, device=DEV))
+    assert ctx.kernel_launches == l0
+    y, _, _ = frames(n, S, 1)
+    ctx.step(torch.from_numpy(y).to(DEV))
+    assert ctx.kernel_launches - l0 == 6  # K0 K1 K2a K2b K3a K3b
