@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""bench.py -- DDH-MBIR hot-path benchmark (contract: DESIGN.md "Measurement").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+Workload (BASELINE.json configs[2], "c3"): 256x256 complex64 DH frames, 64
+independent streams per GPU (distinct seeds across GPUs), 1 EM iteration per
+time step, frozen-flow Kolmogorov phase, blurred-uniform reflectance, SNR 5 dB.
+A STEP is one time step of all 64 streams of a GPU: the whole hot path (K0 ..
+K3b) over one frame batch (64 frames, 32 MiB).  100
+distinct frame batches (3.2 GiB > the 126 MB L2) are staged in HBM before
+timing and cycled; consecutive steps never re-read a batch from L2.
+
+value   = frames/s of the whole job: K * 64 * N_gpus / max-over-ranks device time
+latency = configs[1] ("c2", 1 stream): per-frame device latency p50/p99
+e2e     = the same metric through the host-buffer C-ABI call (ddh_step_host):
+          pinned-host y in, phi out, copies inside the timed region
+roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+UNIT = "frames/s"
+
+# Algorithmic bytes per pixel per launch of each kernel:
+# the compulsory reads + writes of its own inputs/outputs (halo re-reads and
+# the optional user-output copies not counted).
+KERNEL_BYTES_PER_PX = {
+    "k0_stats": 8 + 4,              # y, phi
+    "k1_rows_fwd": 8 + 4 + 8,       # y, phi -> spectrum
+    "k2a_cols": 8 + 4 + 8 + 4 + 4,  # spectrum, r -> spectrum, r_init, q
+    "k2b_ricd": 4 + 4 + 4,          # r_init, q -> r
+    "k3a_rows_inv": 8 + 8 + 4 + 4,  # spectrum, y -> c, theta
+    "k3b_phiicd": 4 + 4 + 4 + 4,    # phi, c, theta -> phi
+}
+STEP_BYTES_PER_PX = 24  # y in (8) + r in/out (8) + phi in/out (8)
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------- clocks
+
+
+class ClockSampler(threading.Thread):
+    """NVML sampling of SM clock and clock-event reasons during a region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x1: "gpu_idle"}
+
+    def __init__(self, index, period=0.01):
+        super().__init__(daemon=True)
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.stop_ev = threading.Event()
+        self.max_mhz = None
+        self.ok = True
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.ok = False
+
+    def run(self):
+        if not self.ok:
+            return
+        nv = self.nv
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def stop(self):
+        self.stop_ev.set()
+        self.join(timeout=2)
+        return {"sm_mhz": float(statistics.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples), "reasons": sorted(self.reasons)}
+
+
+# ------------------------------------------------------------ oracle legs
+
+
+def _oracle_worker(job):
+    """Run the FP64 oracle over a list of (stream, frames) items, sequential per stream."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    import oracle.ddh_oracle as O
+    cfg, n, nv, items = job
+    p = O.OracleParams(n=n, aperture_diam=float(n), noise_var=nv)
+    a = O.aperture_of(p)
+    done = 0
+    for (y_stream,) in items:
+        r = np.full((n, n), p.r_min)
+        phi = np.zeros((n, n))
+        for t in range(y_stream.shape[0]):
+            r, phi, _ = O.ddh_step(r, phi, y_stream[t], p, a)
+            done += 1
+    return done
+
+
+def time_oracle(y, cfg, n, nv, cores):
+    """Wall time of the oracle on frames y [T][S][N][N] (streams split over
+    `cores` processes, frames of a stream sequential).  Returns (frames, s)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    T, S = y.shape[0], y.shape[1]
+    buckets = [[] for _ in range(min(cores, S))]
+    for s in range(S):
+        buckets[s % len(buckets)].append((np.ascontiguousarray(y[:, s]),))
+    with ProcessPoolExecutor(max_workers=len(buckets), mp_context=mp.get_context("spawn")) as ex:
+        # warm the workers (imports) outside the timed region
+        list(ex.map(_oracle_worker, [(cfg, n, nv, [(y[:1, 0],)])] * len(buckets)))
+        t0 = time.perf_counter()
+        done = sum(ex.map(_oracle_worker, [(cfg, n, nv, b) for b in buckets]))
+        dt = time.perf_counter() - t0
+    return done, dt
+
+
+# ------------------------------------------------------------- main legs
+
+
+def dist_setup(backend):
+    import torch.distributed as dist
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def reduce_max(x, ws, device=None):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=device if device is not None else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_setup("gloo")
+    if rank != 0:
+        return 0
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    n, S = cfg["n"], cfg["streams"]
+    nv = synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"])
+    cores = len(os.sched_getaffinity(0))
+    # a step = one stream-frame of the workload; K steps = K stream-frames over
+    # min(S, K) streams, frames sequential per stream (bounded sample)
+    K = args.steps
+    Su = max(1, min(S, K))
+    T = -(-K // Su)
+    y, _ = synth.make_batch(cfg, streams=Su, frames=T, want_phi=False)
+    if args.warmup > 0:
+        time_oracle(y[:1, :1], cfg, n, nv, 1)
+    done, dt = time_oracle(y, cfg, n, nv, cores)
+    value = done / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": K, "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(done, 1) * min(cores, Su),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, Su), "kind": "oracle",
+                         "sample": f"{done} stream-frames ({Su} streams x {T} frames of {args.config}, cold start), "
+                                   f"numpy FP64 oracle, streams over {min(cores, Su)} processes"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg):
+    return {"workload": f"{cfg['name']}: {cfg['n']}x{cfg['n']} complex64 DH frames, {cfg['streams']} streams/GPU, "
+                        f"N_k={cfg['n_k']}, D/r0 " + (f"U{cfg['d_r0_range']}" if cfg.get('d_r0_range') else str(cfg['d_r0'])) +
+                        f", flow {cfg['flow']} px/frame {cfg['direction']}, SNR {cfg['snr_db']} dB",
+            "n": cfg["n"], "streams_per_gpu": cfg["streams"], "n_k": cfg["n_k"],
+            "priors": "qGGMRF r (sigma 0.5, T 1, q 1.2) + GMRF phi (sigma 0.5)",
+            "l2": "inputs larger than L2: 100 distinct 32 MiB frame batches (3.2 GiB) staged in HBM and cycled"}
+
+
+def run_ours(args):
+    import torch
+
+    import synth
+    from paper_2305_03284_b200 import DDH
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    n, S, F = cfg["n"], cfg["streams"], min(args.frames, cfg["frames"])
+    nv = synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"])
+    P = n * n
+    # ---- inputs (synthetic, distinct streams per rank), generated before CUDA init
+    t0 = time.time()
+    y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=rank * S, want_phi=False)
+    gen_s = time.time() - t0
+    ws, rank, local = dist_setup("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    y_dev = torch.from_numpy(y_host).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk)
+    K, W = args.steps, args.warmup
+    for w in range(W):
+        ctx.step(y_dev[w % F:w % F + 1])
+    # parity sample (rank 0): one GPU step vs the oracle from the same FP32 state
+    parity = None
+    if rank == 0 and not args.no_parity:
+        parity = quick_parity(ctx, y_dev, y_host, W % F, n, nv, dev)
+    torch.cuda.synchronize()
+    # ---- timed region: K steps, per-kernel CUDA events on the ctx stream
+    ctx.profile(True)
+    ctx.profile_read()
+    l0 = ctx.kernel_launches
+    barrier(ws)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(K):
+        t = (W + k) % F
+        ctx.step(y_dev[t:t + 1])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    barrier(ws)
+    ms = e0.elapsed_time(e1)
+    launches = ctx.kernel_launches - l0
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    ms_max = reduce_max(ms, ws, dev)
+    frames_total = K * S * ws
+    value = frames_total / (ms_max * 1e-3)
+    # ---- uninstrumented repeat (same K) for the instrumentation overhead
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(K):
+        t = (W + K + k) % F
+        ctx.step(y_dev[t:t + 1])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_plain = reduce_max(e0.elapsed_time(e1), ws, dev)
+    # ---- roofline of the dominant kernel (algorithmic bytes / live event time)
+    peak, peak_src = peaks()
+    kernels = {}
+    for name, (tms, cnt) in prof.items():
+        kernels[name] = {"ms_total": tms, "launches": cnt, "share": tms / max(sum(v[0] for v in prof.values()), 1e-12)}
+        if name in KERNEL_BYTES_PER_PX:
+            iters = K * cfg["n_k"]
+            bytes_total = KERNEL_BYTES_PER_PX[name] * P * S * (iters if name != "k0_stats" else K)
+            kernels[name]["gbs"] = bytes_total / (tms * 1e-3) / 1e9
+            kernels[name]["bytes_per_px"] = KERNEL_BYTES_PER_PX[name]
+    dom = max((k for k in kernels if k in KERNEL_BYTES_PER_PX), key=lambda k: kernels[k]["ms_total"])
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(ncu_path):
+        d = json.load(open(ncu_path))
+        traffic = d.get("dram_bytes_per_launch", {}).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": kernels[dom]["gbs"] / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": KERNEL_BYTES_PER_PX[dom] * P * ctx_chunk(ctx),
+                "step_frac": (STEP_BYTES_PER_PX * P * K * S / (ms * 1e-3) / 1e9) / peak}
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": dict(workload_config(cfg), parallelism=f"streams x{ws} GPUs",
+                                                           synth_seconds=round(gen_s, 1)),
+        "roofline": roofline, "gpu_launches": launches, "clocks": clocks,
+        "uninstrumented": {"value": frames_total / (ms_plain * 1e-3), "ms_per_step": ms_plain / K},
+        "kernels": kernels,
+    }
+    if parity is not None:
+        out["parity"] = parity
+    # ---- e2e: host buffers through ddh_step_host, copies inside the timed region
+    if not args.no_e2e:
+        out["e2e"] = e2e_leg(ctx, y_host, K, ws, dev, S, n)
+    # ---- latency (configs[1], c2): 1 stream, per-frame device latency
+    if not args.no_latency:
+        out["latency"] = latency_leg(dev, local)
+    # ---- cpu baseline (rank 0, N = 1 only)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        m = S
+        done, dt = time_oracle(y_host[:1, :m], cfg, n, nv, cores)
+        out["cpu_baseline"] = {"value": done / dt, "unit": UNIT, "cores": min(cores, m), "kind": "oracle",
+                               "sample": f"one time step of {m} streams of {args.config} (cold start), numpy FP64 "
+                                         f"oracle, streams over {min(cores, m)} processes, {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    del ctx
+    return 0
+
+
+def ctx_chunk(ctx):
+    import ctypes  # noqa: F401
+    # launch-group size chosen by the library (auto): mirror of ddh_create's rule
+    n = ctx.n
+    if ctx.params.chunk_streams > 0:
+        return min(ctx.params.chunk_streams, ctx.S)
+    lim = max(1, int(48 * 1024 * 1024 // (32 * n * n)))
+    sc = 1
+    while sc * 2 <= lim:
+        sc *= 2
+    return min(sc, ctx.S)
+
+
+def quick_parity(ctx, y_dev, y_host, t, n, nv, dev):
+    import torch
+
+    import oracle.ddh_oracle as O
+    r0, phi0, fi = ctx.get_state()
+    S = ctx.S
+    phi_o = torch.empty((1, S, n, n), device=dev)
+    r_o = torch.empty_like(phi_o)
+    ctx.step(y_dev[t:t + 1], phi_o, r_o)
+    torch.cuda.synchronize()
+    p = O.OracleParams(n=n, aperture_diam=float(n), noise_var=nv)
+    a = O.aperture_of(p)
+    s = S - 1
+    gaps = np.full((n, n), np.inf)
+    rr, pp, _ = O.ddh_step(r0[s].cpu().numpy().astype(np.float64), phi0[s].cpu().numpy().astype(np.float64),
+                           y_host[t, s], p, a, gaps)
+    d = np.angle(np.exp(1j * (phi_o[0, s].cpu().numpy() - pp)))[a > 0]
+    d = np.angle(np.exp(1j * (d - np.angle(np.mean(np.exp(1j * d))))))
+    tie = gaps < 1e-6
+    m = tie.copy()
+    for di in range(-2, 3):
+        for dj in range(-2, 3):
+            m |= np.roll(np.roll(tie, di, 0), dj, 1)
+    rg = r_o[0, s].cpu().numpy()
+    rel = float(np.linalg.norm((rg - rr)[~m]) / np.linalg.norm(rr[~m]))
+    return {"stream": s, "frame_batch": t, "phi_max_rad": float(np.max(np.abs(d))), "r_rel_l2": rel,
+            "excluded_px": int(m.sum()), "tol": {"phi": 1e-3, "r": 1e-4}}
+
+
+def e2e_leg(ctx, y_host, K, ws, dev, S, n):
+    import torch
+    E = min(y_host.shape[0], 16)
+    Ke = min(K, 200)
+    y_pin = torch.from_numpy(np.ascontiguousarray(y_host[:E])).pin_memory()
+    phi_pin = torch.empty((1, S, n, n), dtype=torch.float32).pin_memory()
+    for k in range(2):
+        ctx.step_host(y_pin[k:k + 1], phi_out=phi_pin)
+    barrier(ws)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(Ke):
+        ctx.step_host(y_pin[k % E:k % E + 1], phi_out=phi_pin)  # synchronous (D2H of phi inside)
+    dt = time.perf_counter() - t0
+    dt = reduce_max(dt, ws, dev)
+    P = n * n
+    return {"value": Ke * S * ws / dt, "unit": UNIT, "h2d_bytes_per_step": S * P * 8, "d2h_bytes_per_step": S * P * 4,
+            "steps": Ke, "api": "ddh_step_host (pinned host y in, phi out), host wall clock, max over ranks"}
+
+
+def latency_leg(dev, local):
+    import torch
+
+    import synth
+    from paper_2305_03284_b200 import DDH
+    cfg = synth.CONFIGS["c2"]
+    n = cfg["n"]
+    T = cfg["frames"]
+    y, _ = synth.make_batch(cfg, streams=1, frames=T, want_phi=False, workers=1)
+    yd = torch.from_numpy(y).to(dev)
+    ctx = DDH(n, 1, device=local, noise_var=synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"]))
+    stream = torch.cuda.current_stream(dev)
+    dev_us, host_us = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for t in range(T):
+        torch.cuda.synchronize()
+        h0 = time.perf_counter()
+        e0.record(stream)
+        ctx.step(yd[t:t + 1])
+        e1.record(stream)
+        e1.synchronize()
+        host_us.append((time.perf_counter() - h0) * 1e6)
+        dev_us.append(e0.elapsed_time(e1) * 1e3)
+    dev_us, host_us = dev_us[10:], host_us[10:]
+    q = lambda v, f: float(np.percentile(v, f))
+    return {"workload": "c2: 256x256, 1 stream, 200 frames (first 10 discarded), one ddh_step(T=1) per frame",
+            "p50_us": q(dev_us, 50), "p99_us": q(dev_us, 99), "host_p50_us": q(host_us, 50),
+            "host_p99_us": q(host_us, 99), "budget_us_at_fs_10kHz": 100.0}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--frames", type=int, default=100, help="distinct frame batches staged in HBM")
+    ap.add_argument("--chunk", type=int, default=0, help="streams per launch group (0 = library auto)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -161,6 +161,19 @@ uint64_t ddh_kernel_launches(const ddh_ctx *c);
 /* Frames processed so far (the n of Fig. 1). */
 int64_t ddh_frame_index(const ddh_ctx *c);
 
+/* ---- instrumentation: per-kernel device time (CUDA events on the ctx stream) ----
+ * Kernel kinds: 0 K0 stats, 1 K1 rows_fwd, 2 K2a cols, 3 K2b r-ICD,
+ * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl.  When enabled, every
+ * launch of the ctx is bracketed by two events (a small added cost). */
+#define DDH_KIND_COUNT 8
+ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable);
+/* Synchronises the ctx stream and ADDS the accumulated totals since the last
+ * read into ms[k] (milliseconds) and launches[k] (host arrays of
+ * DDH_KIND_COUNT), then clears the pending records. */
+ddh_status ddh_profile_read(ddh_ctx *c, double *ms, int64_t *launches);
+/* Static name of kernel kind k (or "?"). */
+const char *ddh_kind_name(int32_t k);
+
 /* ---- stage entry points for parity tests (same kernels as the hot path) ---- */
 
 /* Centred unitary 2-D DFT F_c (inverse = 0) or F_c^{-1} (inverse = 1) of B

@@ -50,6 +50,10 @@ struct ddh_ctx {
   float2 *y_stage = nullptr;
   float *phi_stage = nullptr, *r_stage = nullptr;
   uint8_t *status_stage = nullptr;
+  // instrumentation
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<int> ev_kind;  // kind of pending record i (events 2i, 2i+1)
   // bookkeeping
   uint64_t launches = 0;
   bool sticky = false;
@@ -79,10 +83,30 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
       return fail((c), DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-#define DDH_LAUNCH(c, call)  \
-  do {                       \
-    DDH_CK(c, call);         \
-    (c)->launches++;         \
+enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL };
+const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
+                                          "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl"};
+
+// Event pair for a launch of `kind` when profiling (nullptr otherwise).
+cudaEvent_t *prof_begin(ddh_ctx *c, int kind) {
+  if (!c->profiling) return nullptr;
+  const size_t i = c->ev_kind.size();
+  while (c->ev_pool.size() < 2 * (i + 1)) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    c->ev_pool.push_back(e);
+  }
+  c->ev_kind.push_back(kind);
+  cudaEventRecord(c->ev_pool[2 * i], c->st);
+  return &c->ev_pool[2 * i + 1];
+}
+
+#define DDH_LAUNCH(c, kind, call)                       \
+  do {                                                  \
+    cudaEvent_t *end_ = prof_begin((c), (kind));        \
+    DDH_CK(c, call);                                    \
+    if (end_) cudaEventRecord(*end_, (c)->st);          \
+    (c)->launches++;                                    \
   } while (0)
 
 bool valid_n(int n) { return n == 64 || n == 128 || n == 256 || n == 512 || n == 1024; }
@@ -161,7 +185,7 @@ ddh_status run_ricd(ddh_ctx *c, const float *r_in, const float *q, float *r_fina
     a.in = in;
     a.out = out;
     a.copy = last ? copy : nullptr;
-    DDH_LAUNCH(c, ddh::launch_ricd(a, sc, c->st));
+    DDH_LAUNCH(c, K_RICD, ddh::launch_ricd(a, sc, c->st));
     in = out;
   }
   return DDH_OK;
@@ -184,7 +208,7 @@ ddh_status run_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const fl
     a.out = out;
     a.copy = last ? copy : nullptr;
     a.apply_plane = (k == 0) ? apply_plane : 0;
-    DDH_LAUNCH(c, ddh::launch_phiicd(a, sc, c->st));
+    DDH_LAUNCH(c, K_PHIICD, ddh::launch_phiicd(a, sc, c->st));
     in = out;
   }
   return DDH_OK;
@@ -206,7 +230,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     const size_t so = (size_t)s0 * P;
     int cur = cur0;
     if (mode == Mode::Boot) {  // cold start r = r_min, phi = 0 (Fig. 1, R14)
-      DDH_LAUNCH(c, ddh::launch_fill(c->r + so, (float)c->p.r_min, (size_t)sc * P, c->st));
+      DDH_LAUNCH(c, K_FILL, ddh::launch_fill(c->r + so, (float)c->p.r_min, (size_t)sc * P, c->st));
       DDH_CK(c, cudaMemsetAsync(c->phi[cur] + so, 0, (size_t)sc * P * sizeof(float), c->st));
     }
     StepArgs a = base_args(c, s0, sc);
@@ -214,7 +238,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     a.phi_in = c->phi[cur] + so;
     a.want_y = 1;
     a.apply_plane = plane ? 1 : 0;
-    DDH_LAUNCH(c, ddh::launch_k0(a, c->st));
+    DDH_LAUNCH(c, K_STATS, ddh::launch_k0(a, c->st));
     for (int it = 0; it < iters; ++it) {
       const bool first = (it == 0), last = (it == iters - 1);
       a.phi_in = c->phi[cur] + so;
@@ -229,11 +253,11 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
         a.la = (float)c->p.boot_alpha;
       }
       a.status = (first && status) ? status + s0 : nullptr;
-      DDH_LAUNCH(c, ddh::launch_k1(a, c->st));
-      DDH_LAUNCH(c, ddh::launch_k2a(a, c->st));
+      DDH_LAUNCH(c, K_ROWS_FWD, ddh::launch_k1(a, c->st));
+      DDH_LAUNCH(c, K_COLS, ddh::launch_k2a(a, c->st));
       ddh_status rs = run_ricd(c, c->rinit, c->q, c->r + so, (last && r_out) ? r_out + so : nullptr, c->part1, sc);
       if (rs != DDH_OK) return rs;
-      DDH_LAUNCH(c, ddh::launch_k3a(a, c->st));
+      DDH_LAUNCH(c, K_ROWS_INV, ddh::launch_k3a(a, c->st));
       rs = run_phiicd(c, c->phi[cur] + so, c->cc, c->theta, c->phi[cur ^ 1] + so,
                       (last && phi_out) ? phi_out + so : nullptr, c->part0, c->part1, a.apply_plane, sc);
       if (rs != DDH_OK) return rs;
@@ -263,6 +287,7 @@ double inv3(const double G[9], double out[9]) {
 
 void free_ctx(ddh_ctx *c) {
   if (!c) return;
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->pmax, c->rowspan, c->tw,
                   c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
@@ -583,7 +608,7 @@ ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, i
     a.apply_plane = 1;
     a.phi_in = phi_hat + off;
     a.phi_sub = phi_true + off;
-    DDH_LAUNCH(c, ddh::launch_k0(a, c->st));
+    DDH_LAUNCH(c, K_STATS, ddh::launch_k0(a, c->st));
     StrehlArgs sa{};
     sa.n = c->n;
     sa.nb = c->strehl_nb;
@@ -624,6 +649,31 @@ const char *ddh_last_error(const ddh_ctx *c) {
 }
 
 uint64_t ddh_kernel_launches(const ddh_ctx *c) { return c ? c->launches : 0; }
+
+ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  c->profiling = enable != 0;
+  return DDH_OK;
+}
+
+ddh_status ddh_profile_read(ddh_ctx *c, double *ms, int64_t *launches) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (!ms || !launches) return fail(c, DDH_E_INVAL, "ddh_profile_read: NULL output");
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  DDH_CK(c, cudaStreamSynchronize(c->st));
+  for (size_t i = 0; i < c->ev_kind.size(); ++i) {
+    float t = 0.f;
+    DDH_CK(c, cudaEventElapsedTime(&t, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]));
+    ms[c->ev_kind[i]] += t;
+    launches[c->ev_kind[i]] += 1;
+  }
+  c->ev_kind.clear();
+  return DDH_OK;
+}
+
+const char *ddh_kind_name(int32_t k) { return (k >= 0 && k < DDH_KIND_COUNT) ? kKindNames[k] : "?"; }
 
 int64_t ddh_frame_index(const ddh_ctx *c) { return c ? c->frame : -1; }
 

@@ -51,7 +51,9 @@ EXPORTS = [
     "ddh_default_params", "ddh_create", "ddh_destroy", "ddh_bootstrap", "ddh_step", "ddh_step_host",
     "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_sync", "ddh_last_error",
     "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_ricd", "ddh_test_phiicd",
+    "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
 ]
+KIND_COUNT = 8
 
 _lib = None
 
@@ -86,8 +88,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.ddh_test_fft2c.argtypes = [vp, vp, vp, i32, i32]
     lib.ddh_test_ricd.argtypes = [vp, vp, vp, i32, vp]
     lib.ddh_test_phiicd.argtypes = [vp, vp, vp, vp, i32, vp]
+    lib.ddh_profile_enable.argtypes = [vp, i32]
+    lib.ddh_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
+    lib.ddh_kind_name.argtypes = [i32]
+    lib.ddh_kind_name.restype = ctypes.c_char_p
     for name in EXPORTS:
-        if name not in ("ddh_last_error", "ddh_kernel_launches", "ddh_frame_index"):
+        if name not in ("ddh_last_error", "ddh_kernel_launches", "ddh_frame_index", "ddh_kind_name"):
             getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -244,6 +250,17 @@ class DDH:
     @property
     def frame_index(self) -> int:
         return int(self.lib.ddh_frame_index(self.h))
+
+    # -- instrumentation
+    def profile(self, enable: bool = True):
+        _check(self.lib.ddh_profile_enable(self.h, int(enable)), self.h)
+
+    def profile_read(self):
+        """{kernel name: (total ms, launches)} accumulated since the last read."""
+        ms = (ctypes.c_double * KIND_COUNT)()
+        cnt = (ctypes.c_int64 * KIND_COUNT)()
+        _check(self.lib.ddh_profile_read(self.h, ms, cnt), self.h)
+        return {self.lib.ddh_kind_name(k).decode(): (ms[k], cnt[k]) for k in range(KIND_COUNT) if cnt[k]}
 
     # -- stage entry points (parity tests)
     def test_fft2c(self, x: torch.Tensor, inverse: bool = False) -> torch.Tensor:
