@@ -49,7 +49,7 @@ def oracle_params(n, diam=None, **kw):
 
 
 def gpu_kwargs(p: O.OracleParams):
-    return dict(noise_var=p.noise_var, lam=p.lam, alpha=p.alpha, n_k=p.n_k, r_min=p.r_min, r_sigma=p.r_sigma,
+    return dict(aperture_diam=p.aperture_diam, noise_var=p.noise_var, lam=p.lam, alpha=p.alpha, n_k=p.n_k, r_min=p.r_min, r_sigma=p.r_sigma,
                 r_T=p.r_T, r_q=p.r_q, phi_sigma=p.phi_sigma, icd_sweeps=p.icd_sweeps, boot_period=p.boot_period,
                 boot_alpha=p.boot_alpha, flags=0 if p.tiptilt else 1)
 
