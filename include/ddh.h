@@ -52,6 +52,8 @@ typedef enum {
 
 /* flags */
 #define DDH_F_NO_TIPTILT 1u /* skip RemoveTipTilt (Fig. 1) in ddh_step  */
+#define DDH_F_UNFUSED 2u    /* force the multi-pass kernels (default for N <= 512:
+                               the cluster-fused 3-kernel iteration)            */
 
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 

@@ -39,7 +39,9 @@ struct ddh_ctx {
   float2 *cbuf = nullptr;
   float *rinit = nullptr, *q = nullptr, *cc = nullptr, *theta = nullptr;
   float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
-  double *part0 = nullptr, *part1 = nullptr;
+  double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
+  bool fused = false;
+  int cs = 0;  // CTAs per stream of the fused path
   float *pmax = nullptr;
   // constants
   int2 *rowspan = nullptr;
@@ -142,6 +144,15 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
   a.r_min = (float)c->p.r_min;
   a.P = (float)c->P;
   std::memcpy(a.minv, c->minv, sizeof(a.minv));
+  a.stats = c->stats;
+  a.r_prior = c->p.r_sigma > 0 ? 1 : 0;
+  if (a.r_prior) {
+    a.r_b0 = (float)(1.0 / (2.0 * c->p.r_sigma * c->p.r_sigma));
+    a.r_inv_Tsig = (float)(1.0 / (c->p.r_T * c->p.r_sigma));
+    a.r_tmq = (float)(2.0 - c->p.r_q);
+  }
+  a.phi_prior = c->p.phi_sigma > 0 ? 1 : 0;
+  if (a.phi_prior) a.phi_w = (float)(1.0 / (c->p.phi_sigma * c->p.phi_sigma));
   return a;
 }
 
@@ -238,6 +249,32 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     a.phi_in = c->phi[cur] + so;
     a.want_y = 1;
     a.apply_plane = plane ? 1 : 0;
+    if (c->fused) {  // KA -> KB -> KC per EM iteration (cluster per stream)
+      a.nb1 = c->cs;
+      for (int it = 0; it < iters; ++it) {
+        const bool first = (it == 0), last = (it == iters - 1);
+        a.phi_in = c->phi[cur] + so;
+        a.phi_out = c->phi[cur ^ 1] + so;
+        a.apply_plane = (plane && first) ? 1 : 0;
+        if (mode == Mode::Step) {
+          a.warm = first ? 1 : 0;
+          a.oml = (float)(1.0 - c->p.lambda);
+          a.la = (float)(c->p.lambda * c->p.alpha);
+        } else {
+          a.warm = (it % c->p.boot_period == 0) ? 1 : 0;
+          a.oml = 0.f;
+          a.la = (float)c->p.boot_alpha;
+        }
+        a.status = (first && status) ? status + s0 : nullptr;
+        a.r_copy = (last && r_out) ? r_out + so : nullptr;
+        a.phi_copy = (last && phi_out) ? phi_out + so : nullptr;
+        DDH_LAUNCH(c, K_ROWS_FWD, ddh::launch_ka(a, c->st));
+        DDH_LAUNCH(c, K_COLS, ddh::launch_kb(a, c->st));
+        DDH_LAUNCH(c, K_ROWS_INV, ddh::launch_kc(a, c->st));
+        cur ^= 1;
+      }
+      continue;
+    }
     DDH_LAUNCH(c, K_STATS, ddh::launch_k0(a, c->st));
     for (int it = 0; it < iters; ++it) {
       const bool first = (it == 0), last = (it == iters - 1);
@@ -289,7 +326,7 @@ void free_ctx(ddh_ctx *c) {
   if (!c) return;
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
-                  c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->pmax, c->rowspan, c->tw,
+                  c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw,
                   c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -428,7 +465,8 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     A(dalloc(&c->ptmp[1], SC * P));
   }
   A(dalloc(&c->part0, SC * c->nb0 * 5));
-  A(dalloc(&c->part1, SC * c->nb1));
+  A(dalloc(&c->part1, SC * std::max(c->nb1, 16)));
+  A(dalloc(&c->stats, SC * 5));
   A(dalloc(&c->pmax, SC * c->strehl_nb));
   A(dalloc(&c->rowspan, (size_t)n));
   A(dalloc(&c->tw, (size_t)n));
@@ -446,6 +484,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   A(cudaMemcpy(c->tw, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
   A(cudaMemcpy(c->rowspan, span.data(), n * sizeof(int2), cudaMemcpyHostToDevice));
   A(ddh::init_kernels(n));
+  c->fused = ddh::fused_supported(n) && !(p.flags & DDH_F_UNFUSED);
+  if (c->fused) {
+    c->cs = ddh::fused_cluster(n);
+    A(ddh::init_fused(n));
+  }
   // state: n = 0, r = r_min, phi = 0 (Fig. 1; R14)
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));
   A(cudaMemsetAsync(c->phi[0], 0, S * P * sizeof(float), c->st));

@@ -1,0 +1,152 @@
+// ddh_common.cuh -- device helpers shared by the unfused (ddh_kernels.cu) and
+// the cluster-fused (ddh_fused.cu) kernels: deterministic reductions, the
+// aperture test, the qGGMRF surrogate weight, the per-pixel r and phi
+// M-step updates (readings R6-R11 of DESIGN.md).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+namespace ddh {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum of K doubles (fixed shuffle tree + fixed warp order).
+// Result valid in thread 0.  sh: >= 32*K doubles of shared memory.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double *sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh[warp * K + k] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double x = lane < nw ? sh[lane * K + k] : 0.0;
+      v[k] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+// Plane coefficients c = Minv h of the RemoveTipTilt normal equations (R17);
+// sums[2..4] = (sum phi, sum phi x, sum phi y) over the aperture.
+__device__ __forceinline__ void plane_from_sums(const double *sums, const double *minv, double *c) {
+  const double h0 = sums[2], h1 = sums[3], h2 = sums[4];
+  c[0] = minv[0] * h0 + minv[1] * h1 + minv[2] * h2;
+  c[1] = minv[3] * h0 + minv[4] * h1 + minv[5] * h2;
+  c[2] = minv[6] * h0 + minv[7] * h1 + minv[8] * h2;
+}
+
+__device__ __forceinline__ bool in_ap(const int2 *__restrict__ rs, int i, int j) {
+  const int2 s = __ldg(rs + i);
+  return j >= s.x && j < s.y;
+}
+
+// 8-neighbour stencil: offsets and weights b (1/6 nearest, 1/12 diagonal; R7)
+__device__ __forceinline__ int nb_di(int k) { return (k < 4) ? ((k == 0) ? -1 : (k == 1) ? 1 : 0) : ((k < 6) ? -1 : 1); }
+__device__ __forceinline__ int nb_dj(int k) { return (k < 4) ? ((k == 2) ? -1 : (k == 3) ? 1 : 0) : ((k & 1) ? 1 : -1); }
+__device__ __forceinline__ float nb_w(int k) { return (k < 4) ? (1.f / 6.f) : (1.f / 12.f); }
+
+// qGGMRF surrogate weight rho'(D)/(2D) in units of 1/(2 sig^2) (R6):
+// (1/(1+t)) (1 - (2-q) t / (2(1+t))),  t = |D/(T sig)|^(2-q).
+__device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
+  const float a = fabsf(d) * inv_Tsig;
+  const float t = a > 0.f ? exp2f(tmq * log2f(a)) : 0.f;
+  const float inv = 1.f / (1.f + t);
+  return inv * (1.f - 0.5f * tmq * t * inv);
+}
+
+// ---- r M-step, one pixel (R9) -------------------------------------------
+// Minimiser over x >= r_min of f(x) = log x + q/x + B x^2 - 2 S x (B > 0).
+// f'(x) = g(x)/x^2 with g(x) = 2B x^3 - 2S x^2 + x - q, g(0) = -q < 0.
+// g is concave left of its inflection xi = S/(3B) and convex right of it, so:
+//  * a root left of xi exists iff g(xi) > 0; monotone Newton from 0 reaches it
+//    (concave, increasing: the iterates stay left of the root);
+//  * a root right of xi exists iff g(xi) <= 0, or the local minimum of g at
+//    x2 = (2S + sqrt(4S^2 - 6B))/(6B) is negative; monotone Newton from
+//    U = max(S/B, q) (where g >= 0) reaches it from the right.
+// These two roots are the local minima of f (the middle root, if any, is a
+// local maximum).  With both present the lower f wins (FP32 difference);
+// candidates are clamped to r_min.  No transcendental root formula, no FP64.
+__device__ __forceinline__ float g_of(float x, float B2, float S2, float q) {
+  return fmaf(fmaf(fmaf(B2, x, -S2), x, 1.f), x, -q);
+}
+__device__ __forceinline__ float dg_of(float x, float B6, float S4) { return fmaf(fmaf(B6, x, -S4), x, 1.f); }
+
+__device__ __forceinline__ float newton_root(float x, float B2, float S2, float B6, float S4, float q) {
+#pragma unroll 1
+  for (int it = 0; it < 16; ++it) {
+    const float g = g_of(x, B2, S2, q);
+    const float d = dg_of(x, B6, S4);
+    if (!(d > 0.f)) break;
+    const float dx = g / d;
+    x -= dx;
+    if (fabsf(dx) <= 2e-7f * fabsf(x)) break;
+  }
+  return x;
+}
+
+__device__ __forceinline__ float r_update(float rc, float q, float B, float S, float r_min) {
+  const float B2 = 2.f * B, S2 = 2.f * S, B6 = 6.f * B, S4 = 4.f * S;
+  const float xi = S / (3.f * B);
+  const float gi = xi > 0.f ? g_of(xi, B2, S2, q) : -q;
+  const bool has_small = gi > 0.f;
+  bool has_large = !has_small;
+  if (has_small) {
+    const float disc = 4.f * S * S - 6.f * B;
+    if (disc > 0.f) {
+      const float x2 = (2.f * S + sqrtf(disc)) / B6;
+      has_large = g_of(x2, B2, S2, q) < 0.f;
+    }
+  }
+  float xs = 0.f, xl = 0.f;
+  if (has_small) xs = newton_root(q, B2, S2, B6, S4, q);  // first Newton step from 0 is x = q
+  if (has_large) xl = newton_root(fmaxf(S / B, q), B2, S2, B6, S4, q);
+  if (!has_large) return fmaxf(xs, r_min);
+  if (!has_small) return fmaxf(xl, r_min);
+  const float a = fmaxf(xs, r_min), b = fmaxf(xl, r_min);
+  // f(b) - f(a)
+  const float df = logf(b / a) + q * (a - b) / (a * b) + (b - a) * (B * (a + b) - 2.f * S);
+  const float tol = 1e-6f * (1.f + fabsf(logf(a)) + q / a);
+  if (fabsf(df) <= tol) return fabsf(a - rc) <= fabsf(b - rc) ? a : b;
+  return df < 0.f ? b : a;
+}
+
+// ---- phi M-step, one pixel (R10-R11) --------------------------------------
+__device__ __forceinline__ float wrap_pi(float x) {  // (-pi, pi]
+  const float twopi = 6.283185307179586f;
+  float y = fmaf(-twopi, rintf(x * 0.15915494309189535f), x);
+  if (y <= -3.14159265358979f) y += twopi;
+  if (y > 3.14159265358979f) y -= twopi;
+  return y;
+}
+
+// phi <- (c s th~ + w sum b phi_j)/(c s + w sum b), s = sin(x0)/x0, th~ = phi - x0,
+// x0 = wrap(phi - theta) (symmetric bound of -c cos(.) at x0).  Prior off:
+// phi <- th~ where c > 0 (exact argmax).
+__device__ __forceinline__ float phi_update(float phi, float c, float th, float nb, float sb, float w, bool prior) {
+  const float x0 = wrap_pi(phi - th);
+  const float tt = phi - x0;
+  if (!prior) return c > 0.f ? tt : phi;
+  const float x2 = x0 * x0;
+  const float s = fabsf(x0) < 1e-3f ? fmaf(x2, fmaf(x2, 1.f / 120.f, -1.f / 6.f), 1.f) : __sinf(x0) / x0;
+  const float num = fmaf(c * s, tt, w * nb);
+  const float den = fmaf(c, s, w * sb);
+  return den != 0.f ? num / den : phi;
+}
+
+}  // namespace ddh

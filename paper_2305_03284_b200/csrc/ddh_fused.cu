@@ -1,0 +1,490 @@
+// ddh_fused.cu -- cluster-fused EM iteration for N <= 512 (sm_100a).
+//
+// One thread-block cluster per stream covers the whole N x N frame: KA and KC
+// split it into row slabs (H rows per CTA), KB into column slabs (W columns
+// per CTA).  Everything that needs a view wider than one slab goes through
+// distributed shared memory (DSMEM) inside the cluster instead of HBM:
+//   KA  kf_rows_fwd  y and phi rows -> per-stream sums (Eq. 4 mean, RemoveTipTilt
+//                    plane) reduced across the cluster over
+//                    DSMEM; z = chi a e^{-j phi'} (y - mu); forward row DFT
+//   KB  kf_cols      column DFT -> u = A^H y-hat (R13); Eq. 3; E-step (R1);
+//                    inverse column DFT of chi mu; qGGMRF r-ICD (R6-R9) over
+//                    the slab, exchanging the boundary columns with the
+//                    neighbouring CTAs over DSMEM before each colour phase
+//   KC  kf_rows_inv  inverse row DFT -> f; c, theta (registers); GMRF phi-ICD
+//                    (R10-R11) with boundary rows exchanged over DSMEM
+// HBM traffic per pixel and EM iteration: KA 20 B, KB 24 B, KC 24 B (68 B),
+// against 112 B and 3 more launches for the unfused pass design.
+//
+// Race-freedom of the halo exchange: before colour phase c every CTA passes a
+// cluster barrier (all phase c-1 writes visible), copies the neighbour's
+// boundary column/row into its halo, then updates its colour-c pixels.  A
+// neighbour may modify the copied column during phase c only if that column
+// has the parity of colour c, in which case the adjacent own column has the
+// other parity and is not updated in phase c, so the possibly stale halo values
+// are not used before the next phase re-copies them.
+#include "ddh_common.cuh"
+#include "ddh_fft.cuh"
+#include "ddh_kernels.h"
+
+#include <cooperative_groups.h>
+
+namespace cg = cooperative_groups;
+
+namespace ddh {
+
+template <int N> struct FusedCfg {
+  static constexpr int CS = (N <= 128) ? 8 : 16;  // CTAs per stream (cluster size)
+  static constexpr int H = N / CS;                // rows per CTA (KA, KC)
+  static constexpr int W = N / CS;                // columns per CTA (KB)
+  static constexpr int E = FftPlan<N>::E;
+  static constexpr int NT = H * (N / E);          // threads per CTA (all three kernels)
+  static constexpr int EPT = H * N / NT;          // pixels per thread (= E)
+  static constexpr int RP = W + 2;                // pitch of the r-ICD slab (1-column halos)
+  static constexpr bool SPILL = (N >= 512);       // KB: r0/q through global scratch (smem limit)
+};
+
+bool fused_supported(int n) { return n == 64 || n == 128 || n == 256 || n == 512; }
+int fused_cluster(int n) { return n <= 128 ? 8 : 16; }
+
+template <int N> __host__ __device__ constexpr size_t ka_smem() { return (size_t)(FusedCfg<N>::H * (N + 1) + N) * sizeof(float2); }
+template <int N> __host__ __device__ constexpr size_t kb_smem() {
+  using C = FusedCfg<N>;
+  const size_t tile = (size_t)N * C::W * sizeof(float2);
+  const size_t rq = (size_t)2 * N * C::RP * sizeof(float);
+  return (C::SPILL ? (tile > rq ? tile : rq) : tile + rq) + (size_t)N * sizeof(float2);
+}
+template <int N> __host__ __device__ constexpr size_t kc_smem() {
+  using C = FusedCfg<N>;
+  const size_t tile = (size_t)C::H * (N + 1) * sizeof(float2);
+  const size_t ph = (size_t)(C::H + 2) * N * sizeof(float);
+  return (tile > ph ? tile : ph) + (size_t)N * sizeof(float2);
+}
+
+// ------------------------------------------------------------------- KA
+
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_fwd(StepArgs A) {
+  using C = FusedCfg<N>;
+  constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ float2 sm[];
+  float2 *tile = sm;
+  float2 *tw = sm + H * PITCH;
+  __shared__ double red[32 * 5];
+  __shared__ double part[5];
+  __shared__ double tot[5];
+  const int tid = threadIdx.x;
+  const int s = blockIdx.y;
+  const int i0 = rank * H;
+  const size_t off = (size_t)s * P;
+  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  float ph[EPT];
+  double v[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1), i = i0 + r;
+    const size_t g = off + (size_t)i * N + j;
+    const float2 y = A.y[g];
+    tile[r * PITCH + j] = y;
+    const float f = A.phi_in[g];
+    ph[k] = f;
+    v[0] += (double)y.x;
+    v[1] += (double)y.y;
+    if (A.apply_plane && in_ap(A.rowspan, i, j)) {
+      v[2] += (double)f;
+      v[3] += (double)f * (double)(j - N / 2);
+      v[4] += (double)f * (double)(i - N / 2);
+    }
+  }
+  block_sum<5>(v, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) part[k] = v[k];
+  }
+  cl.sync();  // all partials of the stream written
+  if (tid < 5) {
+    double acc = 0.0;
+    for (int r = 0; r < CS; ++r) acc += cl.map_shared_rank(part, r)[tid];  // fixed rank order
+    tot[tid] = acc;
+  }
+  cl.barrier_arrive();  // remote reads of `part` done (waited on before exit)
+  __syncthreads();
+  double c[3] = {0, 0, 0};
+  if (A.apply_plane) plane_from_sums(tot, A.minv, c);
+  const double mu_r = tot[0] / P, mu_i = tot[1] / P;
+  if (rank == 0 && tid == 0) {
+    double *st = A.stats + (size_t)s * 5;
+    st[0] = mu_r;
+    st[1] = mu_i;
+    st[2] = c[0];
+    st[3] = c[1];
+    st[4] = c[2];
+  }
+  const float mur = (float)mu_r, mui = (float)mu_i;
+  const float c0 = (float)c[0], c1 = (float)c[1], c2 = (float)c[2];
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1), i = i0 + r;
+    const float2 y = tile[r * PITCH + j];
+    const float dr = y.x - mur, di = y.y - mui;
+    acc += (double)dr * dr + (double)di * di;
+    float2 z = make_float2(0.f, 0.f);
+    if (in_ap(A.rowspan, i, j)) {
+      const float p = ph[k] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
+      float sn, cs;
+      sincosf(p, &sn, &cs);
+      z = make_float2(dr * cs + di * sn, di * cs - dr * sn);  // (y - mu) e^{-j phi'}
+      if ((i + j) & 1) z = make_float2(-z.x, -z.y);
+    }
+    tile[r * PITCH + j] = z;
+  }
+  double a1[1] = {acc};
+  block_sum<1>(a1, red);  // also orders the tile writes before the FFT
+  if (tid == 0) A.part1[(size_t)s * CS + rank] = a1[0];
+  block_fft<N, -1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1);
+    A.cbuf[off + (size_t)(i0 + r) * N + j] = tile[r * PITCH + j];
+  }
+  cl.barrier_wait();
+}
+
+// ------------------------------------------------------------------- KB
+
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
+  using C = FusedCfg<N>;
+  constexpr int W = C::W, NT = C::NT, CS = C::CS, EPT = C::EPT, RP = C::RP, P = N * N;
+  constexpr bool SPILL = C::SPILL;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ float2 sm[];
+  float2 *tile = sm;  // [N][W]
+  float *rS = SPILL ? reinterpret_cast<float *>(sm) : reinterpret_cast<float *>(sm + N * W);  // [N][RP]
+  float *qS = rS + N * RP;
+  float2 *tw = SPILL ? sm + (kb_smem<N>() / sizeof(float2) - N) : reinterpret_cast<float2 *>(qS + N * RP);
+  __shared__ double st[1];
+  const int tid = threadIdx.x;
+  const int s = blockIdx.y;
+  const int c0 = rank * W;
+  const size_t off = (size_t)s * P;
+  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  if (tid == 0) {
+    double d2 = 0.0;
+    for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
+    st[0] = d2;
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    tile[idx] = A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W];
+  }
+  __syncthreads();
+  const double d2 = st[0];
+  const bool degenerate = !(d2 > 0.0);
+  if (A.status && rank == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
+  const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+  const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
+  block_fft<N, -1>(tile + tid % W, true, tid / W, W, tw);
+  const bool warm = A.warm && !degenerate;
+  // Eq. 3 + E-step over 2x2 pixel blocks (one pixel of each colour per block)
+#pragma unroll
+  for (int k = 0; k < EPT / 4; ++k) {
+    const int b = tid + k * NT;
+    const int br = b / (W / 2), bc = b % (W / 2);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int ki = 2 * br + (q4 >> 1), lc = 2 * bc + (q4 & 1), kj = c0 + lc;
+      const float sg = ((ki + kj) & 1) ? -scale : scale;
+      const float2 X = tile[ki * W + lc];
+      const float2 u = make_float2(X.x * sg, X.y * sg);
+      const size_t g = off + (size_t)ki * N + kj;
+      const float rp = A.r_state[g];
+      float r0 = rp;
+      if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
+      const float w = r0 / (r0 + A.s2);
+      const float2 mu = make_float2(w * u.x, w * u.y);
+      const float qv = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+      if (SPILL) {
+        A.rinit[g] = r0;
+        A.q[g] = qv;
+      } else {
+        rS[ki * RP + lc + 1] = r0;
+        qS[ki * RP + lc + 1] = qv;
+      }
+      const float cs = ((ki + kj) & 1) ? -1.f : 1.f;
+      tile[ki * W + lc] = make_float2(cs * mu.x, cs * mu.y);
+    }
+  }
+  __syncthreads();
+  block_fft<N, +1>(tile + tid % W, true, tid / W, W, tw);
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W] = tile[idx];
+  }
+  if (SPILL) {
+    __syncthreads();  // tile dead: reuse as rS / qS
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int idx = tid + k * NT;
+      const int i = idx / W, c = idx % W;
+      const size_t g = off + (size_t)i * N + c0 + c;
+      rS[i * RP + c + 1] = A.rinit[g];
+      qS[i * RP + c + 1] = A.q[g];
+    }
+  }
+  __syncthreads();
+  const bool icd = A.r_prior && !degenerate;  // uniform over the cluster (one stream)
+  if (icd) {
+    float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
+    float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
+    for (int c = 0; c < 4; ++c) {
+      cl.sync();
+      for (int i = tid; i < N; i += NT) {
+        rS[i * RP] = left[i * RP + W];
+        rS[i * RP + W + 1] = right[i * RP + 1];
+      }
+      __syncthreads();
+      const int ci = c >> 1, cj = c & 1;
+#pragma unroll
+      for (int k = 0; k < EPT / 4; ++k) {
+        const int b = tid + k * NT;
+        const int br = b / (W / 2), bc = b % (W / 2);
+        const int ki = 2 * br + ci, lj = 2 * bc + cj + 1;
+        const float ri = rS[ki * RP + lj];
+        float B = 0.f, S = 0.f;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int ni = (ki + nb_di(m)) & (N - 1);  // periodic rows (full columns in the CTA)
+          const float rj = rS[ni * RP + lj + nb_dj(m)];
+          const float bt = nb_w(m) * A.r_b0 * qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
+          B += bt;
+          S = fmaf(bt, rj, S);
+        }
+        rS[ki * RP + lj] = r_update(ri, qS[ki * RP + lj], B, S, A.r_min);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int i = idx / W, c = idx % W;
+    float v = rS[i * RP + c + 1];
+    if (!A.r_prior && !degenerate) v = fmaxf(qS[i * RP + c + 1], A.r_min);  // prior off: max(q, r_min)
+    const size_t g = off + (size_t)i * N + c0 + c;
+    A.r_state[g] = v;
+    if (A.r_copy) A.r_copy[g] = v;
+  }
+  if (icd) cl.sync();  // neighbours may still read our slab (last halo copy)
+}
+
+// ------------------------------------------------------------------- KC
+
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_inv(StepArgs A) {
+  using C = FusedCfg<N>;
+  constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ float2 sm[];
+  float2 *tile = sm;                                // [H][N+1]
+  float *phS = reinterpret_cast<float *>(sm);       // [H+2][N] (aliases the tile after the FFT)
+  float2 *tw = sm + (kc_smem<N>() / sizeof(float2) - N);
+  __shared__ double st[6];
+  const int tid = threadIdx.x;
+  const int s = blockIdx.y;
+  const int i0 = rank * H;
+  const size_t off = (size_t)s * P;
+  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  if (tid == 0) {
+    double d2 = 0.0;
+    for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
+    const double *sv = A.stats + (size_t)s * 5;
+    st[0] = sv[0];
+    st[1] = sv[1];
+    st[2] = sv[2];
+    st[3] = sv[3];
+    st[4] = sv[4];
+    st[5] = d2;
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1);
+    tile[r * PITCH + j] = A.cbuf[off + (size_t)(i0 + r) * N + j];
+  }
+  __syncthreads();
+  const float mur = (float)st[0], mui = (float)st[1];
+  const float c0 = (float)st[2], c1 = (float)st[3], c2 = (float)st[4];
+  const double d2 = st[5];
+  const bool degenerate = !(d2 > 0.0);
+  const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);
+  block_fft<N, +1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+  // phase-correlation terms for this thread's pixels (2x2 blocks), kept in registers
+  float creg[EPT], treg[EPT];
+  const float inv_n = 1.f / (float)N, two_s2 = 2.f / A.s2;
+#pragma unroll
+  for (int k = 0; k < EPT / 4; ++k) {
+    const int b = tid + k * NT;
+    const int br = b / (N / 2), bc = b % (N / 2);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int r = 2 * br + (q4 >> 1), j = 2 * bc + (q4 & 1), i = i0 + r;
+      float c = 0.f, th = 0.f;
+      if (in_ap(A.rowspan, i, j)) {
+        const float sg = ((i + j) & 1) ? -inv_n : inv_n;
+        const float2 X = tile[r * PITCH + j];
+        const float2 f = make_float2(X.x * sg, X.y * sg);
+        const float2 y = A.y[off + (size_t)i * N + j];
+        const float2 yh = make_float2(kappa * (y.x - mur), kappa * (y.y - mui));
+        const float2 z = make_float2(yh.x * f.x + yh.y * f.y, yh.y * f.x - yh.x * f.y);  // yh conj(f)
+        c = two_s2 * hypotf(z.x, z.y);
+        th = atan2f(z.y, z.x);
+      }
+      creg[k * 4 + q4] = c;
+      treg[k * 4 + q4] = th;
+    }
+  }
+  __syncthreads();  // tile dead: reuse as phS
+  if (degenerate) {  // state unchanged (no tip/tilt removal either)
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int idx = tid + k * NT;
+      const size_t g = off + (size_t)(i0 + idx / N) * N + (idx & (N - 1));
+      const float v = A.phi_in[g];
+      A.phi_out[g] = v;
+      if (A.phi_copy) A.phi_copy[g] = v;
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1), i = i0 + r;
+    phS[(r + 1) * N + j] = A.phi_in[off + (size_t)i * N + j] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
+  }
+  __syncthreads();
+  const bool prior = A.phi_prior != 0;
+  const float w = A.phi_w;
+  if (prior) {
+    const float *up = rank > 0 ? cl.map_shared_rank(phS, rank - 1) : nullptr;
+    const float *dn = rank < CS - 1 ? cl.map_shared_rank(phS, rank + 1) : nullptr;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cl.sync();
+      for (int j = tid; j < N; j += NT) {
+        if (up) phS[j] = up[H * N + j];
+        if (dn) phS[(H + 1) * N + j] = dn[N + j];
+      }
+      __syncthreads();
+      const int ci = c >> 1, cj = c & 1;
+#pragma unroll
+      for (int k = 0; k < EPT / 4; ++k) {
+        const int b = tid + k * NT;
+        const int br = b / (N / 2), bc = b % (N / 2);
+        const int r = 2 * br + ci, j = 2 * bc + cj, i = i0 + r, li = r + 1;
+        float nb = 0.f, sb = 0.f;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int ni = i + nb_di(m), nj = j + nb_dj(m);
+          if (ni >= 0 && ni < N && nj >= 0 && nj < N) {  // free boundary
+            nb = fmaf(nb_w(m), phS[(li + nb_di(m)) * N + nj], nb);
+            sb += nb_w(m);
+          }
+        }
+        phS[li * N + j] = phi_update(phS[li * N + j], creg[k * 4 + c], treg[k * 4 + c], nb, sb, w, true);
+      }
+    }
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int k = 0; k < EPT / 4; ++k) {
+      const int b = tid + k * NT;
+      const int br = b / (N / 2), bc = b % (N / 2);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int li = 2 * br + (q4 >> 1) + 1, j = 2 * bc + (q4 & 1);
+        phS[li * N + j] = phi_update(phS[li * N + j], creg[k * 4 + q4], treg[k * 4 + q4], 0.f, 0.f, 0.f, false);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int r = idx / N, j = idx & (N - 1);
+    const size_t g = off + (size_t)(i0 + r) * N + j;
+    const float v = phS[(r + 1) * N + j];
+    A.phi_out[g] = v;
+    if (A.phi_copy) A.phi_copy[g] = v;
+  }
+  if (prior) cl.sync();  // neighbours may still read our boundary rows
+}
+
+// ------------------------------------------------------------- launchers
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, int cs,
+                                  cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+template <int N>
+static cudaError_t init_fused_n() {
+  cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ka_smem<N>());
+  cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kb_smem<N>());
+  cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kc_smem<N>());
+  if (FusedCfg<N>::CS > 8) {
+    cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  return cudaGetLastError();
+}
+
+#define DDH_FDISPATCH(n, CALL)                          \
+  switch (n) {                                          \
+    case 64: { constexpr int N = 64; CALL; } break;     \
+    case 128: { constexpr int N = 128; CALL; } break;   \
+    case 256: { constexpr int N = 256; CALL; } break;   \
+    case 512: { constexpr int N = 512; CALL; } break;   \
+    default: return cudaErrorInvalidValue;              \
+  }
+
+cudaError_t init_fused(int n) { DDH_FDISPATCH(n, return init_fused_n<N>()); }
+
+cudaError_t launch_ka(const StepArgs &a, cudaStream_t st) {
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_fwd<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
+                                           ka_smem<N>(), FusedCfg<N>::CS, st, a));
+}
+cudaError_t launch_kb(const StepArgs &a, cudaStream_t st) {
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_cols<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
+                                           kb_smem<N>(), FusedCfg<N>::CS, st, a));
+}
+cudaError_t launch_kc(const StepArgs &a, cudaStream_t st) {
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_inv<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
+                                           kc_smem<N>(), FusedCfg<N>::CS, st, a));
+}
+
+}  // namespace ddh

@@ -6,6 +6,7 @@
 //   Normalize (Eq. 4), RemoveTipTilt, Eq. 3
 //   (P:183-187), A_phi^H, EM (R1-R12).
 #include "ddh_kernels.h"
+#include "ddh_common.cuh"
 #include "ddh_fft.cuh"
 
 #include <math.h>
@@ -32,40 +33,6 @@ int k0_blocks(int n) {
 
 // ------------------------------------------------------------- reductions
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Deterministic block sum of K doubles (fixed shuffle tree + fixed warp order).
-// Result valid in thread 0.  sh: >= 32*K doubles of shared memory.
-template <int K>
-__device__ __forceinline__ void block_sum(double (&v)[K], double *sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) sh[warp * K + k] = v[k];
-  }
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double x = lane < nw ? sh[lane * K + k] : 0.0;
-      v[k] = warp_sum(x);
-    }
-  }
-  __syncthreads();
-}
-
 // Warp 0 only: per-stream totals of the K0 partials -> out[0..4]
 // (sum re y, sum im y, sum phi, sum phi x, sum phi y) in fixed order.
 __device__ __forceinline__ void reduce_part0(const double *__restrict__ part0, int nb0, int s, double *out) {
@@ -88,19 +55,6 @@ __device__ __forceinline__ double reduce_part1(const double *__restrict__ part1,
   double v = 0.0;
   for (int b = lane; b < nb1; b += 32) v += part1[(size_t)s * nb1 + b];
   return warp_sum(v);
-}
-
-// Plane coefficients c = Minv h of the RemoveTipTilt normal equations (R17).
-__device__ __forceinline__ void plane_from_sums(const double *sums, const double *minv, double *c) {
-  const double h0 = sums[2], h1 = sums[3], h2 = sums[4];
-  c[0] = minv[0] * h0 + minv[1] * h1 + minv[2] * h2;
-  c[1] = minv[3] * h0 + minv[4] * h1 + minv[5] * h2;
-  c[2] = minv[6] * h0 + minv[7] * h1 + minv[8] * h2;
-}
-
-__device__ __forceinline__ bool in_ap(const int2 *__restrict__ rs, int i, int j) {
-  const int2 s = __ldg(rs + i);
-  return j >= s.x && j < s.y;
 }
 
 // ---------------------------------------------------------------- K0: sums
@@ -322,69 +276,6 @@ __global__ void __launch_bounds__(RowCfg<N>::H *(N / FftPlan<N>::E)) k3a_rows_in
 
 // ------------------------------------------------------------ r-ICD (K2b)
 
-// qGGMRF surrogate weight rho'(D)/(2D) / (1/(2 sig^2)) (R6):
-// (1/(1+t)) (1 - (2-q) t / (2(1+t))),  t = |D/(T sig)|^(2-q).
-__device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
-  const float a = fabsf(d) * inv_Tsig;
-  const float t = a > 0.f ? exp2f(tmq * log2f(a)) : 0.f;
-  const float inv = 1.f / (1.f + t);
-  return inv * (1.f - 0.5f * tmq * t * inv);
-}
-
-__device__ __forceinline__ double rsurr(double x, double q, double B, double S) {
-  return log(x) + q / x + B * x * x - 2.0 * S * x;
-}
-
-// Newton polish of a root of g(x) = 2B x^3 - 2S x^2 + x - q (guarded).
-__device__ __forceinline__ double polish(double x, double q, double B, double S) {
-#pragma unroll
-  for (int it = 0; it < 2; ++it) {
-    const double g = ((2.0 * B * x - 2.0 * S) * x + 1.0) * x - q;
-    const double gp = (6.0 * B * x - 4.0 * S) * x + 1.0;
-    if (gp == 0.0) break;
-    const double dx = g / gp;
-    if (!(fabs(dx) <= 1e-2 * fabs(x) + 1e-30)) break;
-    x -= dx;
-  }
-  return x;
-}
-
-// Exact minimiser over x >= r_min of f(x) = log x + q/x + B x^2 - 2 S x (R9):
-// stationary points are the real roots of 2B x^3 - 2S x^2 + x - q; with one
-// real root it is the unique local minimum, with three the outer two are the
-// local minima (f' = g/x^2).  Candidates clamped to r_min; ties within
-// 1e-12 (1+|f|) go to the candidate nearest the current value.  FP64.
-__device__ double r_minimise(double rc, double q, double B, double S, double r_min) {
-  const double a2 = -S / B, a1 = 0.5 / B, a0 = -0.5 * q / B;
-  const double a23 = a2 / 3.0;
-  const double p = a1 - a2 * a23;
-  const double qq = (2.0 * a23 * a23 - a1) * a23 + a0;  // 2 a2^3/27 - a2 a1/3 + a0
-  const double disc = 0.25 * qq * qq + p * p * p / 27.0;
-  if (disc >= 0.0) {
-    const double sq = sqrt(disc);
-    const double m = cbrt(0.5 * fabs(qq) + sq);
-    const double Au = qq > 0.0 ? -m : m;
-    const double tr = Au != 0.0 ? Au - p / (3.0 * Au) : 0.0;
-    double x = polish(tr - a23, q, B, S);
-    return x > r_min ? x : r_min;
-  }
-  const double m = 2.0 * sqrt(-p / 3.0);
-  double arg = 3.0 * qq / (p * m);
-  arg = fmin(1.0, fmax(-1.0, arg));
-  const double th = acos(arg) / 3.0;
-  const double t0 = m * cos(th);                          // largest root
-  const double t2 = m * cos(th + 2.0943951023931957);     // smallest root (th + 2pi/3)
-  double xh = polish(t0 - a23, q, B, S);
-  double xl = polish(t2 - a23, q, B, S);
-  xh = xh > r_min ? xh : r_min;
-  xl = xl > r_min ? xl : r_min;
-  const double fh = rsurr(xh, q, B, S), fl = rsurr(xl, q, B, S);
-  const double fm = fmin(fh, fl);
-  const double tol = 1e-12 * (1.0 + fabs(fm));
-  if (fabs(fh - fl) <= tol) return fabs(xh - rc) <= fabs(xl - rc) ? xh : xl;
-  return fh < fl ? xh : xl;
-}
-
 // grid (N/tile, N/tile, sc), block 256.  One 4-colour sweep (R8) over a tile
 // with a halo of 4 (periodic): after colour phase k the values at distance >= k
 // from the region edge equal those of the global colour-ordered sweep.
@@ -416,7 +307,7 @@ __global__ void __launch_bounds__(kIcdThreads) k2b_ricd(IcdArgs A) {
   }
   __syncthreads();
   if (A.prior && !degenerate) {
-    const double rmin = A.r_min;
+    const float rmin = A.r_min;
     const float b0 = A.b0;
     const int half = R / 2;
     for (int c = 0; c < 4; ++c) {
@@ -429,15 +320,14 @@ __global__ void __launch_bounds__(kIcdThreads) k2b_ricd(IcdArgs A) {
         float B = 0.f, S = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int di = (k < 4) ? ((k == 0) ? -1 : (k == 1) ? 1 : 0) : ((k < 6) ? -1 : 1);
-          const int dj = (k < 4) ? ((k == 2) ? -1 : (k == 3) ? 1 : 0) : ((k & 1) ? 1 : -1);
-          const float bw = (k < 4) ? (1.f / 6.f) : (1.f / 12.f);
+          const int di = nb_di(k), dj = nb_dj(k);
+          const float bw = nb_w(k);
           const float rj = rs[(li + di) * RW + lj + dj];
           const float bt = bw * b0 * qgg_w(ri - rj, A.inv_Tsig, A.two_minus_q);
           B += bt;
           S = fmaf(bt, rj, S);
         }
-        rs[li * RW + lj] = (float)r_minimise(ri, qs[li * RW + lj], B, S, rmin);
+        rs[li * RW + lj] = r_update(ri, qs[li * RW + lj], B, S, rmin);
       }
       __syncthreads();
     }
@@ -454,15 +344,6 @@ __global__ void __launch_bounds__(kIcdThreads) k2b_ricd(IcdArgs A) {
 }
 
 // ---------------------------------------------------------- phi-ICD (K3b)
-
-__device__ __forceinline__ float wrap_pi(float x) {
-  // (-pi, pi]
-  const float twopi = 6.283185307179586f;
-  float y = x - twopi * rintf(x * 0.15915494309189535f);
-  if (y <= -3.14159265358979f) y += twopi;
-  if (y > 3.14159265358979f) y -= twopi;
-  return y;
-}
 
 // grid (N/tile, N/tile, sc), block 256, dynamic smem 3 R^2 floats.  One
 // 4-colour sweep of the GMRF phi update (R10-R11), free boundary.  The symmetric
@@ -534,32 +415,19 @@ __global__ void __launch_bounds__(kIcdThreads) k3b_phiicd(IcdArgs A) {
       if (li < lo || li >= hi || lj < lo || lj >= hi) continue;
       const int gi = i0 - kIcdHalo + li, gj = j0 - kIcdHalo + lj;
       if (gi < 0 || gi >= n || gj < 0 || gj >= n) continue;
-      const float phi = ps[li * RW + lj];
-      const float cv = cs[li * RW + lj];
-      const float x0 = wrap_pi(phi - ts[li * RW + lj]);
-      const float tt = phi - x0;
-      float outv;
+      float nb = 0.f, sb = 0.f;
       if (A.prior) {
-        const float x2 = x0 * x0;
-        const float sc = fabsf(x0) < 1e-3f ? 1.f - x2 * (1.f / 6.f) + x2 * x2 * (1.f / 120.f) : sinf(x0) / x0;
-        float nb = 0.f, sb = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          const int di = (k < 4) ? ((k == 0) ? -1 : (k == 1) ? 1 : 0) : ((k < 6) ? -1 : 1);
-          const int dj = (k < 4) ? ((k == 2) ? -1 : (k == 3) ? 1 : 0) : ((k & 1) ? 1 : -1);
-          const float bw = (k < 4) ? (1.f / 6.f) : (1.f / 12.f);
+          const int di = nb_di(k), dj = nb_dj(k);
           const int ni = gi + di, nj = gj + dj;
           if (ni >= 0 && ni < n && nj >= 0 && nj < n) {
-            nb = fmaf(bw, ps[(li + di) * RW + lj + dj], nb);
-            sb += bw;
+            nb = fmaf(nb_w(k), ps[(li + di) * RW + lj + dj], nb);
+            sb += nb_w(k);
           }
         }
-        const float num = fmaf(cv * sc, tt, w * nb);
-        const float den = fmaf(cv, sc, w * sb);
-        outv = den != 0.f ? num / den : phi;
-      } else {
-        outv = cv > 0.f ? tt : phi;
       }
+      const float outv = phi_update(ps[li * RW + lj], cs[li * RW + lj], ts[li * RW + lj], nb, sb, w, A.prior != 0);
       ps[li * RW + lj] = outv;
     }
     __syncthreads();

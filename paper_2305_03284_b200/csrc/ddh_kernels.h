@@ -45,6 +45,14 @@ struct StepArgs {
   float s2, r_min;        // noise variance, r floor
   float P;                // N*N
   double minv[9];         // inverse of the aperture plane normal matrix
+  // fused (cluster) path
+  double *stats;          // [sc][5]: mu re, mu im, plane c0, c1, c2 (written by KA)
+  float *phi_out;         // KC: phi after the M-step [sc][N][N]
+  float *phi_copy, *r_copy;  // optional user outputs [sc][N][N] or null
+  int r_prior;            // qGGMRF on
+  float r_b0, r_inv_Tsig, r_tmq;  // 1/(2 sig_r^2), 1/(T sig_r), 2 - q
+  int phi_prior;          // GMRF on
+  float phi_w;            // 1/sig_phi^2
 };
 
 struct IcdArgs {
@@ -93,6 +101,14 @@ cudaError_t launch_ricd(const IcdArgs &a, int sc, cudaStream_t st);
 cudaError_t launch_phiicd(const IcdArgs &a, int sc, cudaStream_t st);
 cudaError_t launch_fill(float *p, float v, size_t count, cudaStream_t st);
 cudaError_t launch_strehl(const StrehlArgs &a, int B, cudaStream_t st);
+// cluster-fused EM iteration (N <= 512): KA rows+stats, KB cols+E+r-ICD, KC rows+phi-ICD
+bool fused_supported(int n);
+int fused_cluster(int n);  // CTAs per stream (= nb1 of the fused path)
+cudaError_t init_fused(int n);
+cudaError_t launch_ka(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_kb(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_kc(const StepArgs &a, cudaStream_t st);
+
 cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
                               cudaStream_t st);
 

@@ -48,10 +48,10 @@ def oracle_params(n, diam=None, **kw):
     return p
 
 
-def gpu_kwargs(p: O.OracleParams):
+def gpu_kwargs(p: O.OracleParams, unfused=False):
     return dict(aperture_diam=p.aperture_diam, noise_var=p.noise_var, lam=p.lam, alpha=p.alpha, n_k=p.n_k, r_min=p.r_min, r_sigma=p.r_sigma,
                 r_T=p.r_T, r_q=p.r_q, phi_sigma=p.phi_sigma, icd_sweeps=p.icd_sweeps, boot_period=p.boot_period,
-                boot_alpha=p.boot_alpha, flags=0 if p.tiptilt else 1)
+                boot_alpha=p.boot_alpha, flags=(0 if p.tiptilt else 1) | (2 if unfused else 0))
 
 
 def tie_mask(gaps, thr=1e-6, rad=2):
@@ -168,7 +168,7 @@ def test_phiicd_stage_parity(n, prior):
 # -------------------------------------------------------------- one step
 
 
-def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, **frame_over):
+def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, unfused=False, **frame_over):
     y, ph, c = frames(n, S, seed_frames, cfg, **frame_over)
     a = O.aperture_of(p)
     # a realistic state: oracle bootstrap on frame 0, rounded to FP32
@@ -178,7 +178,7 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, **frame_
     r32 = orc.r.astype(np.float32)
     p32 = orc.phi.astype(np.float32)
     orc.set_state(r32, p32, 1)
-    ctx = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(p))
+    ctx = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(p, unfused))
     ctx.set_state(torch.from_numpy(r32).to(DEV), torch.from_numpy(p32).to(DEV), 1)
     yt = torch.from_numpy(y[1:2]).to(DEV)
     phi_o = torch.empty((1, S, n, n), device=DEV)
@@ -206,28 +206,35 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, **frame_
     return worst
 
 
-@pytest.mark.parametrize("n,S,chunk", [(64, 2, 0), (128, 3, 2), (256, 2, 0)])
-def test_step_parity_priors_on(n, S, chunk):
+PATHS = [pytest.param(False, id="fused"), pytest.param(True, id="unfused")]
+
+
+@pytest.mark.parametrize("unfused", PATHS)
+@pytest.mark.parametrize("n,S,chunk", [(64, 2, 0), (128, 3, 2), (256, 2, 0), (512, 1, 0)])
+def test_step_parity_priors_on(n, S, chunk, unfused):
     p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0))
-    _step_parity(n, S, p, chunk=chunk)
+    _step_parity(n, S, p, chunk=chunk, unfused=unfused, pre_boot=8 if n <= 256 else 2)
 
 
-def test_step_parity_priors_off():
+@pytest.mark.parametrize("unfused", PATHS)
+def test_step_parity_priors_off(unfused):
     n = 64
     p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0), r_sigma=0.0, phi_sigma=0.0)
-    _step_parity(n, 2, p)
+    _step_parity(n, 2, p, unfused=unfused)
 
 
-def test_step_parity_nk2_two_sweeps_no_tiptilt():
+@pytest.mark.parametrize("unfused", PATHS)
+def test_step_parity_nk2_two_sweeps_no_tiptilt(unfused):
     n = 128
     p = oracle_params(n, noise_var=0.2, n_k=2, icd_sweeps=2, tiptilt=False)
-    _step_parity(n, 2, p)
+    _step_parity(n, 2, p, unfused=unfused)
 
 
-def test_step_parity_masked_aperture():
+@pytest.mark.parametrize("unfused", PATHS)
+def test_step_parity_masked_aperture(unfused):
     n = 64
     p = oracle_params(n, diam=50, noise_var=0.15)
-    _step_parity(n, 2, p)
+    _step_parity(n, 2, p, unfused=unfused)
 
 
 # -------------------------------------------------- bootstrap and static
@@ -421,4 +428,28 @@ def test_kernel_launch_count_and_empty_call():
     assert ctx.kernel_launches == l0
     y, _, _ = frames(n, S, 1)
     ctx.step(torch.from_numpy(y).to(DEV))
-    assert ctx.kernel_launches - l0 == 6  # K0 K1 K2a K2b K3a K3b
+    assert ctx.kernel_launches - l0 == 3  # fused: KA KB KC
+    u = DDH(n, S, noise_var=0.1, flags=2)
+    l0 = u.kernel_launches
+    u.step(torch.from_numpy(y).to(DEV))
+    assert u.kernel_launches - l0 == 6  # unfused: K0 K1 K2a K2b K3a K3b
+
+
+def test_fused_and_unfused_paths_agree():
+    """The cluster-fused and the multi-pass kernels compute the same step (FP32
+    rounding order differs: compare at the parity tolerance, 3 frames)."""
+    n, S = 256, 2
+    y, _, _ = frames(n, S, 3)
+    yt = torch.from_numpy(y).to(DEV)
+    outs = []
+    for flags in (0, 2):
+        ctx = DDH(n, S, noise_var=0.2, flags=flags)
+        po = torch.empty((3, S, n, n), device=DEV)
+        ro = torch.empty_like(po)
+        ctx.step(yt, po, ro)
+        outs.append((po.cpu().numpy(), ro.cpu().numpy()))
+    a = O.aperture(n, n)
+    for t in range(3):
+        for s in range(S):
+            assert phi_err(outs[0][0][t, s], outs[1][0][t, s].astype(np.float64), a) < 1e-3
+            assert np.linalg.norm(outs[0][1][t, s] - outs[1][1][t, s]) / np.linalg.norm(outs[1][1][t, s]) < 1e-3
