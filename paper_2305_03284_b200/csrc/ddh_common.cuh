@@ -72,22 +72,24 @@ __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
 
 // ---- r M-step, one pixel (R9) -------------------------------------------
 // Minimiser over x >= r_min of f(x) = log x + q/x + B x^2 - 2 S x (B > 0).
-// f'(x) = g(x)/x^2 with g(x) = 2B x^3 - 2S x^2 + x - q, g(0) = -q < 0.
-// g is concave left of its inflection xi = S/(3B) and convex right of it, so:
-//  * a root left of xi exists iff g(xi) > 0; monotone Newton from 0 reaches it
-//    (concave, increasing: the iterates stay left of the root);
-//  * a root right of xi exists iff g(xi) <= 0, or the local minimum of g at
-//    x2 = (2S + sqrt(4S^2 - 6B))/(6B) is negative; monotone Newton from
-//    U = max(S/B, q) (where g >= 0) reaches it from the right.
-// These two roots are the local minima of f (the middle root, if any, is a
-// local maximum).  With both present the lower f wins (FP32 difference);
-// candidates are clamped to r_min.  No transcendental root formula, no FP64.
-__device__ __forceinline__ float g_of(float x, float B2, float S2, float q) {
+// f'(x) = g(x)/x^2 with g(x) = 2B x^3 - 2S x^2 + x - q, g(0) = -q < 0; g is
+// concave left of its inflection xi = S/(3B) and convex right of it.
+//  * If g has two positive stationary points x1 < xi < x2 (S > 0 and
+//    4S^2 > 6B): a small root exists iff g(x1) > 0 and lies in (0, x1)
+//    (concave, increasing: monotone Newton from 0, whose first iterate is q);
+//    a large root exists iff g(x2) < 0 and lies in (x2, U], U = max(S/B, q)
+//    with g(U) >= 0 (convex, increasing: monotone Newton from U).  Both
+//    present: three roots, the middle one a local maximum of f.
+//  * Otherwise g increases on (0, inf): one root, left of xi iff g(xi) > 0.
+// The small and large roots are the local minima of f; with both present the
+// lower f wins (FP32 difference).  Candidates are clamped to r_min.  No
+// transcendental root formula and no FP64 on this path.
+__host__ __device__ __forceinline__ float g_of(float x, float B2, float S2, float q) {
   return fmaf(fmaf(fmaf(B2, x, -S2), x, 1.f), x, -q);
 }
-__device__ __forceinline__ float dg_of(float x, float B6, float S4) { return fmaf(fmaf(B6, x, -S4), x, 1.f); }
+__host__ __device__ __forceinline__ float dg_of(float x, float B6, float S4) { return fmaf(fmaf(B6, x, -S4), x, 1.f); }
 
-__device__ __forceinline__ float newton_root(float x, float B2, float S2, float B6, float S4, float q) {
+__host__ __device__ __forceinline__ float newton_root(float x, float B2, float S2, float B6, float S4, float q) {
 #pragma unroll 1
   for (int it = 0; it < 16; ++it) {
     const float g = g_of(x, B2, S2, q);
@@ -100,18 +102,19 @@ __device__ __forceinline__ float newton_root(float x, float B2, float S2, float 
   return x;
 }
 
-__device__ __forceinline__ float r_update(float rc, float q, float B, float S, float r_min) {
+__host__ __device__ __forceinline__ float r_update(float rc, float q, float B, float S, float r_min) {
   const float B2 = 2.f * B, S2 = 2.f * S, B6 = 6.f * B, S4 = 4.f * S;
-  const float xi = S / (3.f * B);
-  const float gi = xi > 0.f ? g_of(xi, B2, S2, q) : -q;
-  const bool has_small = gi > 0.f;
-  bool has_large = !has_small;
-  if (has_small) {
-    const float disc = 4.f * S * S - 6.f * B;
-    if (disc > 0.f) {
-      const float x2 = (2.f * S + sqrtf(disc)) / B6;
-      has_large = g_of(x2, B2, S2, q) < 0.f;
-    }
+  const float disc = 4.f * S * S - 6.f * B;
+  bool has_small, has_large;
+  if (S > 0.f && disc > 0.f) {
+    const float x2 = (2.f * S + sqrtf(disc)) / B6;
+    const float x1 = 1.f / (B6 * x2);  // x1 x2 = 1/(6B)
+    has_small = g_of(x1, B2, S2, q) > 0.f;
+    has_large = g_of(x2, B2, S2, q) < 0.f;
+  } else {
+    const float xi = S / (3.f * B);
+    has_small = xi > 0.f && g_of(xi, B2, S2, q) > 0.f;
+    has_large = !has_small;
   }
   float xs = 0.f, xl = 0.f;
   if (has_small) xs = newton_root(q, B2, S2, B6, S4, q);  // first Newton step from 0 is x = q
