@@ -338,11 +338,7 @@ def ctx_chunk(ctx):
     n = ctx.n
     if ctx.params.chunk_streams > 0:
         return min(ctx.params.chunk_streams, ctx.S)
-    lim = max(1, int(48 * 1024 * 1024 // (32 * n * n)))
-    sc = 1
-    while sc * 2 <= lim:
-        sc *= 2
-    return min(sc, ctx.S)
+    return min(max(1, int(2 * 1024 ** 3 // (40 * n * n))), ctx.S)
 
 
 def quick_parity(ctx, y_dev, y_host, t, n, nv, dev):

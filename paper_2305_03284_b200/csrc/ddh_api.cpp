@@ -151,6 +151,7 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
     a.r_inv_Tsig = (float)(1.0 / (c->p.r_T * c->p.r_sigma));
     a.r_tmq = (float)(2.0 - c->p.r_q);
   }
+  a.sweeps = c->p.icd_sweeps;
   a.phi_prior = c->p.phi_sigma > 0 ? 1 : 0;
   if (a.phi_prior) a.phi_w = (float)(1.0 / (c->p.phi_sigma * c->p.phi_sigma));
   return a;
@@ -436,12 +437,12 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   c->nb1 = n / ddh::row_block_rows(n);
   c->strehl_nb = n / ddh::col_block_cols(n);
   // launch group: keep the per-group workspace (~32 B/px) L2-resident
+  // launch group: all streams up to a 2 GiB workspace cap (~24-40 B/px per
+  // stream); one launch per kernel per step keeps the grids large
   int sc = p.chunk_streams;
   if (sc <= 0) {
-    const double bytes = 32.0 * (double)c->P;
-    int lim = (int)std::max(1.0, std::floor(48.0 * 1024 * 1024 / bytes));
-    sc = 1;
-    while (sc * 2 <= lim) sc *= 2;
+    const double bytes = 40.0 * (double)c->P;
+    sc = (int)std::max(1.0, std::floor(2.0 * 1024 * 1024 * 1024 / bytes));
   }
   c->sc = std::min(sc, c->S);
   const size_t S = c->S, P = c->P, SC = c->sc;

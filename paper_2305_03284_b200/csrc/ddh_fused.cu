@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_fwd(StepArgs A) {
     if (in_ap(A.rowspan, i, j)) {
       const float p = ph[k] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
       float sn, cs;
-      sincosf(p, &sn, &cs);
+      __sincosf(fmaf(-6.283185307179586f, rintf(p * 0.15915494309189535f), p), &sn, &cs);  // |arg| <= pi
       z = make_float2(dr * cs + di * sn, di * cs - dr * sn);  // (y - mu) e^{-j phi'}
       if ((i + j) & 1) z = make_float2(-z.x, -z.y);
     }
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
       const float rp = A.r_state[g];
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
-      const float w = r0 / (r0 + A.s2);
+      const float w = __fdividef(r0, r0 + A.s2);
       const float2 mu = make_float2(w * u.x, w * u.y);
       const float qv = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
       if (SPILL) {
@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
   if (icd) {
     float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
     float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
-    for (int c = 0; c < 4; ++c) {
+    for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
+      const int c = cc & 3;
       cl.sync();
       for (int i = tid; i < N; i += NT) {
         rS[i * RP] = left[i * RP + W];
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_inv(StepArgs A) {
         const float2 y = A.y[off + (size_t)i * N + j];
         const float2 yh = make_float2(kappa * (y.x - mur), kappa * (y.y - mui));
         const float2 z = make_float2(yh.x * f.x + yh.y * f.y, yh.y * f.x - yh.x * f.y);  // yh conj(f)
-        c = two_s2 * hypotf(z.x, z.y);
+        c = two_s2 * sqrtf(fmaf(z.x, z.x, z.y * z.y));
         th = atan2f(z.y, z.x);
       }
       creg[k * 4 + q4] = c;
@@ -378,6 +379,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_inv(StepArgs A) {
   if (prior) {
     const float *up = rank > 0 ? cl.map_shared_rank(phS, rank - 1) : nullptr;
     const float *dn = rank < CS - 1 ? cl.map_shared_rank(phS, rank + 1) : nullptr;
+#pragma unroll 1
+    for (int sw = 0; sw < A.sweeps; ++sw)
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       cl.sync();

@@ -53,6 +53,7 @@ struct StepArgs {
   float r_b0, r_inv_Tsig, r_tmq;  // 1/(2 sig_r^2), 1/(T sig_r), 2 - q
   int phi_prior;          // GMRF on
   float phi_w;            // 1/sig_phi^2
+  int sweeps;             // ICD colour sweeps per M-step (R8)
 };
 
 struct IcdArgs {
