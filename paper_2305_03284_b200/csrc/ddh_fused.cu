@@ -41,7 +41,7 @@ template <int N> struct FusedCfg {
   static constexpr int NT = H * (N / E);          // threads per CTA (all three kernels)
   static constexpr int EPT = H * N / NT;          // pixels per thread (= E)
   static constexpr int RP = W + 2;                // pitch of the r-ICD slab (1-column halos)
-  static constexpr bool SPILL = (N >= 512);       // KB: r0/q through global scratch (smem limit)
+  static constexpr int MINB = NT >= 1024 ? 1 : (NT >= 256 ? 4 : 8);  // CTAs/SM for __launch_bounds__
 };
 
 bool fused_supported(int n) { return n == 64 || n == 128 || n == 256 || n == 512; }
@@ -50,9 +50,7 @@ int fused_cluster(int n) { return n <= 128 ? 8 : 16; }
 template <int N> __host__ __device__ constexpr size_t ka_smem() { return (size_t)(FusedCfg<N>::H * (N + 1) + N) * sizeof(float2); }
 template <int N> __host__ __device__ constexpr size_t kb_smem() {
   using C = FusedCfg<N>;
-  const size_t tile = (size_t)N * C::W * sizeof(float2);
-  const size_t rq = (size_t)2 * N * C::RP * sizeof(float);
-  return (C::SPILL ? (tile > rq ? tile : rq) : tile + rq) + (size_t)N * sizeof(float2);
+  return (size_t)N * C::W * sizeof(float2) + (size_t)N * C::RP * sizeof(float) + (size_t)N * sizeof(float2);
 }
 template <int N> __host__ __device__ constexpr size_t kc_smem() {
   using C = FusedCfg<N>;
@@ -64,7 +62,7 @@ template <int N> __host__ __device__ constexpr size_t kc_smem() {
 // ------------------------------------------------------------------- KA
 
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_fwd(StepArgs A) {
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fwd(StepArgs A) {
   using C = FusedCfg<N>;
   constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
   cg::cluster_group cl = cg::this_cluster();
@@ -158,18 +156,20 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_fwd(StepArgs A) {
 
 // ------------------------------------------------------------------- KB
 
+// Column slab of W columns x N rows.  Order: column DFT -> Eq. 3 + E-step
+// (r0 -> rS, q -> registers, chi mu -> tile) -> r-ICD over rS (each thread
+// updates exactly the pixels whose q it holds) -> write r -> inverse column
+// DFT of the tile -> write the spectrum slab.
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(StepArgs A) {
   using C = FusedCfg<N>;
   constexpr int W = C::W, NT = C::NT, CS = C::CS, EPT = C::EPT, RP = C::RP, P = N * N;
-  constexpr bool SPILL = C::SPILL;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   extern __shared__ float2 sm[];
-  float2 *tile = sm;  // [N][W]
-  float *rS = SPILL ? reinterpret_cast<float *>(sm) : reinterpret_cast<float *>(sm + N * W);  // [N][RP]
-  float *qS = rS + N * RP;
-  float2 *tw = SPILL ? sm + (kb_smem<N>() / sizeof(float2) - N) : reinterpret_cast<float2 *>(qS + N * RP);
+  float2 *tile = sm;                                       // [N][W]
+  float *rS = reinterpret_cast<float *>(sm + N * W);       // [N][RP], columns 0 and W+1 = halos
+  float2 *tw = reinterpret_cast<float2 *>(rS + N * RP);
   __shared__ double st[1];
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
   const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
   block_fft<N, -1>(tile + tid % W, true, tid / W, W, tw);
   const bool warm = A.warm && !degenerate;
+  float qreg[EPT];
   // Eq. 3 + E-step over 2x2 pixel blocks (one pixel of each colour per block)
 #pragma unroll
   for (int k = 0; k < EPT / 4; ++k) {
@@ -205,85 +206,76 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
       const float sg = ((ki + kj) & 1) ? -scale : scale;
       const float2 X = tile[ki * W + lc];
       const float2 u = make_float2(X.x * sg, X.y * sg);
-      const size_t g = off + (size_t)ki * N + kj;
-      const float rp = A.r_state[g];
+      const float rp = A.r_state[off + (size_t)ki * N + kj];
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
       const float w = __fdividef(r0, r0 + A.s2);
       const float2 mu = make_float2(w * u.x, w * u.y);
-      const float qv = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
-      if (SPILL) {
-        A.rinit[g] = r0;
-        A.q[g] = qv;
-      } else {
-        rS[ki * RP + lc + 1] = r0;
-        qS[ki * RP + lc + 1] = qv;
-      }
+      qreg[k * 4 + q4] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+      rS[ki * RP + lc + 1] = r0;
       const float cs = ((ki + kj) & 1) ? -1.f : 1.f;
       tile[ki * W + lc] = make_float2(cs * mu.x, cs * mu.y);
     }
   }
+  const bool icd = A.r_prior && !degenerate;  // uniform over the cluster (one stream)
+  if (icd) {
+    float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
+    float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
+#pragma unroll 1
+    for (int sw = 0; sw < A.sweeps; ++sw) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        cl.sync();
+        for (int i = tid; i < N; i += NT) {
+          rS[i * RP] = left[i * RP + W];
+          rS[i * RP + W + 1] = right[i * RP + 1];
+        }
+        __syncthreads();
+        const int ci = c >> 1, cj = c & 1;
+#pragma unroll
+        for (int k = 0; k < EPT / 4; ++k) {
+          const int b = tid + k * NT;
+          const int br = b / (W / 2), bc = b % (W / 2);
+          const int ki = 2 * br + ci, lj = 2 * bc + cj + 1;
+          const float ri = rS[ki * RP + lj];
+          float B = 0.f, S = 0.f;
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            const int ni = (ki + nb_di(m)) & (N - 1);  // periodic rows (full columns in the CTA)
+            const float rj = rS[ni * RP + lj + nb_dj(m)];
+            const float bt = nb_w(m) * qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
+            B += bt;
+            S = fmaf(bt, rj, S);
+          }
+          rS[ki * RP + lj] = r_update(ri, qreg[k * 4 + c], A.r_b0 * B, A.r_b0 * S, A.r_min);
+        }
+      }
+    }
+  } else if (!degenerate) {  // prior off: r = max(q, r_min)
+#pragma unroll
+    for (int k = 0; k < EPT / 4; ++k) {
+      const int b = tid + k * NT;
+      const int br = b / (W / 2), bc = b % (W / 2);
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4)
+        rS[(2 * br + (q4 >> 1)) * RP + 2 * bc + (q4 & 1) + 1] = fmaxf(qreg[k * 4 + q4], A.r_min);
+    }
+  }
   __syncthreads();
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int i = idx / W, c = idx % W;
+    const float v = rS[i * RP + c + 1];
+    const size_t g = off + (size_t)i * N + c0 + c;
+    A.r_state[g] = v;
+    if (A.r_copy) A.r_copy[g] = v;
+  }
   block_fft<N, +1>(tile + tid % W, true, tid / W, W, tw);
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W] = tile[idx];
-  }
-  if (SPILL) {
-    __syncthreads();  // tile dead: reuse as rS / qS
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-      const int idx = tid + k * NT;
-      const int i = idx / W, c = idx % W;
-      const size_t g = off + (size_t)i * N + c0 + c;
-      rS[i * RP + c + 1] = A.rinit[g];
-      qS[i * RP + c + 1] = A.q[g];
-    }
-  }
-  __syncthreads();
-  const bool icd = A.r_prior && !degenerate;  // uniform over the cluster (one stream)
-  if (icd) {
-    float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
-    float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
-    for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
-      const int c = cc & 3;
-      cl.sync();
-      for (int i = tid; i < N; i += NT) {
-        rS[i * RP] = left[i * RP + W];
-        rS[i * RP + W + 1] = right[i * RP + 1];
-      }
-      __syncthreads();
-      const int ci = c >> 1, cj = c & 1;
-#pragma unroll
-      for (int k = 0; k < EPT / 4; ++k) {
-        const int b = tid + k * NT;
-        const int br = b / (W / 2), bc = b % (W / 2);
-        const int ki = 2 * br + ci, lj = 2 * bc + cj + 1;
-        const float ri = rS[ki * RP + lj];
-        float B = 0.f, S = 0.f;
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const int ni = (ki + nb_di(m)) & (N - 1);  // periodic rows (full columns in the CTA)
-          const float rj = rS[ni * RP + lj + nb_dj(m)];
-          const float bt = nb_w(m) * A.r_b0 * qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
-          B += bt;
-          S = fmaf(bt, rj, S);
-        }
-        rS[ki * RP + lj] = r_update(ri, qS[ki * RP + lj], B, S, A.r_min);
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int k = 0; k < EPT; ++k) {
-    const int idx = tid + k * NT;
-    const int i = idx / W, c = idx % W;
-    float v = rS[i * RP + c + 1];
-    if (!A.r_prior && !degenerate) v = fmaxf(qS[i * RP + c + 1], A.r_min);  // prior off: max(q, r_min)
-    const size_t g = off + (size_t)i * N + c0 + c;
-    A.r_state[g] = v;
-    if (A.r_copy) A.r_copy[g] = v;
   }
   if (icd) cl.sync();  // neighbours may still read our slab (last halo copy)
 }
@@ -291,7 +283,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT) kf_cols(StepArgs A) {
 // ------------------------------------------------------------------- KC
 
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT) kf_rows_inv(StepArgs A) {
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_inv(StepArgs A) {
   using C = FusedCfg<N>;
   constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
   cg::cluster_group cl = cg::this_cluster();
