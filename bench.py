@@ -151,29 +151,19 @@ def time_oracle(y, cfg, n, nv, cores):
 
 
 def dist_setup(backend):
-    import torch.distributed as dist
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1 and not dist.is_initialized():
-        dist.init_process_group(backend=backend)
-    return ws, rank, local
+    from paper_2305_03284_b200 import sched
+    return sched.init(backend)
 
 
 def reduce_max(x, ws, device=None):
-    if ws == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([float(x)], device=device if device is not None else "cpu", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2305_03284_b200 import sched
+    return sched.max_over_ranks(x, device) if ws > 1 else x
 
 
 def barrier(ws):
+    from paper_2305_03284_b200 import sched
     if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
+        sched.barrier()
 
 
 def run_reference(args):
@@ -223,15 +213,17 @@ def run_ours(args):
 
     import synth
     from paper_2305_03284_b200 import DDH
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    from paper_2305_03284_b200 import sched
+    ws, rank, _ = sched.env_rank()
     cfg = synth.CONFIGS[args.config]
-    n, S, F = cfg["n"], cfg["streams"], min(args.frames, cfg["frames"])
+    n, F = cfg["n"], min(args.frames, cfg["frames"])
     nv = synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"])
     P = n * n
-    # ---- inputs (synthetic, distinct streams per rank), generated before CUDA init
+    # ---- weak scaling: cfg["streams"] streams per GPU; rank r owns global
+    # streams [first, first + S) (sched.shard of S * ws streams), seeds per stream
+    first, S = sched.shard(cfg["streams"] * ws, ws, rank)
     t0 = time.time()
-    y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=rank * S, want_phi=False)
+    y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=first, want_phi=False)
     gen_s = time.time() - t0
     ws, rank, local = dist_setup("nccl")
     torch.cuda.set_device(local)
