@@ -46,6 +46,10 @@ KERNEL_BYTES_PER_PX = {
     "k2b_ricd": 4 + 4 + 4,          # r_init, q -> r
     "k3a_rows_inv": 8 + 8 + 4 + 4,  # spectrum, y -> c, theta
     "k3b_phiicd": 4 + 4 + 4 + 4,    # phi, c, theta -> phi
+    # cluster-fused path
+    "kf_rows_fwd": 8 + 4 + 8,       # y, phi -> spectrum
+    "kf_cols": 8 + 4 + 4 + 8,       # spectrum, r -> r, spectrum
+    "kf_rows_inv": 8 + 8 + 4 + 4,   # spectrum, y, phi -> phi
 }
 STEP_BYTES_PER_PX = 24  # y in (8) + r in/out (8) + phi in/out (8)
 

@@ -165,9 +165,10 @@ int64_t ddh_frame_index(const ddh_ctx *c);
 
 /* ---- instrumentation: per-kernel device time (CUDA events on the ctx stream) ----
  * Kernel kinds: 0 K0 stats, 1 K1 rows_fwd, 2 K2a cols, 3 K2b r-ICD,
- * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl.  When enabled, every
- * launch of the ctx is bracketed by two events (a small added cost). */
-#define DDH_KIND_COUNT 8
+ * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
+ * 8 KA kf_rows_fwd, 9 KB kf_cols, 10 KC kf_rows_inv (cluster-fused path).
+ * When enabled, every launch of the ctx is bracketed by two events. */
+#define DDH_KIND_COUNT 11
 ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable);
 /* Synchronises the ctx stream and ADDS the accumulated totals since the last
  * read into ms[k] (milliseconds) and launches[k] (host arrays of

@@ -85,9 +85,10 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
       return fail((c), DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL };
+enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
-                                          "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl"};
+                                          "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
+                                          "kf_rows_fwd", "kf_cols", "kf_rows_inv"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind) {
@@ -269,9 +270,9 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
         a.status = (first && status) ? status + s0 : nullptr;
         a.r_copy = (last && r_out) ? r_out + so : nullptr;
         a.phi_copy = (last && phi_out) ? phi_out + so : nullptr;
-        DDH_LAUNCH(c, K_ROWS_FWD, ddh::launch_ka(a, c->st));
-        DDH_LAUNCH(c, K_COLS, ddh::launch_kb(a, c->st));
-        DDH_LAUNCH(c, K_ROWS_INV, ddh::launch_kc(a, c->st));
+        DDH_LAUNCH(c, K_KA, ddh::launch_ka(a, c->st));
+        DDH_LAUNCH(c, K_KB, ddh::launch_kb(a, c->st));
+        DDH_LAUNCH(c, K_KC, ddh::launch_kc(a, c->st));
         cur ^= 1;
       }
       continue;
