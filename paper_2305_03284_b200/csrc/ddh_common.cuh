@@ -71,10 +71,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
+  // (1/(1+t)) (1 - (2-q) t/(2(1+t))) = (1 + (q/2) t) / (1+t)^2
   const float a = fmaxf(fabsf(d) * inv_Tsig, 1e-30f);
   const float t = ex2_approx(tmq * __log2f(a));
-  const float inv = __fdividef(1.f, 1.f + t);
-  return inv * fmaf(-0.5f * tmq * t, inv, 1.f);
+  const float u = 1.f + t;
+  return fmaf(1.f - 0.5f * tmq, t, 1.f) * __fdividef(1.f, u * u);
 }
 
 // ---- r M-step, one pixel (R9) -------------------------------------------
@@ -131,6 +132,18 @@ __host__ __device__ __forceinline__ float newton_root(float x, float B2, float S
   return x;
 }
 
+// Three roots (both local minima present): the lower surrogate value wins.
+static __host__ __device__ __noinline__ float r_pick_two(float rc, float q, float B, float S, float r_min, float xs,
+                                                  float B2, float S2, float B6, float S4) {
+  const float xl = newton_root(fmaxf(S / B, q), B2, S2, B6, S4, q);
+  const float a = fmaxf(xs, r_min), b = fmaxf(xl, r_min);
+  // f(b) - f(a)
+  const float df = logf(b / a) + q * (a - b) / (a * b) + (b - a) * (B * (a + b) - 2.f * S);
+  const float tol = 1e-6f * (1.f + fabsf(logf(a)) + q / a);
+  if (fabsf(df) <= tol) return fabsf(a - rc) <= fabsf(b - rc) ? a : b;
+  return df < 0.f ? b : a;
+}
+
 __host__ __device__ __forceinline__ float r_update(float rc, float q, float B, float S, float r_min) {
   const float B2 = 2.f * B, S2 = 2.f * S, B6 = 6.f * B, S4 = 4.f * S;
   const float disc = 4.f * S * S - 6.f * B;
@@ -145,17 +158,12 @@ __host__ __device__ __forceinline__ float r_update(float rc, float q, float B, f
     has_small = xi > 0.f && g_of(xi, B2, S2, q) > 0.f;
     has_large = !has_small;
   }
-  float xs = 0.f, xl = 0.f;
-  if (has_small) xs = newton_root(q, B2, S2, B6, S4, q);  // first Newton step from 0 is x = q
-  if (has_large) xl = newton_root(fmaxf(S / B, q), B2, S2, B6, S4, q);
-  if (!has_large) return fmaxf(xs, r_min);
-  if (!has_small) return fmaxf(xl, r_min);
-  const float a = fmaxf(xs, r_min), b = fmaxf(xl, r_min);
-  // f(b) - f(a)
-  const float df = logf(b / a) + q * (a - b) / (a * b) + (b - a) * (B * (a + b) - 2.f * S);
-  const float tol = 1e-6f * (1.f + fabsf(logf(a)) + q / a);
-  if (fabsf(df) <= tol) return fabsf(a - rc) <= fabsf(b - rc) ? a : b;
-  return df < 0.f ? b : a;
+  // one Newton run per lane: the small root if it exists (from 0: first iterate
+  // q), else the large root (from max(S/B, q)); the second minimum only when
+  // both exist (rare; separate non-inlined path)
+  const float x = newton_root(has_small ? q : fmaxf(S / B, q), B2, S2, B6, S4, q);
+  if (has_small && has_large) return r_pick_two(rc, q, B, S, r_min, x, B2, S2, B6, S4);
+  return fmaxf(x, r_min);
 }
 
 // ---- phi M-step, one pixel (R10-R11) --------------------------------------

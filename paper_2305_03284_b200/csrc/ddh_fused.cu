@@ -222,9 +222,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
     float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
 #pragma unroll 1
-    for (int sw = 0; sw < A.sweeps; ++sw) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
+    for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
+      const int c = cc & 3;
+      {
         cl.sync();
         for (int i = tid; i < N; i += NT) {
           rS[i * RP] = left[i * RP + W];
@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
             B += bt;
             S = fmaf(bt, rj, S);
           }
-          rS[ki * RP + lj] = r_update(ri, qreg[k * 4 + c], A.r_b0 * B, A.r_b0 * S, A.r_min);
+          const float qv = c == 0 ? qreg[k * 4] : c == 1 ? qreg[k * 4 + 1] : c == 2 ? qreg[k * 4 + 2] : qreg[k * 4 + 3];
+          rS[ki * RP + lj] = r_update(ri, qv, A.r_b0 * B, A.r_b0 * S, A.r_min);
         }
       }
     }
@@ -372,9 +373,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     const float *up = rank > 0 ? cl.map_shared_rank(phS, rank - 1) : nullptr;
     const float *dn = rank < CS - 1 ? cl.map_shared_rank(phS, rank + 1) : nullptr;
 #pragma unroll 1
-    for (int sw = 0; sw < A.sweeps; ++sw)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
+      const int c = cc & 3;
       cl.sync();
       for (int j = tid; j < N; j += NT) {
         if (up) phS[j] = up[H * N + j];
@@ -396,7 +396,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
             sb += nb_w(m);
           }
         }
-        phS[li * N + j] = phi_update(phS[li * N + j], creg[k * 4 + c], treg[k * 4 + c], nb, sb, w, true);
+        const float cv = c == 0 ? creg[k * 4] : c == 1 ? creg[k * 4 + 1] : c == 2 ? creg[k * 4 + 2] : creg[k * 4 + 3];
+        const float tv = c == 0 ? treg[k * 4] : c == 1 ? treg[k * 4 + 1] : c == 2 ? treg[k * 4 + 2] : treg[k * 4 + 3];
+        phS[li * N + j] = phi_update(phS[li * N + j], cv, tv, nb, sb, w, true);
       }
     }
     __syncthreads();
