@@ -70,12 +70,27 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 1/x by one MUFU.RCP (relative error ~1 ulp; inputs here are normal numbers)
+__host__ __device__ __forceinline__ float rcp_approx(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return 1.f / x;
+#endif
+}
 __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
   // (1/(1+t)) (1 - (2-q) t/(2(1+t))) = (1 + (q/2) t) / (1+t)^2
   const float a = fmaxf(fabsf(d) * inv_Tsig, 1e-30f);
-  const float t = ex2_approx(tmq * __log2f(a));
+  const float t = ex2_approx(tmq * lg2_approx(a));
   const float u = 1.f + t;
-  return fmaf(1.f - 0.5f * tmq, t, 1.f) * __fdividef(1.f, u * u);
+  return fmaf(1.f - 0.5f * tmq, t, 1.f) * rcp_approx(u * u);
 }
 
 // ---- r M-step, one pixel (R9) -------------------------------------------
@@ -97,11 +112,7 @@ __host__ __device__ __forceinline__ float g_of(float x, float B2, float S2, floa
 }
 __host__ __device__ __forceinline__ float dg_of(float x, float B6, float S4) { return fmaf(fmaf(B6, x, -S4), x, 1.f); }
 
-#ifdef __CUDA_ARCH__
-#define DDH_FDIV(a, b) __fdividef((a), (b))
-#else
-#define DDH_FDIV(a, b) ((a) / (b))
-#endif
+#define DDH_FDIV(a, b) ((a) * rcp_approx(b))
 
 // Monotone Newton on g: three unrolled steps (enough for ~95% of pixels on the
 // BASELINE workloads, measured with tools/check_r_update.py) then a guarded
@@ -147,21 +158,24 @@ static __host__ __device__ __noinline__ float r_pick_two(float rc, float q, floa
 __host__ __device__ __forceinline__ float r_update(float rc, float q, float B, float S, float r_min) {
   const float B2 = 2.f * B, S2 = 2.f * S, B6 = 6.f * B, S4 = 4.f * S;
   const float disc = 4.f * S * S - 6.f * B;
+  const float iB = rcp_approx(B);
+  // (approximate x1, x2, xi only classify; near a boundary the two minima are
+  // within rounding of each other's surrogate value, so either choice is exact)
   bool has_small, has_large;
   if (S > 0.f && disc > 0.f) {
-    const float x2 = (2.f * S + sqrtf(disc)) / B6;
-    const float x1 = 1.f / (B6 * x2);  // x1 x2 = 1/(6B)
+    const float x2 = (2.f * S + sqrtf(disc)) * iB * (1.f / 6.f);
+    const float x1 = iB * (1.f / 6.f) * rcp_approx(x2);  // x1 x2 = 1/(6B)
     has_small = g_of(x1, B2, S2, q) > 0.f;
     has_large = g_of(x2, B2, S2, q) < 0.f;
   } else {
-    const float xi = S / (3.f * B);
+    const float xi = S * iB * (1.f / 3.f);
     has_small = xi > 0.f && g_of(xi, B2, S2, q) > 0.f;
     has_large = !has_small;
   }
   // one Newton run per lane: the small root if it exists (from 0: first iterate
   // q), else the large root (from max(S/B, q)); the second minimum only when
   // both exist (rare; separate non-inlined path)
-  const float x = newton_root(has_small ? q : fmaxf(S / B, q), B2, S2, B6, S4, q);
+  const float x = newton_root(has_small ? q : fmaxf(S * iB, q), B2, S2, B6, S4, q);
   if (has_small && has_large) return r_pick_two(rc, q, B, S, r_min, x, B2, S2, B6, S4);
   return fmaxf(x, r_min);
 }
@@ -183,10 +197,10 @@ __device__ __forceinline__ float phi_update(float phi, float c, float th, float 
   const float tt = phi - x0;
   if (!prior) return c > 0.f ? tt : phi;
   const float x2 = x0 * x0;
-  const float s = fabsf(x0) < 1e-3f ? fmaf(x2, fmaf(x2, 1.f / 120.f, -1.f / 6.f), 1.f) : __sinf(x0) / x0;
+  const float s = fabsf(x0) < 1e-3f ? fmaf(x2, fmaf(x2, 1.f / 120.f, -1.f / 6.f), 1.f) : __sinf(x0) * rcp_approx(x0);
   const float num = fmaf(c * s, tt, w * nb);
   const float den = fmaf(c, s, w * sb);
-  return den != 0.f ? num / den : phi;
+  return den != 0.f ? num * rcp_approx(den) : phi;
 }
 
 }  // namespace ddh

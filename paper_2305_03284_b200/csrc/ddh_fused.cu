@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       const float rp = A.r_state[off + (size_t)ki * N + kj];
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
-      const float w = __fdividef(r0, r0 + A.s2);
+      const float w = r0 * rcp_approx(r0 + A.s2);
       const float2 mu = make_float2(w * u.x, w * u.y);
       qreg[k * 4 + q4] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
       rS[ki * RP + lc + 1] = r0;
