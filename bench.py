@@ -234,7 +234,12 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     y_dev = torch.from_numpy(y_host).to(dev)
     stream = torch.cuda.current_stream(dev)
-    ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk)
+    extra = {}
+    if args.priors_off:  # diagnostic only (isolates the ICD cost); never the reported configuration
+        extra = dict(r_sigma=0.0, phi_sigma=0.0)
+    if args.unfused:
+        extra["flags"] = 2
+    ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk, **extra)
     K, W = args.steps, args.warmup
     for w in range(W):
         ctx.step(y_dev[w % F:w % F + 1])
@@ -429,6 +434,8 @@ def main():
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--priors-off", action="store_true", help="diagnostic: disable both priors")
+    ap.add_argument("--unfused", action="store_true", help="diagnostic: multi-pass kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
