@@ -28,8 +28,22 @@
 #include "ddh_kernels.h"
 
 #include <cooperative_groups.h>
+#include <cstdio>
 
 namespace cg = cooperative_groups;
+
+// Phase timestamps (instrumentation build only: -DDDH_PHASE_TIMING): thread 0
+// of rank-0 CTAs of streams 0..3 prints clock64() deltas at phase boundaries.
+#ifdef DDH_PHASE_TIMING
+#define DDH_T0() long long t_ph[12]; int n_ph = 0; if (threadIdx.x == 0) t_ph[n_ph++] = clock64();
+#define DDH_TS() do { if (threadIdx.x == 0 && n_ph < 12) t_ph[n_ph++] = clock64(); } while (0)
+#define DDH_TPRINT(tag) do { if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y < 4) { \
+    printf("%s s=%d", tag, (int)blockIdx.y); for (int k_ = 1; k_ < n_ph; ++k_) printf(" %lld", t_ph[k_] - t_ph[k_ - 1]); printf("\n"); } } while (0)
+#else
+#define DDH_T0()
+#define DDH_TS()
+#define DDH_TPRINT(tag)
+#endif
 
 namespace ddh {
 
@@ -174,6 +188,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
   const int c0 = rank * W;
+  DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   if (tid == 0) {
@@ -187,12 +202,14 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     tile[idx] = A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W];
   }
   __syncthreads();
+  DDH_TS();  // 1: loaded
   const double d2 = st[0];
   const bool degenerate = !(d2 > 0.0);
   if (A.status && rank == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
   const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
   block_fft<N, -1>(tile + tid % W, true, tid / W, W, tw);
+  DDH_TS();  // 2: forward column DFT
   const bool warm = A.warm && !degenerate;
   float qreg[EPT];
   // Eq. 3 + E-step over 2x2 pixel blocks (one pixel of each colour per block)
@@ -217,6 +234,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       tile[ki * W + lc] = make_float2(cs * mu.x, cs * mu.y);
     }
   }
+  DDH_TS();  // 3: Eq. 3 + E-step
   const bool icd = A.r_prior && !degenerate;  // uniform over the cluster (one stream)
   if (icd) {
     float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
@@ -263,6 +281,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     }
   }
   __syncthreads();
+  DDH_TS();  // 4: r-ICD
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
@@ -272,13 +291,18 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     A.r_state[g] = v;
     if (A.r_copy) A.r_copy[g] = v;
   }
+  DDH_TS();  // 5: r written
   block_fft<N, +1>(tile + tid % W, true, tid / W, W, tw);
+  DDH_TS();  // 6: inverse column DFT
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W] = tile[idx];
   }
+  DDH_TS();  // 7: spectrum stored
   if (icd) cl.sync();  // neighbours may still read our slab (last halo copy)
+  DDH_TS();  // 8: final cluster barrier
+  DDH_TPRINT("KB");
 }
 
 // ------------------------------------------------------------------- KC

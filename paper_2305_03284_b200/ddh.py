@@ -14,7 +14,7 @@ from typing import Optional
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libddh.so")
+LIB_PATH = os.environ.get("DDH_LIB") or os.path.join(_HERE, "lib", "libddh.so")
 
 DDH_F_NO_TIPTILT = 1
 

@@ -1,0 +1,28 @@
+"""Run one c3 step with the instrumented library and average the per-phase
+clock64 deltas printed by rank-0 CTAs (tools/build_timing.sh)."""
+import os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+code = r'''
+import sys, torch, numpy as np
+sys.path.insert(0, "%s")
+import synth
+from paper_2305_03284_b200 import DDH
+cfg = synth.CONFIGS["c3"]
+y, _ = synth.make_batch(cfg, streams=64, frames=3, want_phi=False)
+yd = torch.from_numpy(y).cuda()
+ctx = DDH(256, 64, noise_var=synth.recon_noise_var(256, 256, 5.0))
+for t in range(3):
+    ctx.step(yd[t:t+1]); torch.cuda.synchronize()
+''' % ROOT
+env = dict(os.environ, DDH_LIB=os.path.join(ROOT, "paper_2305_03284_b200/lib/timing/libddh_timing.so"))
+out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+lines = [l.split() for l in out.stdout.splitlines() if l[:2] in ("KA", "KB", "KC")]
+if not lines:
+    print(out.stdout[-2000:], out.stderr[-2000:])
+by = {}
+for l in lines[len(lines) // 3:]:  # skip the first frame (warm-up)
+    by.setdefault(l[0], []).append([int(x) for x in l[2:]])
+for k, rows in by.items():
+    import numpy as np
+    a = np.array(rows)
+    print(k, "mean cycles per phase:", " ".join(f"{v:.0f}" for v in a.mean(0)), " total", f"{a.sum(1).mean():.0f}")
