@@ -37,8 +37,10 @@ namespace cg = cooperative_groups;
 #ifdef DDH_PHASE_TIMING
 #define DDH_T0() long long t_ph[12]; int n_ph = 0; if (threadIdx.x == 0) t_ph[n_ph++] = clock64();
 #define DDH_TS() do { if (threadIdx.x == 0 && n_ph < 12) t_ph[n_ph++] = clock64(); } while (0)
-#define DDH_TPRINT(tag) do { if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y < 4) { \
-    printf("%s s=%d", tag, (int)blockIdx.y); for (int k_ = 1; k_ < n_ph; ++k_) printf(" %lld", t_ph[k_] - t_ph[k_ - 1]); printf("\n"); } } while (0)
+#define DDH_TPRINT(tag) do { if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y < 4) { long long d_[11]; \
+    for (int k_ = 0; k_ < 11; ++k_) d_[k_] = (k_ + 1 < n_ph) ? t_ph[k_ + 1] - t_ph[k_] : 0; \
+    printf("%s %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, d_[0], d_[1], d_[2], d_[3], d_[4], \
+           d_[5], d_[6], d_[7], d_[8], d_[9], d_[10]); } } while (0)
 #else
 #define DDH_T0()
 #define DDH_TS()

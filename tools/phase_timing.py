@@ -21,7 +21,7 @@ if not lines:
     print(out.stdout[-2000:], out.stderr[-2000:])
 by = {}
 for l in lines[len(lines) // 3:]:  # skip the first frame (warm-up)
-    by.setdefault(l[0], []).append([int(x) for x in l[2:]])
+    by.setdefault(l[0], []).append([int(x) for x in l[1:]])
 for k, rows in by.items():
     import numpy as np
     a = np.array(rows)
