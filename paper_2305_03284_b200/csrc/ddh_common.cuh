@@ -86,11 +86,13 @@ __host__ __device__ __forceinline__ float rcp_approx(float x) {
 #endif
 }
 __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
-  // (1/(1+t)) (1 - (2-q) t/(2(1+t))) = (1 + (q/2) t) / (1+t)^2
-  const float a = fmaxf(fabsf(d) * inv_Tsig, 1e-30f);
+  // (1/(1+t)) (1 - (2-q) t/(2(1+t))) = k/u + (1-k)/u^2,  u = 1+t, k = q/2 = 1 - tmq/2:
+  // 3 MUFU (lg2, ex2, rcp) + 6 FMA-pipe instructions
+  const float a = fmaf(fabsf(d), inv_Tsig, 1e-30f);
   const float t = ex2_approx(tmq * lg2_approx(a));
-  const float u = 1.f + t;
-  return fmaf(1.f - 0.5f * tmq, t, 1.f) * rcp_approx(u * u);
+  const float r = rcp_approx(1.f + t);
+  const float k = 1.f - 0.5f * tmq;
+  return fmaf(1.f - k, r, k) * r;
 }
 
 // ---- r M-step, one pixel (R9) -------------------------------------------

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
   const int i0 = rank * H;
+  DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   float ph[EPT];
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
       v[4] += (double)f * (double)(i - N / 2);
     }
   }
+  DDH_TS();  // 1: loaded + local sums
   block_sum<5>(v, red);
   if (tid == 0) {
 #pragma unroll
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   }
   cl.barrier_arrive();  // remote reads of `part` done (waited on before exit)
   __syncthreads();
+  DDH_TS();  // 2: cluster reduction
   double c[3] = {0, 0, 0};
   if (A.apply_plane) plane_from_sums(tot, A.minv, c);
   const double mu_r = tot[0] / P, mu_i = tot[1] / P;
@@ -160,14 +163,19 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   double a1[1] = {acc};
   block_sum<1>(a1, red);  // also orders the tile writes before the FFT
   if (tid == 0) A.part1[(size_t)s * CS + rank] = a1[0];
+  DDH_TS();  // 3: z, |y - mu|^2
   block_fft<N, -1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+  DDH_TS();  // 4: row DFT
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1);
     A.cbuf[off + (size_t)(i0 + r) * N + j] = tile[r * PITCH + j];
   }
+  DDH_TS();  // 5: stored
   cl.barrier_wait();
+  DDH_TS();  // 6: exit barrier
+  DDH_TPRINT("KA");
 }
 
 // ------------------------------------------------------------------- KB
@@ -203,6 +211,15 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     const int idx = tid + k * NT;
     tile[idx] = A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W];
   }
+  // r_prev slab -> rS (asynchronous copy; consumed after the forward column DFT)
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int idx = tid + k * NT;
+    const int i = idx / W, c = idx % W;
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(rS + i * RP + c + 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(A.r_state + off + (size_t)i * N + c0 + c));
+  }
+  asm volatile("cp.async.commit_group;");
   __syncthreads();
   DDH_TS();  // 1: loaded
   const double d2 = st[0];
@@ -211,6 +228,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
   const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
   block_fft<N, -1>(tile + tid % W, true, tid / W, W, tw);
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();
   DDH_TS();  // 2: forward column DFT
   const bool warm = A.warm && !degenerate;
   float qreg[EPT];
@@ -225,7 +244,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       const float sg = ((ki + kj) & 1) ? -scale : scale;
       const float2 X = tile[ki * W + lc];
       const float2 u = make_float2(X.x * sg, X.y * sg);
-      const float rp = A.r_state[off + (size_t)ki * N + kj];
+      const float rp = rS[ki * RP + lc + 1];  // prefetched r_prev
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
       const float w = r0 * rcp_approx(r0 + A.s2);
@@ -258,20 +277,29 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
           const int br = b / (W / 2), bc = b % (W / 2);
           const int ki = 2 * br + ci, lj = 2 * bc + cj + 1;
           const float ri = rS[ki * RP + lj];
-          float B = 0.f, S = 0.f;
+          float B4 = 0.f, S4 = 0.f, Bd = 0.f, Sd = 0.f;  // nearest / diagonal neighbours
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
             const int ni = (ki + nb_di(m)) & (N - 1);  // periodic rows (full columns in the CTA)
             const float rj = rS[ni * RP + lj + nb_dj(m)];
-            const float bt = nb_w(m) * qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
-            B += bt;
-            S = fmaf(bt, rj, S);
+            const float bt = qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
+            if (m < 4) {
+              B4 += bt;
+              S4 = fmaf(bt, rj, S4);
+            } else {
+              Bd += bt;
+              Sd = fmaf(bt, rj, Sd);
+            }
           }
+          // b = 1/6 (nearest), 1/12 (diagonal), times 1/(2 sig_r^2)
+          const float B = A.r_b0 * fmaf(Bd, 1.f / 12.f, B4 * (1.f / 6.f));
+          const float S = A.r_b0 * fmaf(Sd, 1.f / 12.f, S4 * (1.f / 6.f));
           const float qv = c == 0 ? qreg[k * 4] : c == 1 ? qreg[k * 4 + 1] : c == 2 ? qreg[k * 4 + 2] : qreg[k * 4 + 3];
-          rS[ki * RP + lj] = r_update(ri, qv, A.r_b0 * B, A.r_b0 * S, A.r_min);
+          rS[ki * RP + lj] = r_update(ri, qv, B, S, A.r_min);
         }
       }
     }
+    cl.barrier_arrive();  // last remote read of a neighbour's slab done (wait before exit)
   } else if (!degenerate) {  // prior off: r = max(q, r_min)
 #pragma unroll
     for (int k = 0; k < EPT / 4; ++k) {
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     A.cbuf[off + (size_t)(idx / W) * N + c0 + idx % W] = tile[idx];
   }
   DDH_TS();  // 7: spectrum stored
-  if (icd) cl.sync();  // neighbours may still read our slab (last halo copy)
+  if (icd) cl.barrier_wait();  // neighbours may still read our slab until they arrive
   DDH_TS();  // 8: final cluster barrier
   DDH_TPRINT("KB");
 }
@@ -323,6 +351,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
   const int i0 = rank * H;
+  DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   if (tid == 0) {
@@ -348,7 +377,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   const double d2 = st[5];
   const bool degenerate = !(d2 > 0.0);
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);
+  DDH_TS();  // 1: loaded
   block_fft<N, +1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+  DDH_TS();  // 2: inverse row DFT
   // phase-correlation terms for this thread's pixels (2x2 blocks), kept in registers
   float creg[EPT], treg[EPT];
   const float inv_n = 1.f / (float)N, two_s2 = 2.f / A.s2;
@@ -375,6 +406,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     }
   }
   __syncthreads();  // tile dead: reuse as phS
+  DDH_TS();  // 3: c, theta
   if (degenerate) {  // state unchanged (no tip/tilt removal either)
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
@@ -393,6 +425,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     phS[(r + 1) * N + j] = A.phi_in[off + (size_t)i * N + j] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
   }
   __syncthreads();
+  DDH_TS();  // 4: phi loaded
   const bool prior = A.phi_prior != 0;
   const float w = A.phi_w;
   if (prior) {
@@ -427,6 +460,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
         phS[li * N + j] = phi_update(phS[li * N + j], cv, tv, nb, sb, w, true);
       }
     }
+    cl.barrier_arrive();  // last remote read done (wait before exit)
     __syncthreads();
   } else {
 #pragma unroll
@@ -441,6 +475,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     }
     __syncthreads();
   }
+  DDH_TS();  // 5: phi-ICD
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
@@ -450,7 +485,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     A.phi_out[g] = v;
     if (A.phi_copy) A.phi_copy[g] = v;
   }
-  if (prior) cl.sync();  // neighbours may still read our boundary rows
+  DDH_TS();  // 6: phi stored
+  if (prior) cl.barrier_wait();  // neighbours may still read our boundary rows until they arrive
+  DDH_TS();  // 7: exit barrier
+  DDH_TPRINT("KC");
 }
 
 // ------------------------------------------------------------- launchers
