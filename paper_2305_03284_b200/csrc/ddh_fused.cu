@@ -60,6 +60,13 @@ template <int N> struct FusedCfg {
   static constexpr int MINB = NT >= 1024 ? 1 : (NT >= 256 ? 4 : 8);  // CTAs/SM for __launch_bounds__
 };
 
+// L2 prefetch of [p, p + bytes) by the threads of a CTA (one request per 128 B line)
+__device__ __forceinline__ void prefetch_l2(const void *p, size_t bytes, int tid, int nt) {
+  const char *c = reinterpret_cast<const char *>(p);
+  for (size_t o = (size_t)tid * 128; o < bytes; o += (size_t)nt * 128)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
 bool fused_supported(int n) { return n == 64 || n == 128 || n == 256 || n == 512; }
 int fused_cluster(int n) { return n <= 128 ? 8 : 16; }
 
@@ -90,11 +97,19 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   __shared__ double part[5];
   __shared__ double tot[5];
   const int tid = threadIdx.x;
-  const int s = blockIdx.y;
   const int i0 = rank * H;
-  DDH_T0();
-  const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
+  __syncthreads();  // previous iteration's shared-memory reads are done
+  {
+    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
+    if (sn < A.sc) {
+      prefetch_l2(A.y + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
+      prefetch_l2(A.phi_in + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float), tid, NT);
+    }
+  }
+  const size_t off = (size_t)s * P;
+  DDH_T0();
   float ph[EPT];
   double v[5] = {0, 0, 0, 0, 0};
 #pragma unroll
@@ -176,6 +191,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   cl.barrier_wait();
   DDH_TS();  // 6: exit barrier
   DDH_TPRINT("KA");
+  }  // stream loop
 }
 
 // ------------------------------------------------------------------- KB
@@ -196,11 +212,21 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   float2 *tw = reinterpret_cast<float2 *>(rS + N * RP);
   __shared__ double st[1];
   const int tid = threadIdx.x;
-  const int s = blockIdx.y;
   const int c0 = rank * W;
-  DDH_T0();
-  const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
+  __syncthreads();  // previous iteration's shared-memory reads are done
+  {
+    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
+    if (sn < A.sc) {
+      for (int i = tid; i < N; i += NT) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.cbuf + (size_t)sn * P + (size_t)i * N + c0));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.r_state + (size_t)sn * P + (size_t)i * N + c0));
+      }
+    }
+  }
+  const size_t off = (size_t)s * P;
+  DDH_T0();
   if (tid == 0) {
     double d2 = 0.0;
     for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
@@ -333,6 +359,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   if (icd) cl.barrier_wait();  // neighbours may still read our slab until they arrive
   DDH_TS();  // 8: final cluster barrier
   DDH_TPRINT("KB");
+  }  // stream loop
 }
 
 // ------------------------------------------------------------------- KC
@@ -349,11 +376,20 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   float2 *tw = sm + (kc_smem<N>() / sizeof(float2) - N);
   __shared__ double st[6];
   const int tid = threadIdx.x;
-  const int s = blockIdx.y;
   const int i0 = rank * H;
-  DDH_T0();
-  const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
+  __syncthreads();  // previous iteration's shared-memory reads are done
+  {
+    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
+    if (sn < A.sc) {
+      prefetch_l2(A.cbuf + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
+      prefetch_l2(A.y + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
+      prefetch_l2(A.phi_in + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float), tid, NT);
+    }
+  }
+  const size_t off = (size_t)s * P;
+  DDH_T0();
   if (tid == 0) {
     double d2 = 0.0;
     for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
@@ -416,7 +452,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       A.phi_out[g] = v;
       if (A.phi_copy) A.phi_copy[g] = v;
     }
-    return;
+    continue;
   }
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
@@ -489,6 +525,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   if (prior) cl.barrier_wait();  // neighbours may still read our boundary rows until they arrive
   DDH_TS();  // 7: exit barrier
   DDH_TPRINT("KC");
+  }  // stream loop
 }
 
 // ------------------------------------------------------------- launchers
@@ -512,6 +549,9 @@ static cudaError_t launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 bloc
 }
 
 template <int N>
+static void init_grids();
+
+template <int N>
 static cudaError_t init_fused_n() {
   cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ka_smem<N>());
   cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kb_smem<N>());
@@ -521,6 +561,7 @@ static cudaError_t init_fused_n() {
     cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
+  init_grids<N>();
   return cudaGetLastError();
 }
 
@@ -535,17 +576,56 @@ static cudaError_t init_fused_n() {
 
 cudaError_t init_fused(int n) { DDH_FDISPATCH(n, return init_fused_n<N>()); }
 
+// Persistent grids: as many clusters as can be co-resident (queried once per
+// kernel with cudaOccupancyMaxActiveClusters), each looping over streams.
+static int g_max_clusters[3][11];  // [kernel][log2 N]
+
+template <typename... KArgs>
+static int max_clusters(void (*kernel)(KArgs...), int cs, int nt, size_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1024);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void *)kernel, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 1 << 20;  // unknown: one cluster per stream
+  }
+  return n;
+}
+
+template <int N>
+static void init_grids() {
+  using C = FusedCfg<N>;
+  const int l = 31 - __builtin_clz(N);
+  g_max_clusters[0][l] = max_clusters(kf_rows_fwd<N>, C::CS, C::NT, ka_smem<N>());
+  g_max_clusters[1][l] = max_clusters(kf_cols<N>, C::CS, C::NT, kb_smem<N>());
+  g_max_clusters[2][l] = max_clusters(kf_rows_inv<N>, C::CS, C::NT, kc_smem<N>());
+}
+
+static inline int grid_y(int which, int n, int sc) {
+  const int m = g_max_clusters[which][31 - __builtin_clz(n)];
+  return m > 0 && m < sc ? m : sc;
+}
+
 cudaError_t launch_ka(const StepArgs &a, cudaStream_t st) {
-  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_fwd<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
-                                           ka_smem<N>(), FusedCfg<N>::CS, st, a));
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_fwd<N>, dim3(FusedCfg<N>::CS, grid_y(0, N, a.sc)),
+                                           dim3(FusedCfg<N>::NT), ka_smem<N>(), FusedCfg<N>::CS, st, a));
 }
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st) {
-  DDH_FDISPATCH(a.n, return launch_cluster(kf_cols<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
-                                           kb_smem<N>(), FusedCfg<N>::CS, st, a));
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_cols<N>, dim3(FusedCfg<N>::CS, grid_y(1, N, a.sc)),
+                                           dim3(FusedCfg<N>::NT), kb_smem<N>(), FusedCfg<N>::CS, st, a));
 }
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st) {
-  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_inv<N>, dim3(FusedCfg<N>::CS, a.sc), dim3(FusedCfg<N>::NT),
-                                           kc_smem<N>(), FusedCfg<N>::CS, st, a));
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_inv<N>, dim3(FusedCfg<N>::CS, grid_y(2, N, a.sc)),
+                                           dim3(FusedCfg<N>::NT), kc_smem<N>(), FusedCfg<N>::CS, st, a));
 }
 
 }  // namespace ddh
