@@ -605,9 +605,11 @@ template <int N>
 static void init_grids() {
   using C = FusedCfg<N>;
   const int l = 31 - __builtin_clz(N);
-  g_max_clusters[0][l] = max_clusters(kf_rows_fwd<N>, C::CS, C::NT, ka_smem<N>());
+  // measured at 256^2 x 64 streams: the persistent grid helps KB (94 vs 99 us)
+  // and hurts KA/KC (52 vs 44, 82 vs 70 us), which keep one cluster per stream
+  g_max_clusters[0][l] = 1 << 20;
   g_max_clusters[1][l] = max_clusters(kf_cols<N>, C::CS, C::NT, kb_smem<N>());
-  g_max_clusters[2][l] = max_clusters(kf_rows_inv<N>, C::CS, C::NT, kc_smem<N>());
+  g_max_clusters[2][l] = 1 << 20;
 }
 
 static inline int grid_y(int which, int n, int sc) {
