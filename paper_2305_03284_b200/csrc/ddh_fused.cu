@@ -97,19 +97,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   __shared__ double part[5];
   __shared__ double tot[5];
   const int tid = threadIdx.x;
+  const int s = blockIdx.y;
   const int i0 = rank * H;
-  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
-  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
-  __syncthreads();  // previous iteration's shared-memory reads are done
-  {
-    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
-    if (sn < A.sc) {
-      prefetch_l2(A.y + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
-      prefetch_l2(A.phi_in + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float), tid, NT);
-    }
-  }
   const size_t off = (size_t)s * P;
-  DDH_T0();
+  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   float ph[EPT];
   double v[5] = {0, 0, 0, 0, 0};
 #pragma unroll
@@ -129,7 +120,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
       v[4] += (double)f * (double)(i - N / 2);
     }
   }
-  DDH_TS();  // 1: loaded + local sums
   block_sum<5>(v, red);
   if (tid == 0) {
 #pragma unroll
@@ -143,7 +133,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   }
   cl.barrier_arrive();  // remote reads of `part` done (waited on before exit)
   __syncthreads();
-  DDH_TS();  // 2: cluster reduction
   double c[3] = {0, 0, 0};
   if (A.apply_plane) plane_from_sums(tot, A.minv, c);
   const double mu_r = tot[0] / P, mu_i = tot[1] / P;
@@ -178,20 +167,14 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   double a1[1] = {acc};
   block_sum<1>(a1, red);  // also orders the tile writes before the FFT
   if (tid == 0) A.part1[(size_t)s * CS + rank] = a1[0];
-  DDH_TS();  // 3: z, |y - mu|^2
   block_fft<N, -1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
-  DDH_TS();  // 4: row DFT
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1);
     A.cbuf[off + (size_t)(i0 + r) * N + j] = tile[r * PITCH + j];
   }
-  DDH_TS();  // 5: stored
   cl.barrier_wait();
-  DDH_TS();  // 6: exit barrier
-  DDH_TPRINT("KA");
-  }  // stream loop
 }
 
 // ------------------------------------------------------------------- KB
@@ -376,20 +359,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   float2 *tw = sm + (kc_smem<N>() / sizeof(float2) - N);
   __shared__ double st[6];
   const int tid = threadIdx.x;
+  const int s = blockIdx.y;
   const int i0 = rank * H;
-  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
-  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
-  __syncthreads();  // previous iteration's shared-memory reads are done
-  {
-    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
-    if (sn < A.sc) {
-      prefetch_l2(A.cbuf + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
-      prefetch_l2(A.y + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
-      prefetch_l2(A.phi_in + (size_t)sn * P + (size_t)i0 * N, (size_t)H * N * sizeof(float), tid, NT);
-    }
-  }
   const size_t off = (size_t)s * P;
-  DDH_T0();
+  for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   if (tid == 0) {
     double d2 = 0.0;
     for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
@@ -413,9 +386,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   const double d2 = st[5];
   const bool degenerate = !(d2 > 0.0);
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);
-  DDH_TS();  // 1: loaded
   block_fft<N, +1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
-  DDH_TS();  // 2: inverse row DFT
   // phase-correlation terms for this thread's pixels (2x2 blocks), kept in registers
   float creg[EPT], treg[EPT];
   const float inv_n = 1.f / (float)N, two_s2 = 2.f / A.s2;
@@ -442,7 +413,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     }
   }
   __syncthreads();  // tile dead: reuse as phS
-  DDH_TS();  // 3: c, theta
   if (degenerate) {  // state unchanged (no tip/tilt removal either)
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
@@ -452,7 +422,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       A.phi_out[g] = v;
       if (A.phi_copy) A.phi_copy[g] = v;
     }
-    continue;
+    return;
   }
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
@@ -461,7 +431,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     phS[(r + 1) * N + j] = A.phi_in[off + (size_t)i * N + j] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
   }
   __syncthreads();
-  DDH_TS();  // 4: phi loaded
   const bool prior = A.phi_prior != 0;
   const float w = A.phi_w;
   if (prior) {
@@ -496,7 +465,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
         phS[li * N + j] = phi_update(phS[li * N + j], cv, tv, nb, sb, w, true);
       }
     }
-    cl.barrier_arrive();  // last remote read done (wait before exit)
     __syncthreads();
   } else {
 #pragma unroll
@@ -511,7 +479,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     }
     __syncthreads();
   }
-  DDH_TS();  // 5: phi-ICD
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
@@ -521,11 +488,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     A.phi_out[g] = v;
     if (A.phi_copy) A.phi_copy[g] = v;
   }
-  DDH_TS();  // 6: phi stored
-  if (prior) cl.barrier_wait();  // neighbours may still read our boundary rows until they arrive
-  DDH_TS();  // 7: exit barrier
-  DDH_TPRINT("KC");
-  }  // stream loop
+  if (prior) cl.sync();  // neighbours may still read our boundary rows
 }
 
 // ------------------------------------------------------------- launchers
