@@ -77,9 +77,7 @@ template <int N> __host__ __device__ constexpr size_t kb_smem() {
 }
 template <int N> __host__ __device__ constexpr size_t kc_smem() {
   using C = FusedCfg<N>;
-  const size_t tile = (size_t)C::H * (N + 1) * sizeof(float2);
-  const size_t ph = (size_t)(C::H + 2) * N * sizeof(float);
-  return (tile > ph ? tile : ph) + (size_t)N * sizeof(float2);
+  return (size_t)C::H * (N + 1) * sizeof(float2) + (size_t)(C::H + 2) * N * sizeof(float) + (size_t)N * sizeof(float2);
 }
 
 // ------------------------------------------------------------------- KA
@@ -99,6 +97,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
   const int i0 = rank * H;
+  DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   float ph[EPT];
@@ -120,6 +119,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
       v[4] += (double)f * (double)(i - N / 2);
     }
   }
+  DDH_TS();  // 1: loaded + local sums
   block_sum<5>(v, red);
   if (tid == 0) {
 #pragma unroll
@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   }
   cl.barrier_arrive();  // remote reads of `part` done (waited on before exit)
   __syncthreads();
+  DDH_TS();  // 2: cluster reduction
   double c[3] = {0, 0, 0};
   if (A.apply_plane) plane_from_sums(tot, A.minv, c);
   const double mu_r = tot[0] / P, mu_i = tot[1] / P;
@@ -167,14 +168,19 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   double a1[1] = {acc};
   block_sum<1>(a1, red);  // also orders the tile writes before the FFT
   if (tid == 0) A.part1[(size_t)s * CS + rank] = a1[0];
+  DDH_TS();  // 3: z, |y - mu|^2
   block_fft<N, -1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+  DDH_TS();  // 4: row DFT
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1);
     A.cbuf[off + (size_t)(i0 + r) * N + j] = tile[r * PITCH + j];
   }
+  DDH_TS();  // 5: stored
   cl.barrier_wait();
+  DDH_TS();  // 6: exit barrier
+  DDH_TPRINT("KA");
 }
 
 // ------------------------------------------------------------------- KB
@@ -354,13 +360,14 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
   extern __shared__ float2 sm[];
-  float2 *tile = sm;                                // [H][N+1]
-  float *phS = reinterpret_cast<float *>(sm);       // [H+2][N] (aliases the tile after the FFT)
-  float2 *tw = sm + (kc_smem<N>() / sizeof(float2) - N);
+  float2 *tile = sm;                                                       // [H][N+1]
+  float *phS = reinterpret_cast<float *>(sm + H * PITCH);                  // [H+2][N]
+  float2 *tw = reinterpret_cast<float2 *>(phS + (H + 2) * N);
   __shared__ double st[6];
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
   const int i0 = rank * H;
+  DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   if (tid == 0) {
@@ -374,6 +381,15 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     st[4] = sv[4];
     st[5] = d2;
   }
+  // y rows -> L2 now (read in the epilogue); phi rows -> phS asynchronously
+  prefetch_l2(A.y + off + (size_t)i0 * N, (size_t)H * N * sizeof(float2), tid, NT);
+#pragma unroll
+  for (int k = 0; k < EPT / 4; ++k) {
+    const int idx = (tid + k * NT) * 4;  // 16-byte chunks of the H x N phi slab
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(phS + N + idx);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(A.phi_in + off + (size_t)i0 * N + idx));
+  }
+  asm volatile("cp.async.commit_group;");
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
@@ -386,7 +402,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   const double d2 = st[5];
   const bool degenerate = !(d2 > 0.0);
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);
+  DDH_TS();  // 1: loaded
   block_fft<N, +1>(tile + (tid % H) * PITCH, true, tid / H, 1, tw);
+  DDH_TS();  // 2: inverse row DFT
   // phase-correlation terms for this thread's pixels (2x2 blocks), kept in registers
   float creg[EPT], treg[EPT];
   const float inv_n = 1.f / (float)N, two_s2 = 2.f / A.s2;
@@ -412,7 +430,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       treg[k * 4 + q4] = th;
     }
   }
-  __syncthreads();  // tile dead: reuse as phS
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();
+  DDH_TS();  // 3: c, theta
   if (degenerate) {  // state unchanged (no tip/tilt removal either)
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
@@ -428,9 +448,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1), i = i0 + r;
-    phS[(r + 1) * N + j] = A.phi_in[off + (size_t)i * N + j] - (c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2));
+    phS[(r + 1) * N + j] -= c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2);  // phi' = phi - plane
   }
   __syncthreads();
+  DDH_TS();  // 4: phi loaded
   const bool prior = A.phi_prior != 0;
   const float w = A.phi_w;
   if (prior) {
@@ -465,6 +486,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
         phS[li * N + j] = phi_update(phS[li * N + j], cv, tv, nb, sb, w, true);
       }
     }
+    cl.barrier_arrive();  // last remote read done (wait before exit)
     __syncthreads();
   } else {
 #pragma unroll
@@ -479,6 +501,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     }
     __syncthreads();
   }
+  DDH_TS();  // 5: phi-ICD
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
@@ -488,7 +511,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     A.phi_out[g] = v;
     if (A.phi_copy) A.phi_copy[g] = v;
   }
-  if (prior) cl.sync();  // neighbours may still read our boundary rows
+  DDH_TS();  // 6: phi stored
+  if (prior) cl.barrier_wait();  // neighbours may still read our boundary rows until they arrive
+  DDH_TS();  // 7: exit barrier
+  DDH_TPRINT("KC");
 }
 
 // ------------------------------------------------------------- launchers
