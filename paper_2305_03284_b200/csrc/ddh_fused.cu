@@ -73,11 +73,11 @@ int fused_cluster(int n) { return n <= 128 ? 8 : 16; }
 template <int N> __host__ __device__ constexpr size_t ka_smem() { return (size_t)(FusedCfg<N>::H * (N + 1) + N) * sizeof(float2); }
 template <int N> __host__ __device__ constexpr size_t kb_smem() {
   using C = FusedCfg<N>;
-  return (size_t)N * C::W * sizeof(float2) + (size_t)N * C::RP * sizeof(float) + (size_t)N * sizeof(float2);
+  return (size_t)N * C::W * sizeof(float2) + (size_t)(N + 2) * C::RP * sizeof(float) + (size_t)N * sizeof(float2);
 }
 template <int N> __host__ __device__ constexpr size_t kc_smem() {
   using C = FusedCfg<N>;
-  return (size_t)C::H * (N + 1) * sizeof(float2) + (size_t)(C::H + 2) * N * sizeof(float) + (size_t)N * sizeof(float2);
+  return (size_t)C::H * (N + 1) * sizeof(float2) + (size_t)(C::H + 2) * (N + 8) * sizeof(float) + (size_t)N * sizeof(float2);
 }
 
 // ------------------------------------------------------------------- KA
@@ -197,8 +197,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   const int rank = (int)cl.block_rank();
   extern __shared__ float2 sm[];
   float2 *tile = sm;                                       // [N][W]
-  float *rS = reinterpret_cast<float *>(sm + N * W);       // [N][RP], columns 0 and W+1 = halos
-  float2 *tw = reinterpret_cast<float2 *>(rS + N * RP);
+  // rS: [N+2][RP]; data row i at padded row i+1, columns 1..W; column 0 / W+1 and
+  // rows 0 / N+1 are halos (neighbour CTAs' columns, periodic row wrap)
+  float *rS = reinterpret_cast<float *>(sm + N * W);
+  float2 *tw = reinterpret_cast<float2 *>(rS + (N + 2) * RP);
   __shared__ double st[1];
   const int tid = threadIdx.x;
   const int c0 = rank * W;
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int i = idx / W, c = idx % W;
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(rS + i * RP + c + 1);
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(rS + (i + 1) * RP + c + 1);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(A.r_state + off + (size_t)i * N + c0 + c));
   }
   asm volatile("cp.async.commit_group;");
@@ -259,13 +261,13 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       const float sg = ((ki + kj) & 1) ? -scale : scale;
       const float2 X = tile[ki * W + lc];
       const float2 u = make_float2(X.x * sg, X.y * sg);
-      const float rp = rS[ki * RP + lc + 1];  // prefetched r_prev
+      const float rp = rS[(ki + 1) * RP + lc + 1];  // prefetched r_prev
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);
       const float w = r0 * rcp_approx(r0 + A.s2);
       const float2 mu = make_float2(w * u.x, w * u.y);
       qreg[k * 4 + q4] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
-      rS[ki * RP + lc + 1] = r0;
+      rS[(ki + 1) * RP + lc + 1] = r0;
       const float cs = ((ki + kj) & 1) ? -1.f : 1.f;
       tile[ki * W + lc] = make_float2(cs * mu.x, cs * mu.y);
     }
@@ -280,9 +282,16 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       const int c = cc & 3;
       {
         cl.sync();
-        for (int i = tid; i < N; i += NT) {
-          rS[i * RP] = left[i * RP + W];
-          rS[i * RP + W + 1] = right[i * RP + 1];
+        // halos: neighbour columns for all padded rows (rows 0 / N+1 take the
+        // neighbours' data rows N / 1) and the periodic row wrap of own columns
+        for (int i = tid; i < N + 2; i += NT) {
+          const int src = i == 0 ? N : (i == N + 1 ? 1 : i);
+          rS[i * RP] = left[src * RP + W];
+          rS[i * RP + W + 1] = right[src * RP + 1];
+        }
+        for (int c = tid; c < W; c += NT) {
+          rS[c + 1] = rS[N * RP + c + 1];
+          rS[(N + 1) * RP + c + 1] = rS[RP + c + 1];
         }
         __syncthreads();
         const int ci = c >> 1, cj = c & 1;
@@ -290,13 +299,12 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
         for (int k = 0; k < EPT / 4; ++k) {
           const int b = tid + k * NT;
           const int br = b / (W / 2), bc = b % (W / 2);
-          const int ki = 2 * br + ci, lj = 2 * bc + cj + 1;
+          const int ki = 2 * br + ci + 1, lj = 2 * bc + cj + 1;  // padded coordinates
           const float ri = rS[ki * RP + lj];
           float B4 = 0.f, S4 = 0.f, Bd = 0.f, Sd = 0.f;  // nearest / diagonal neighbours
 #pragma unroll
           for (int m = 0; m < 8; ++m) {
-            const int ni = (ki + nb_di(m)) & (N - 1);  // periodic rows (full columns in the CTA)
-            const float rj = rS[ni * RP + lj + nb_dj(m)];
+            const float rj = rS[(ki + nb_di(m)) * RP + lj + nb_dj(m)];  // periodic rows via the wrap halo
             const float bt = qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
             if (m < 4) {
               B4 += bt;
@@ -322,7 +330,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
       const int br = b / (W / 2), bc = b % (W / 2);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4)
-        rS[(2 * br + (q4 >> 1)) * RP + 2 * bc + (q4 & 1) + 1] = fmaxf(qreg[k * 4 + q4], A.r_min);
+        rS[(2 * br + (q4 >> 1) + 1) * RP + 2 * bc + (q4 & 1) + 1] = fmaxf(qreg[k * 4 + q4], A.r_min);
     }
   }
   __syncthreads();
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int i = idx / W, c = idx % W;
-    const float v = rS[i * RP + c + 1];
+    const float v = rS[(i + 1) * RP + c + 1];
     const size_t g = off + (size_t)i * N + c0 + c;
     A.r_state[g] = v;
     if (A.r_copy) A.r_copy[g] = v;
@@ -361,8 +369,11 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   const int rank = (int)cl.block_rank();
   extern __shared__ float2 sm[];
   float2 *tile = sm;                                                       // [H][N+1]
-  float *phS = reinterpret_cast<float *>(sm + H * PITCH);                  // [H+2][N]
-  float2 *tw = reinterpret_cast<float2 *>(phS + (H + 2) * N);
+  // phS: [H+2][PP], data row r at row r+1, column j at j+4; zero borders make
+  // missing neighbours of the free boundary contribute nothing
+  constexpr int PP = N + 8;
+  float *phS = reinterpret_cast<float *>(sm + H * PITCH);
+  float2 *tw = reinterpret_cast<float2 *>(phS + (H + 2) * PP);
   __shared__ double st[6];
   const int tid = threadIdx.x;
   const int s = blockIdx.y;
@@ -370,6 +381,14 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   DDH_T0();
   const size_t off = (size_t)s * P;
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
+  for (int k = tid; k < (H + 2) * 8; k += NT) {  // pad columns
+    const int r = k >> 3, c = k & 7;
+    phS[r * PP + (c < 4 ? c : N + c)] = 0.f;
+  }
+  for (int k = tid; k < N; k += NT) {  // halo rows (overwritten where a neighbour CTA exists)
+    phS[4 + k] = 0.f;
+    phS[(H + 1) * PP + 4 + k] = 0.f;
+  }
   if (tid == 0) {
     double d2 = 0.0;
     for (int r = 0; r < CS; ++r) d2 += A.part1[(size_t)s * CS + r];
@@ -386,7 +405,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
 #pragma unroll
   for (int k = 0; k < EPT / 4; ++k) {
     const int idx = (tid + k * NT) * 4;  // 16-byte chunks of the H x N phi slab
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(phS + N + idx);
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(phS + (idx / N + 1) * PP + 4 + (idx & (N - 1)));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(A.phi_in + off + (size_t)i0 * N + idx));
   }
   asm volatile("cp.async.commit_group;");
@@ -448,7 +467,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   for (int k = 0; k < EPT; ++k) {
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1), i = i0 + r;
-    phS[(r + 1) * N + j] -= c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2);  // phi' = phi - plane
+    phS[(r + 1) * PP + 4 + j] -= c0 + c1 * (float)(j - N / 2) + c2 * (float)(i - N / 2);  // phi' = phi - plane
   }
   __syncthreads();
   DDH_TS();  // 4: phi loaded
@@ -462,8 +481,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       const int c = cc & 3;
       cl.sync();
       for (int j = tid; j < N; j += NT) {
-        if (up) phS[j] = up[H * N + j];
-        if (dn) phS[(H + 1) * N + j] = dn[N + j];
+        if (up) phS[4 + j] = up[H * PP + 4 + j];
+        if (dn) phS[(H + 1) * PP + 4 + j] = dn[PP + 4 + j];
       }
       __syncthreads();
       const int ci = c >> 1, cj = c & 1;
@@ -471,19 +490,21 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       for (int k = 0; k < EPT / 4; ++k) {
         const int b = tid + k * NT;
         const int br = b / (N / 2), bc = b % (N / 2);
-        const int r = 2 * br + ci, j = 2 * bc + cj, i = i0 + r, li = r + 1;
-        float nb = 0.f, sb = 0.f;
+        const int r = 2 * br + ci, j = 2 * bc + cj, i = i0 + r, li = r + 1, lj = j + 4;
+        float n4 = 0.f, nd = 0.f;  // zero borders: no bounds checks
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          const int ni = i + nb_di(m), nj = j + nb_dj(m);
-          if (ni >= 0 && ni < N && nj >= 0 && nj < N) {  // free boundary
-            nb = fmaf(nb_w(m), phS[(li + nb_di(m)) * N + nj], nb);
-            sb += nb_w(m);
-          }
+          const float v = phS[(li + nb_di(m)) * PP + lj + nb_dj(m)];
+          if (m < 4) n4 += v; else nd += v;
         }
+        const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
+        // sum of b over the existing neighbours (1 inside the grid)
+        const bool tp = i == 0, bt = i == N - 1, lf = j == 0, rt = j == N - 1;
+        const float sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+                         (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
         const float cv = c == 0 ? creg[k * 4] : c == 1 ? creg[k * 4 + 1] : c == 2 ? creg[k * 4 + 2] : creg[k * 4 + 3];
         const float tv = c == 0 ? treg[k * 4] : c == 1 ? treg[k * 4 + 1] : c == 2 ? treg[k * 4 + 2] : treg[k * 4 + 3];
-        phS[li * N + j] = phi_update(phS[li * N + j], cv, tv, nb, sb, w, true);
+        phS[li * PP + lj] = phi_update(phS[li * PP + lj], cv, tv, nb, sb, w, true);
       }
     }
     cl.barrier_arrive();  // last remote read done (wait before exit)
@@ -495,8 +516,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
       const int br = b / (N / 2), bc = b % (N / 2);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        const int li = 2 * br + (q4 >> 1) + 1, j = 2 * bc + (q4 & 1);
-        phS[li * N + j] = phi_update(phS[li * N + j], creg[k * 4 + q4], treg[k * 4 + q4], 0.f, 0.f, 0.f, false);
+        const int li = 2 * br + (q4 >> 1) + 1, lj = 2 * bc + (q4 & 1) + 4;
+        phS[li * PP + lj] = phi_update(phS[li * PP + lj], creg[k * 4 + q4], treg[k * 4 + q4], 0.f, 0.f, 0.f, false);
       }
     }
     __syncthreads();
@@ -507,7 +528,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
     const int idx = tid + k * NT;
     const int r = idx / N, j = idx & (N - 1);
     const size_t g = off + (size_t)(i0 + r) * N + j;
-    const float v = phS[(r + 1) * N + j];
+    const float v = phS[(r + 1) * PP + 4 + j];
     A.phi_out[g] = v;
     if (A.phi_copy) A.phi_copy[g] = v;
   }
