@@ -41,7 +41,13 @@ namespace cg = cooperative_groups;
     for (int k_ = 0; k_ < 11; ++k_) d_[k_] = (k_ + 1 < n_ph) ? t_ph[k_ + 1] - t_ph[k_] : 0; \
     printf("%s %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", tag, d_[0], d_[1], d_[2], d_[3], d_[4], \
            d_[5], d_[6], d_[7], d_[8], d_[9], d_[10]); } } while (0)
+#define DDH_SYNC_T(stmt) do { long long a_ = clock64(); stmt; if (threadIdx.x == 0) t_sync += clock64() - a_; } while (0)
+#define DDH_SYNC_DECL long long t_sync = 0;
+#define DDH_SYNC_PRINT(tag) do { if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y < 4) printf("%s %lld\n", tag, t_sync); } while (0)
 #else
+#define DDH_SYNC_T(stmt) stmt
+#define DDH_SYNC_DECL
+#define DDH_SYNC_PRINT(tag)
 #define DDH_T0()
 #define DDH_TS()
 #define DDH_TPRINT(tag)
@@ -274,6 +280,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   }
   DDH_TS();  // 3: Eq. 3 + E-step
   const bool icd = A.r_prior && !degenerate;  // uniform over the cluster (one stream)
+  DDH_SYNC_DECL
   if (icd) {
     float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
     float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
@@ -281,7 +288,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
       const int c = cc & 3;
       {
-        cl.sync();
+        DDH_SYNC_T(cl.sync());
         // halos: neighbour columns for all padded rows (rows 0 / N+1 take the
         // neighbours' data rows N / 1) and the periodic row wrap of own columns
         for (int i = tid; i < N + 2; i += NT) {
@@ -293,7 +300,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
           rS[c + 1] = rS[N * RP + c + 1];
           rS[(N + 1) * RP + c + 1] = rS[RP + c + 1];
         }
-        __syncthreads();
+        DDH_SYNC_T(__syncthreads());
         const int ci = c >> 1, cj = c & 1;
 #pragma unroll
         for (int k = 0; k < EPT / 4; ++k) {
@@ -356,6 +363,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   if (icd) cl.barrier_wait();  // neighbours may still read our slab until they arrive
   DDH_TS();  // 8: final cluster barrier
   DDH_TPRINT("KB");
+  DDH_SYNC_PRINT("KBsync");
   }  // stream loop
 }
 
@@ -473,18 +481,19 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   DDH_TS();  // 4: phi loaded
   const bool prior = A.phi_prior != 0;
   const float w = A.phi_w;
+  DDH_SYNC_DECL
   if (prior) {
     const float *up = rank > 0 ? cl.map_shared_rank(phS, rank - 1) : nullptr;
     const float *dn = rank < CS - 1 ? cl.map_shared_rank(phS, rank + 1) : nullptr;
 #pragma unroll 1
     for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
       const int c = cc & 3;
-      cl.sync();
+      DDH_SYNC_T(cl.sync());
       for (int j = tid; j < N; j += NT) {
         if (up) phS[4 + j] = up[H * PP + 4 + j];
         if (dn) phS[(H + 1) * PP + 4 + j] = dn[PP + 4 + j];
       }
-      __syncthreads();
+      DDH_SYNC_T(__syncthreads());
       const int ci = c >> 1, cj = c & 1;
 #pragma unroll
       for (int k = 0; k < EPT / 4; ++k) {
@@ -536,6 +545,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   if (prior) cl.barrier_wait();  // neighbours may still read our boundary rows until they arrive
   DDH_TS();  // 7: exit barrier
   DDH_TPRINT("KC");
+  DDH_SYNC_PRINT("KCsync");
 }
 
 // ------------------------------------------------------------- launchers
