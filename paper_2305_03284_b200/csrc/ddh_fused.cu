@@ -488,10 +488,17 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
 #pragma unroll 1
     for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
       const int c = cc & 3;
-      DDH_SYNC_T(cl.sync());
-      for (int j = tid; j < N; j += NT) {
-        if (up) phS[4 + j] = up[H * PP + 4 + j];
-        if (dn) phS[(H + 1) * PP + 4 + j] = dn[PP + 4 + j];
+      // Row parity changes only every two phases: the halo row above (global
+      // row i0-1, odd) is read in phases 0/1 and modified by its owner only in
+      // phases 2/3; the halo row below (i0+H, even) is read in phases 2/3 and
+      // modified only in phases 0/1.  So one cluster barrier + copy before
+      // phase 0 (row above) and one before phase 2 (row below) per sweep.
+      if (c == 0 || c == 2) {
+        DDH_SYNC_T(cl.sync());
+        for (int j = tid; j < N; j += NT) {
+          if (c == 0 && up) phS[4 + j] = up[H * PP + 4 + j];
+          if (c == 2 && dn) phS[(H + 1) * PP + 4 + j] = dn[PP + 4 + j];
+        }
       }
       DDH_SYNC_T(__syncthreads());
       const int ci = c >> 1, cj = c & 1;
