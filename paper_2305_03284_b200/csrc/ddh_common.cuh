@@ -101,7 +101,7 @@ __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
   // 3 MUFU (lg2, ex2, rcp) + 6 FMA-pipe instructions
   const float a = fmaf(fabsf(d), inv_Tsig, 1e-30f);
   const float t = ex2_approx(tmq * lg2_approx(a));
-  const float r = rcp_fma(1.f + t);
+  const float r = rcp_approx(1.f + t);
   const float k = 1.f - 0.5f * tmq;
   return fmaf(1.f - k, r, k) * r;
 }
