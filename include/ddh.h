@@ -80,11 +80,15 @@ typedef struct {
   double boot_alpha;    /* bootstrap back-projection weight alpha_b > 0, default 1 (R15)   */
   int32_t chunk_streams;/* streams per launch group (L2-resident workspace); 0 = auto       */
   uint32_t flags;       /* DDH_F_*                                                        */
+  int32_t lanes;        /* fused path: concurrent sub-groups of a launch group, each on its
+                           own CUDA stream forked from / joined to the ctx stream, so the
+                           kernels of different sub-groups share the SMs; 1..8, 0 = auto
+                           (streams/16 clamped to [1,4]).  Results do not depend on it.   */
 } ddh_params;
 
 /* Defaults: N=256, S=1, device 0, D=N, sigma^2=0.1, lambda=0.45, alpha=0.025,
  * N_k=1, r_min=1e-4, sigma_r=0.5, T=1, q=1.2, sigma_phi=0.5, 1 sweep,
- * P_b=200, alpha_b=1, chunk auto, flags 0.  Errors: DDH_E_INVAL if p is NULL. */
+ * P_b=200, alpha_b=1, chunk auto, flags 0, lanes auto.  Errors: DDH_E_INVAL if p is NULL. */
 ddh_status ddh_default_params(ddh_params *p);
 
 /* Create a ctx for S streams on p->device: validates p, allocates the state

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -52,6 +53,12 @@ struct ddh_ctx {
   float2 *y_stage = nullptr;
   float *phi_stage = nullptr, *r_stage = nullptr;
   uint8_t *status_stage = nullptr;
+  // concurrent launch lanes of the fused path: the streams of a launch group
+  // are split over `lanes` CUDA streams so that the kernels of different
+  // sub-groups (KA of one, KB of another, ...) share the SMs
+  int lanes = 1;
+  cudaStream_t lane_st[8] = {};
+  cudaEvent_t lane_ev[9] = {};
   // instrumentation
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -91,7 +98,7 @@ const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols",
                                           "kf_rows_fwd", "kf_cols", "kf_rows_inv"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
-cudaEvent_t *prof_begin(ddh_ctx *c, int kind) {
+cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
   if (!c->profiling) return nullptr;
   const size_t i = c->ev_kind.size();
   while (c->ev_pool.size() < 2 * (i + 1)) {
@@ -100,17 +107,18 @@ cudaEvent_t *prof_begin(ddh_ctx *c, int kind) {
     c->ev_pool.push_back(e);
   }
   c->ev_kind.push_back(kind);
-  cudaEventRecord(c->ev_pool[2 * i], c->st);
+  cudaEventRecord(c->ev_pool[2 * i], st);
   return &c->ev_pool[2 * i + 1];
 }
 
-#define DDH_LAUNCH(c, kind, call)                       \
+#define DDH_LAUNCH_ON(c, kind, st, call)                \
   do {                                                  \
-    cudaEvent_t *end_ = prof_begin((c), (kind));        \
+    cudaEvent_t *end_ = prof_begin((c), (kind), (st));  \
     DDH_CK(c, call);                                    \
-    if (end_) cudaEventRecord(*end_, (c)->st);          \
+    if (end_) cudaEventRecord(*end_, (st));             \
     (c)->launches++;                                    \
   } while (0)
+#define DDH_LAUNCH(c, kind, call) DDH_LAUNCH_ON(c, kind, (c)->st, call)
 
 bool valid_n(int n) { return n == 64 || n == 128 || n == 256 || n == 512 || n == 1024; }
 
@@ -253,28 +261,55 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     a.apply_plane = plane ? 1 : 0;
     if (c->fused) {  // KA -> KB -> KC per EM iteration (cluster per stream)
       a.nb1 = c->cs;
-      for (int it = 0; it < iters; ++it) {
-        const bool first = (it == 0), last = (it == iters - 1);
-        a.phi_in = c->phi[cur] + so;
-        a.phi_out = c->phi[cur ^ 1] + so;
-        a.apply_plane = (plane && first) ? 1 : 0;
-        if (mode == Mode::Step) {
-          a.warm = first ? 1 : 0;
-          a.oml = (float)(1.0 - c->p.lambda);
-          a.la = (float)(c->p.lambda * c->p.alpha);
-        } else {
-          a.warm = (it % c->p.boot_period == 0) ? 1 : 0;
-          a.oml = 0.f;
-          a.la = (float)c->p.boot_alpha;
-        }
-        a.status = (first && status) ? status + s0 : nullptr;
-        a.r_copy = (last && r_out) ? r_out + so : nullptr;
-        a.phi_copy = (last && phi_out) ? phi_out + so : nullptr;
-        DDH_LAUNCH(c, K_KA, ddh::launch_ka(a, c->st));
-        DDH_LAUNCH(c, K_KB, ddh::launch_kb(a, c->st));
-        DDH_LAUNCH(c, K_KC, ddh::launch_kc(a, c->st));
-        cur ^= 1;
+      // lanes: sub-groups of streams on their own CUDA streams (fork/join
+      // with events); each sub-group uses its own slice of the workspace
+      const int L = std::min(c->lanes, sc);
+      if (L > 1) {
+        DDH_CK(c, cudaEventRecord(c->lane_ev[8], c->st));
+        for (int l = 0; l < L; ++l) DDH_CK(c, cudaStreamWaitEvent(c->lane_st[l], c->lane_ev[8], 0));
       }
+      for (int l = 0; l < L; ++l) {
+        const int g0 = (int)((long)sc * l / L), g1 = (int)((long)sc * (l + 1) / L);
+        const size_t go = (size_t)(s0 + g0) * P;
+        cudaStream_t st = L > 1 ? c->lane_st[l] : c->st;
+        StepArgs b = a;
+        b.sc = g1 - g0;
+        b.y = y + go;
+        b.r_state = c->r + go;
+        b.cbuf = c->cbuf + (size_t)g0 * P;
+        b.part1 = c->part1 + (size_t)g0 * c->cs;
+        b.stats = c->stats + (size_t)g0 * 5;
+        int cl = cur;
+        for (int it = 0; it < iters; ++it) {
+          const bool first = (it == 0), last = (it == iters - 1);
+          b.phi_in = c->phi[cl] + go;
+          b.phi_out = c->phi[cl ^ 1] + go;
+          b.apply_plane = (plane && first) ? 1 : 0;
+          if (mode == Mode::Step) {
+            b.warm = first ? 1 : 0;
+            b.oml = (float)(1.0 - c->p.lambda);
+            b.la = (float)(c->p.lambda * c->p.alpha);
+          } else {
+            b.warm = (it % c->p.boot_period == 0) ? 1 : 0;
+            b.oml = 0.f;
+            b.la = (float)c->p.boot_alpha;
+          }
+          b.status = (first && status) ? status + s0 + g0 : nullptr;
+          b.r_copy = (last && r_out) ? r_out + go : nullptr;
+          b.phi_copy = (last && phi_out) ? phi_out + go : nullptr;
+          DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
+          DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
+          DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
+          cl ^= 1;
+        }
+      }
+      if (L > 1) {
+        for (int l = 0; l < L; ++l) {
+          DDH_CK(c, cudaEventRecord(c->lane_ev[l], c->lane_st[l]));
+          DDH_CK(c, cudaStreamWaitEvent(c->st, c->lane_ev[l], 0));
+        }
+      }
+      cur ^= (iters & 1);
       continue;
     }
     DDH_LAUNCH(c, K_STATS, ddh::launch_k0(a, c->st));
@@ -327,6 +362,10 @@ double inv3(const double G[9], double out[9]) {
 void free_ctx(ddh_ctx *c) {
   if (!c) return;
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->lane_ev)
+    if (e) cudaEventDestroy(e);
+  for (cudaStream_t s : c->lane_st)
+    if (s) cudaStreamDestroy(s);
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw,
                   c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
@@ -361,6 +400,7 @@ ddh_status ddh_default_params(ddh_params *p) {
   p->boot_alpha = 1.0;
   p->chunk_streams = 0;
   p->flags = 0;
+  p->lanes = 0;
   return DDH_OK;
 }
 
@@ -381,6 +421,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (p.boot_period < 1 || !(p.boot_alpha > 0))
     return fail(nullptr, DDH_E_INVAL, "ddh_create: boot_period >= 1 and boot_alpha > 0 required");
   if (p.chunk_streams < 0) return fail(nullptr, DDH_E_INVAL, "ddh_create: chunk_streams must be >= 0");
+  if (p.lanes < 0 || p.lanes > 8) return fail(nullptr, DDH_E_INVAL, "ddh_create: lanes must be in [0, 8]");
   if (!(p.aperture_diam > 0) && !p.aperture_mask)
     return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture_diam <= 0 requires aperture_mask");
 
@@ -490,6 +531,14 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (c->fused) {
     c->cs = ddh::fused_cluster(n);
     A(ddh::init_fused(n));
+    const char *ev = std::getenv("DDH_LANES");  // diagnostic override
+    c->lanes = ev ? std::atoi(ev) : p.lanes;
+    if (c->lanes <= 0) c->lanes = std::min(4, std::max(1, c->sc / 16));
+    c->lanes = std::max(1, std::min(8, c->lanes));
+    if (c->lanes > 1) {
+      for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
+      for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
+    }
   }
   // state: n = 0, r = r_min, phi = 0 (Fig. 1; R14)
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));

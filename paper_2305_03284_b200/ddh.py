@@ -44,6 +44,7 @@ class DdhParams(ctypes.Structure):
         ("boot_alpha", ctypes.c_double),
         ("chunk_streams", ctypes.c_int32),
         ("flags", ctypes.c_uint32),
+        ("lanes", ctypes.c_int32),
     ]
 
 

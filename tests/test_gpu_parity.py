@@ -389,12 +389,15 @@ def test_sharding_and_launch_groups_bit_exact():
     y, _, _ = frames(n, S, 3)
     yt = torch.from_numpy(y).to(DEV)
     outs = []
-    for chunk in (1, 4):
-        ctx = DDH(n, S, noise_var=0.1, chunk_streams=chunk)
+    for chunk, lanes in ((1, 1), (4, 1), (4, 3), (4, 4)):
+        ctx = DDH(n, S, noise_var=0.1, chunk_streams=chunk, lanes=lanes)
         po = torch.empty((3, S, n, n), device=DEV)
-        ctx.step(yt, po)
-        outs.append(po)
-    assert torch.equal(outs[0], outs[1])
+        ro = torch.empty_like(po)
+        ctx.step(yt, po, ro)
+        outs.append((po, ro))
+    for po, ro in outs[1:]:
+        assert torch.equal(outs[0][0], po) and torch.equal(outs[0][1], ro)
+    outs = [o[0] for o in outs]
     halves = []
     for h in range(2):
         ctx = DDH(n, 2, noise_var=0.1)

@@ -17,7 +17,7 @@ for what in "$@"; do
       echo "quick rc=$?"; python - <<'PY'
 import json
 d = json.loads(open("gpurun_out/quick.log").read().strip().splitlines()[-1])
-print("value", round(d["value"]), "plain", round(d["uninstrumented"]["value"]), "parity", d.get("parity"))
+print("value", round(d["value"]), "attr", round(d["attribution_pass"]["value"]), "parity", d.get("parity"))
 print({k: (round(v["ms_total"] / d["steps"] * 1000, 1), round(v.get("gbs", 0))) for k, v in d["kernels"].items()})
 PY
       ;;
