@@ -50,6 +50,13 @@ KERNEL_BYTES_PER_PX = {
     "kf_rows_fwd": 8 + 4 + 8,       # y, phi -> spectrum
     "kf_cols": 8 + 4 + 4 + 8,       # spectrum, r -> r, spectrum
     "kf_rows_inv": 8 + 8 + 4 + 4,   # spectrum, y, phi -> phi
+    # streaming path (default)
+    "ks_stats": 8 + 4,              # y, phi
+    "ks_rows_fwd": 8 + 4 + 8,       # y, phi -> spectrum
+    "ks_cols": 8 + 4 + 4 + 4 + 8,   # spectrum, r -> r0, q, spectrum
+    "ks_ricd": 4 + 4 + 4,           # r0, q -> r
+    "ks_rows_inv": 8 + 8 + 4 + 4,   # spectrum, y -> c, theta
+    "ks_phiicd": 4 + 4 + 4 + 4,     # phi, c, theta -> phi
 }
 STEP_BYTES_PER_PX = 24  # y in (8) + r in/out (8) + phi in/out (8)
 
@@ -238,7 +245,8 @@ def run_ours(args):
     if args.priors_off:  # diagnostic only (isolates the ICD cost); never the reported configuration
         extra = dict(r_sigma=0.0, phi_sigma=0.0)
     if args.unfused:
-        extra["flags"] = 2
+        args.path = "multipass"
+    extra["flags"] = {"stream": 0, "cluster": 4, "multipass": 2}[args.path]
     ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk, **extra)
     K, W = args.steps, args.warmup
     for w in range(W):
@@ -316,7 +324,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": dict(workload_config(cfg), parallelism=f"streams x{ws} GPUs",
-                                                           lanes=lanes,
+                                                           lanes=lanes, path=args.path,
                                                            synth_seconds=round(gen_s, 1)),
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks,
         "attribution_pass": {"value": frames_total / (ms_attr * 1e-3), "ms_per_step": ms_attr / K, "lanes": 1,
@@ -456,7 +464,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--priors-off", action="store_true", help="diagnostic: disable both priors")
-    ap.add_argument("--unfused", action="store_true", help="diagnostic: multi-pass kernels")
+    ap.add_argument("--unfused", action="store_true", help="diagnostic: multi-pass kernels (= --path multipass)")
+    ap.add_argument("--path", choices=["stream", "cluster", "multipass"], default="stream",
+                    help="EM-iteration implementation (default: streaming)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -52,8 +52,10 @@ typedef enum {
 
 /* flags */
 #define DDH_F_NO_TIPTILT 1u /* skip RemoveTipTilt (Fig. 1) in ddh_step  */
-#define DDH_F_UNFUSED 2u    /* force the multi-pass kernels (default for N <= 512:
-                               the cluster-fused 3-kernel iteration)            */
+#define DDH_F_UNFUSED 2u    /* force the multi-pass kernels K0-K3b (reference
+                               structure, used as a second implementation)      */
+#define DDH_F_CLUSTER 4u    /* force the cluster-fused 3-kernel iteration (N <= 512);
+                               default: the streaming 6-kernel iteration          */
 
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 
@@ -172,7 +174,7 @@ int64_t ddh_frame_index(const ddh_ctx *c);
  * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
  * 8 KA kf_rows_fwd, 9 KB kf_cols, 10 KC kf_rows_inv (cluster-fused path).
  * When enabled, every launch of the ctx is bracketed by two events. */
-#define DDH_KIND_COUNT 11
+#define DDH_KIND_COUNT 17
 ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable);
 /* Synchronises the ctx stream and ADDS the accumulated totals since the last
  * read into ms[k] (milliseconds) and launches[k] (host arrays of

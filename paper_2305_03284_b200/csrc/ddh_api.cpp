@@ -43,6 +43,8 @@ struct ddh_ctx {
   double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
   bool fused = false;
   int cs = 0;  // CTAs per stream of the fused path
+  bool streaming = false;  // cluster-free 6-kernel path (ddh_stream.cu)
+  float4 *tw4 = nullptr;
   float *pmax = nullptr;
   // constants
   int2 *rowspan = nullptr;
@@ -92,10 +94,12 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
       return fail((c), DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC };
+enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
+            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
-                                          "kf_rows_fwd", "kf_cols", "kf_rows_inv"};
+                                          "kf_rows_fwd", "kf_cols", "kf_rows_inv",
+                                          "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
@@ -149,6 +153,7 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
   a.part1 = c->part1;
   a.rowspan = c->rowspan;
   a.tw = c->tw;
+  a.tw4 = c->tw4;
   a.s2 = (float)c->p.noise_var;
   a.r_min = (float)c->p.r_min;
   a.P = (float)c->P;
@@ -159,6 +164,10 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
     a.r_b0 = (float)(1.0 / (2.0 * c->p.r_sigma * c->p.r_sigma));
     a.r_inv_Tsig = (float)(1.0 / (c->p.r_T * c->p.r_sigma));
     a.r_tmq = (float)(2.0 - c->p.r_q);
+    a.r_b6 = (float)(1.0 / (12.0 * c->p.r_sigma * c->p.r_sigma));
+    a.r_h = (float)(0.5 * (2.0 - c->p.r_q));
+    a.r_g = (float)((2.0 - c->p.r_q) * std::log2(1.0 / (c->p.r_T * c->p.r_sigma)));
+    a.r_k = (float)(0.5 * c->p.r_q);
   }
   a.sweeps = c->p.icd_sweeps;
   a.phi_prior = c->p.phi_sigma > 0 ? 1 : 0;
@@ -259,6 +268,79 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     a.phi_in = c->phi[cur] + so;
     a.want_y = 1;
     a.apply_plane = plane ? 1 : 0;
+    if (c->streaming) {  // S0 ; N_k x [S1 ; S2 ; sweeps x S3 ; S4 ; sweeps x S5]
+      const int L = std::min(c->lanes, sc);
+      if (L > 1) {
+        DDH_CK(c, cudaEventRecord(c->lane_ev[8], c->st));
+        for (int l = 0; l < L; ++l) DDH_CK(c, cudaStreamWaitEvent(c->lane_st[l], c->lane_ev[8], 0));
+      }
+      const int nb0 = ddh::stream_nb0(c->n), nb1 = ddh::stream_nb1(c->n);
+      const int sw = c->p.icd_sweeps;
+      for (int l = 0; l < L; ++l) {
+        const int g0 = (int)((long)sc * l / L), g1 = (int)((long)sc * (l + 1) / L);
+        const size_t go = (size_t)(s0 + g0) * P, wo = (size_t)g0 * P;  // state / workspace offsets
+        cudaStream_t st = L > 1 ? c->lane_st[l] : c->st;
+        StepArgs b = a;
+        b.sc = g1 - g0;
+        b.nb0 = nb0;
+        b.nb1 = nb1;
+        b.y = y + go;
+        b.r_state = c->r + go;
+        b.cbuf = c->cbuf + wo;
+        b.rinit = c->rinit + wo;
+        b.q = c->q + wo;
+        b.cc = c->cc + wo;
+        b.theta = c->theta + wo;
+        b.part0 = c->part0 + (size_t)g0 * nb0 * 5;
+        b.part1 = c->part1 + (size_t)g0 * nb1;
+        b.want_y = 1;
+        b.apply_plane = plane ? 1 : 0;
+        b.phi_in = c->phi[cur] + go;
+        DDH_LAUNCH_ON(c, K_S0, st, ddh::launch_s0(b, st));
+        int cl = cur;
+        for (int it = 0; it < iters; ++it) {
+          const bool first = (it == 0), last = (it == iters - 1);
+          b.phi_in = c->phi[cl] + go;
+          b.apply_plane = (plane && first) ? 1 : 0;
+          if (mode == Mode::Step) {
+            b.warm = first ? 1 : 0;
+            b.oml = (float)(1.0 - c->p.lambda);
+            b.la = (float)(c->p.lambda * c->p.alpha);
+          } else {
+            b.warm = (it % c->p.boot_period == 0) ? 1 : 0;
+            b.oml = 0.f;
+            b.la = (float)c->p.boot_alpha;
+          }
+          b.status = (first && status) ? status + s0 + g0 : nullptr;
+          DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
+          DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
+          for (int k = 0; k < sw; ++k) {  // r M-step sweeps
+            b.icd_in = k == 0 ? c->rinit + wo : c->rtmp[(k - 1) & 1] + wo;
+            b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
+            b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
+            DDH_LAUNCH_ON(c, K_S3, st, ddh::launch_s3(b, st));
+          }
+          DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
+          const int plane_it = b.apply_plane;
+          for (int k = 0; k < sw; ++k) {  // phi M-step sweeps (plane removed in the first)
+            b.icd_in = k == 0 ? c->phi[cl] + go : c->ptmp[(k - 1) & 1] + wo;
+            b.icd_out = k == sw - 1 ? c->phi[cl ^ 1] + go : c->ptmp[k & 1] + wo;
+            b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
+            b.apply_plane = k == 0 ? plane_it : 0;
+            DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+          }
+          cl ^= 1;
+        }
+      }
+      if (L > 1) {
+        for (int l = 0; l < L; ++l) {
+          DDH_CK(c, cudaEventRecord(c->lane_ev[l], c->lane_st[l]));
+          DDH_CK(c, cudaStreamWaitEvent(c->st, c->lane_ev[l], 0));
+        }
+      }
+      cur ^= (iters & 1);
+      continue;
+    }
     if (c->fused) {  // KA -> KB -> KC per EM iteration (cluster per stream)
       a.nb1 = c->cs;
       // lanes: sub-groups of streams on their own CUDA streams (fork/join
@@ -367,7 +449,7 @@ void free_ctx(ddh_ctx *c) {
   for (cudaStream_t s : c->lane_st)
     if (s) cudaStreamDestroy(s);
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
-                  c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw,
+                  c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
                   c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -501,14 +583,15 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   A(dalloc(&c->q, SC * P));
   A(dalloc(&c->cc, SC * P));
   A(dalloc(&c->theta, SC * P));
+  A(dalloc(&c->tw4, (size_t)n));
   if (p.icd_sweeps > 1) {
     A(dalloc(&c->rtmp[0], SC * P));
     A(dalloc(&c->rtmp[1], SC * P));
     A(dalloc(&c->ptmp[0], SC * P));
     A(dalloc(&c->ptmp[1], SC * P));
   }
-  A(dalloc(&c->part0, SC * c->nb0 * 5));
-  A(dalloc(&c->part1, SC * std::max(c->nb1, 16)));
+  A(dalloc(&c->part0, SC * std::max(c->nb0, ddh::stream_nb0(n)) * 5));
+  A(dalloc(&c->part1, SC * std::max(std::max(c->nb1, 16), ddh::stream_nb1(n))));
   A(dalloc(&c->stats, SC * 5));
   A(dalloc(&c->pmax, SC * c->strehl_nb));
   A(dalloc(&c->rowspan, (size_t)n));
@@ -525,12 +608,26 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     tw[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
   }
   A(cudaMemcpy(c->tw, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+  {  // packed twiddles (w.x, w.y, -w.y, w.x) of the streaming path
+    std::vector<float4> tw4(n);
+    for (int m = 0; m < n; ++m) tw4[m] = make_float4(tw[m].x, tw[m].y, -tw[m].y, tw[m].x);
+    A(cudaMemcpy(c->tw4, tw4.data(), n * sizeof(float4), cudaMemcpyHostToDevice));
+  }
   A(cudaMemcpy(c->rowspan, span.data(), n * sizeof(int2), cudaMemcpyHostToDevice));
   A(ddh::init_kernels(n));
-  c->fused = ddh::fused_supported(n) && !(p.flags & DDH_F_UNFUSED);
-  if (c->fused) {
-    c->cs = ddh::fused_cluster(n);
-    A(ddh::init_fused(n));
+  {
+    const char *pe = std::getenv("DDH_PATH");  // diagnostic override: stream | cluster | multipass
+    const std::string path = pe ? pe : "";
+    if (path == "multipass" || (path.empty() && (p.flags & DDH_F_UNFUSED))) {
+      c->fused = c->streaming = false;
+    } else if (path == "cluster" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
+      c->fused = ddh::fused_supported(n);
+    } else {
+      c->streaming = true;
+    }
+  }
+  if (c->streaming) A(ddh::init_stream(n));
+  if (c->streaming || ddh::fused_supported(n)) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = ev ? std::atoi(ev) : p.lanes;
     if (c->lanes <= 0) c->lanes = std::min(4, std::max(1, c->sc / 16));
@@ -539,6 +636,10 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
+  }
+  if (c->fused) {
+    c->cs = ddh::fused_cluster(n);
+    A(ddh::init_fused(n));
   }
   // state: n = 0, r = r_min, phi = 0 (Fig. 1; R14)
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));

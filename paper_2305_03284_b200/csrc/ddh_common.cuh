@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include "ddh_f32x2.cuh"
+
 namespace ddh {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -106,6 +108,24 @@ __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
   return fmaf(1.f - k, r, k) * r;
 }
 
+// The same weight for a pair of neighbours (rj.x, rj.y) of pixel ri on packed
+// FP32 pairs (fused path): t = (|d| / (T sig))^(2-q) = 2^(h lg2(d^2 + tiny) + g)
+// with h = (2-q)/2, g = (2-q) lg2(1/(T sig)); the 1e-37 floor keeps lg2 finite
+// at d = 0 (t ~ 2^-49 there, and t = 1 exactly at q = 2).  1/(1+t) on the FMA
+// pipe: magic-constant seed + 3 Newton steps (rel. error < 2e-7), which leaves
+// 2 MUFU per neighbour (lg2, ex2) instead of 3.  Returns (w(d.x), w(d.y)).
+__device__ __forceinline__ float2 qgg_w2(float ri, float2 rj, float h, float g, float k) {
+  const float2 d = p_sub(bc2(ri), rj);
+  const float2 a = p_fma(d, d, bc2(1e-37f));
+  const float2 e = p_fma(make_float2(lg2_approx(a.x), lg2_approx(a.y)), bc2(h), bc2(g));
+  const float2 u = p_add(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(1.f));
+  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(u.x)), __int_as_float(0x7EF311C3 - __float_as_int(u.y)));
+  const float2 nu = make_float2(-u.x, -u.y);
+#pragma unroll
+  for (int it = 0; it < 3; ++it) y = p_mul(y, p_fma(nu, y, bc2(2.f)));
+  return p_mul(p_fma(y, bc2(1.f - k), bc2(k)), y);  // (k + (1-k)/u) / u
+}
+
 // ---- r M-step, one pixel (R9) -------------------------------------------
 // Minimiser over x >= r_min of f(x) = log x + q/x + B x^2 - 2 S x (B > 0).
 // f'(x) = g(x)/x^2 with g(x) = 2B x^3 - 2S x^2 + x - q, g(0) = -q < 0; g is
@@ -124,6 +144,17 @@ __host__ __device__ __forceinline__ float g_of(float x, float B2, float S2, floa
   return fmaf(fmaf(fmaf(B2, x, -S2), x, 1.f), x, -q);
 }
 __host__ __device__ __forceinline__ float dg_of(float x, float B6, float S4) { return fmaf(fmaf(B6, x, -S4), x, 1.f); }
+
+// sqrt(x) for x > 0 normal by one MUFU.RSQ (only classifies the root set)
+__host__ __device__ __forceinline__ float sqrt_approx(float x) {
+#ifdef __CUDA_ARCH__
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return x * y;
+#else
+  return sqrtf(x);
+#endif
+}
 
 #define DDH_FDIV(a, b) ((a) * rcp_approx(b))
 
@@ -176,7 +207,7 @@ __host__ __device__ __forceinline__ float r_update(float rc, float q, float B, f
   // within rounding of each other's surrogate value, so either choice is exact)
   bool has_small, has_large;
   if (S > 0.f && disc > 0.f) {
-    const float x2 = (2.f * S + sqrtf(disc)) * iB * (1.f / 6.f);
+    const float x2 = (2.f * S + sqrt_approx(disc)) * iB * (1.f / 6.f);
     const float x1 = iB * (1.f / 6.f) * rcp_approx(x2);  // x1 x2 = 1/(6B)
     has_small = g_of(x1, B2, S2, q) > 0.f;
     has_large = g_of(x2, B2, S2, q) < 0.f;

@@ -285,9 +285,9 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
     float *left = cl.map_shared_rank(rS, (rank + CS - 1) % CS);
     float *right = cl.map_shared_rank(rS, (rank + 1) % CS);
 #pragma unroll 1
-    for (int cc = 0; cc < 4 * A.sweeps; ++cc) {
-      const int c = cc & 3;
-      {
+    for (int sw = 0; sw < A.sweeps; ++sw) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
         DDH_SYNC_T(cl.sync());
         // halos: neighbour columns for all padded rows (rows 0 / N+1 take the
         // neighbours' data rows N / 1) and the periodic row wrap of own columns
@@ -302,30 +302,38 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
         }
         DDH_SYNC_T(__syncthreads());
         const int ci = c >> 1, cj = c & 1;
+        // pixels of one colour never neighbour each other: gather B, S of all
+        // of this thread's colour-c pixels first (independent chains the
+        // scheduler can interleave), then update, then store
+        float Bv[EPT / 4], Sv[EPT / 4], Rv[EPT / 4];
 #pragma unroll
         for (int k = 0; k < EPT / 4; ++k) {
           const int b = tid + k * NT;
           const int br = b / (W / 2), bc = b % (W / 2);
           const int ki = 2 * br + ci + 1, lj = 2 * bc + cj + 1;  // padded coordinates
           const float ri = rS[ki * RP + lj];
-          float B4 = 0.f, S4 = 0.f, Bd = 0.f, Sd = 0.f;  // nearest / diagonal neighbours
+          // neighbour pairs (nearest: up/down, left/right; diagonal: upper, lower)
+          const float2 nA = make_float2(rS[(ki - 1) * RP + lj], rS[(ki + 1) * RP + lj]);
+          const float2 nB = make_float2(rS[ki * RP + lj - 1], rS[ki * RP + lj + 1]);
+          const float2 dA = make_float2(rS[(ki - 1) * RP + lj - 1], rS[(ki - 1) * RP + lj + 1]);
+          const float2 dB = make_float2(rS[(ki + 1) * RP + lj - 1], rS[(ki + 1) * RP + lj + 1]);
+          const float2 wA = qgg_w2(ri, nA, A.r_h, A.r_g, A.r_k), wB = qgg_w2(ri, nB, A.r_h, A.r_g, A.r_k);
+          const float2 wC = qgg_w2(ri, dA, A.r_h, A.r_g, A.r_k), wD = qgg_w2(ri, dB, A.r_h, A.r_g, A.r_k);
+          // b = 1/6 (nearest), 1/12 (diagonal), times 1/(2 sig_r^2) = r_b0:
+          // B = (r_b0/6) (sum_4 w + sum_d w / 2), S likewise with w r_j
+          const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+          const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+          Bv[k] = A.r_b6 * (bs.x + bs.y);
+          Sv[k] = A.r_b6 * (ss.x + ss.y);
+          Rv[k] = ri;
+        }
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const float rj = rS[(ki + nb_di(m)) * RP + lj + nb_dj(m)];  // periodic rows via the wrap halo
-            const float bt = qgg_w(ri - rj, A.r_inv_Tsig, A.r_tmq);
-            if (m < 4) {
-              B4 += bt;
-              S4 = fmaf(bt, rj, S4);
-            } else {
-              Bd += bt;
-              Sd = fmaf(bt, rj, Sd);
-            }
-          }
-          // b = 1/6 (nearest), 1/12 (diagonal), times 1/(2 sig_r^2)
-          const float B = A.r_b0 * fmaf(Bd, 1.f / 12.f, B4 * (1.f / 6.f));
-          const float S = A.r_b0 * fmaf(Sd, 1.f / 12.f, S4 * (1.f / 6.f));
-          const float qv = c == 0 ? qreg[k * 4] : c == 1 ? qreg[k * 4 + 1] : c == 2 ? qreg[k * 4 + 2] : qreg[k * 4 + 3];
-          rS[ki * RP + lj] = r_update(ri, qv, B, S, A.r_min);
+        for (int k = 0; k < EPT / 4; ++k) Rv[k] = r_update(Rv[k], qreg[k * 4 + c], Bv[k], Sv[k], A.r_min);
+#pragma unroll
+        for (int k = 0; k < EPT / 4; ++k) {
+          const int b = tid + k * NT;
+          const int br = b / (W / 2), bc = b % (W / 2);
+          rS[(2 * br + ci + 1) * RP + 2 * bc + cj + 1] = Rv[k];
         }
       }
     }

@@ -51,9 +51,15 @@ struct StepArgs {
   float *phi_copy, *r_copy;  // optional user outputs [sc][N][N] or null
   int r_prior;            // qGGMRF on
   float r_b0, r_inv_Tsig, r_tmq;  // 1/(2 sig_r^2), 1/(T sig_r), 2 - q
+  float r_b6, r_h, r_g, r_k;       // r_b0/6, (2-q)/2, (2-q) log2(1/(T sig_r)), q/2 (qgg_w2)
   int phi_prior;          // GMRF on
   float phi_w;            // 1/sig_phi^2
   int sweeps;             // ICD colour sweeps per M-step (R8)
+  // streaming path (ddh_stream.cu)
+  const float4 *tw4;      // [N] (w.x, w.y, -w.y, w.x), w = e^{-2 pi i m / N}
+  const float *icd_in;    // S3: r before the sweep; S5: phi before the sweep [sc][N][N]
+  float *icd_out;         // S3 / S5 output [sc][N][N]
+  float *icd_copy;        // optional user copy of the output or null
 };
 
 struct IcdArgs {
@@ -109,6 +115,18 @@ cudaError_t init_fused(int n);
 cudaError_t launch_ka(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st);
+
+// streaming (cluster-free) EM iteration, ddh_stream.cu: S0 stats, S1 rows,
+// S2 cols + E-step, S3 r-ICD tiles, S4 inverse rows + c/theta, S5 phi-ICD tiles
+cudaError_t init_stream(int n);
+int stream_nb0(int n);  // S0 blocks per stream
+int stream_nb1(int n);  // S1 row blocks per stream (part1 entries)
+cudaError_t launch_s0(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s1(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
 
 cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
                               cudaStream_t st);

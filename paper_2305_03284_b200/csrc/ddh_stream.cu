@@ -1,0 +1,569 @@
+// ddh_stream.cu -- the streaming (cluster-free) EM iteration, sm_100a.
+//
+// One EM iteration of S independent streams (Fig. 1) as six
+// kernels with no inter-CTA dependency inside a launch, so every launch
+// packs the SMs freely (no thread-block-cluster co-scheduling, no wave
+// quantisation at the cluster granularity) and the launches of different
+// stream sub-groups ("lanes", ddh_api.cpp) overlap on the GPU:
+//
+//   S0 ks_stats     per stream: sum y (Eq. 4 mean) and the
+//                   RemoveTipTilt normal-equation sums of phi
+//   S1 ks_rows_fwd  z = chi a e^{-j phi'} (y - mu); forward row DFT;
+//                   partial ||y - mu||^2
+//   S2 ks_cols      column DFT -> u = A^H y-hat (R13); Eq. 3; E-step (R1)
+//                   -> r0, q to HBM; FFT of conj(chi mu) (the inverse column
+//                   DFT by conjugation)
+//   S3 ks_ricd      qGGMRF r-ICD on 64x64 tiles with a 4-pixel periodic halo
+//                   (one colour sweep, R6-R9), recomputing the halo ring
+//   S4 ks_rows_inv  row DFT of the conjugated spectrum -> f = F_c^{-1} mu;
+//                   c = (2/s2)|y-hat||f|, theta = arg(y-hat conj f)
+//   S5 ks_phiicd    GMRF phi-ICD on 64x64 tiles, 4-pixel halo, free edge
+//                   (R10-R11)
+//
+// FFTs are register-resident (ddh_fft_reg.cuh: one shared-memory exchange at
+// N <= 256), all arithmetic on complex pairs uses packed FP32x2 instructions.
+// The ICD kernels store the tile colour-separated (four (i mod 2, j mod 2)
+// sub-grids), so a colour phase reads and writes consecutive words.
+#include "ddh_common.cuh"
+#include "ddh_fft_reg.cuh"
+#include "ddh_kernels.h"
+
+namespace ddh {
+
+namespace {
+
+constexpr int kSThreads = 256;
+
+template <int N> struct SCfg {
+  static constexpr int E = RPlan<N>::E;
+  static constexpr int TPV = N / E;                                  // threads per vector
+  static constexpr int H = (kSThreads / TPV) < 1 ? 1 : kSThreads / TPV;  // rows per row CTA
+  static constexpr int NTR = H * TPV;                                // threads per row CTA
+  static constexpr int W = (kSThreads / TPV) < 16 ? 16 : kSThreads / TPV;  // cols per col CTA
+  static constexpr int NTC = W * TPV;                                // threads per col CTA
+  static constexpr int RPITCH = N + N / 16;                          // padded row pitch
+};
+
+__device__ __forceinline__ void sincos_red(float p, float &sn, float &cs) {
+  // |argument| <= pi after one rint reduction, then MUFU sin/cos
+  __sincosf(fmaf(-6.283185307179586f, rintf(p * 0.15915494309189535f), p), &sn, &cs);
+}
+
+// Warp 0: per-stream totals of the S0 partials (fixed order) -> out[0..4]
+__device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int nb0, int s, double *out) {
+  const int lane = threadIdx.x & 31;
+  double v[5] = {0, 0, 0, 0, 0};
+  for (int b = lane; b < nb0; b += 32) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) v[k] += part0[((size_t)s * nb0 + b) * 5 + k];
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    v[k] = warp_sum(v[k]);
+    if (lane == 0) out[k] = v[k];
+  }
+}
+__device__ __forceinline__ double sum_part1(const double *__restrict__ part1, int nb1, int s) {
+  const int lane = threadIdx.x & 31;
+  double v = 0.0;
+  for (int b = lane; b < nb1; b += 32) v += part1[(size_t)s * nb1 + b];
+  return warp_sum(v);
+}
+
+template <int N>
+__device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g, int tid, int nt) {
+  for (int k = tid; k < N; k += nt) tw[k] = g[k];
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ S0
+
+// grid (nb0, sc), block 256: block b sums pixels [b P/nb0, (b+1) P/nb0) of
+// stream s, 8 consecutive pixels per thread and iteration (16-byte loads).
+__global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
+  __shared__ double red[32 * 5];
+  const int n = A.n, lg = 31 - __clz(n);
+  const size_t P = (size_t)n * n;
+  const int s = blockIdx.y;
+  const size_t per = P / A.nb0;
+  const size_t base = blockIdx.x * per;
+  const size_t off = (size_t)s * P;
+  double v[5] = {0, 0, 0, 0, 0};
+  for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
+    const float4 *y4 = reinterpret_cast<const float4 *>(A.y + off + p0);
+    float sr = 0.f, si = 0.f;
+    if (A.want_y) {
+      float4 a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] = __ldg(y4 + k);  // kept in L2 for S1
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        sr += a[k].x + a[k].z;
+        si += a[k].y + a[k].w;
+      }
+    }
+    v[0] += (double)sr;
+    v[1] += (double)si;
+    if (A.apply_plane) {
+      const int i = (int)(p0 >> lg), j0 = (int)(p0 & (n - 1));
+      const int2 sp = __ldg(A.rowspan + i);
+      const float4 *f4 = reinterpret_cast<const float4 *>(A.phi_in + off + p0);
+      const float4 f0 = f4[0], f1 = f4[1];
+      const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+      float s0 = 0.f, sx = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = j0 + k;
+        const float fk = (j >= sp.x && j < sp.y) ? f[k] : 0.f;
+        s0 += fk;
+        sx = fmaf(fk, (float)(j - n / 2), sx);
+      }
+      v[2] += (double)s0;
+      v[3] += (double)sx;
+      v[4] += (double)s0 * (double)(i - n / 2);
+    }
+  }
+  block_sum<5>(v, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + k] = v[k];
+  }
+}
+
+// ------------------------------------------------------------------ S1
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
+  using C = SCfg<N>;
+  constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;                                             // [N]
+  float2 *buf = reinterpret_cast<float2 *>(smem4 + N);            // [H][RPITCH]
+  __shared__ double st[5];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int t = tid % TPV, b = tid / TPV;
+  const int i = blockIdx.x * H + b;
+  const size_t off = (size_t)s * P;
+  const size_t row = off + (size_t)i * N;
+  // issue the loads first (y: 8 B, phi: 4 B per pixel, comb t + TPV e)
+  float2 v[E];
+  float ph[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = A.y[row + t + TPV * e];
+#pragma unroll
+  for (int e = 0; e < E; ++e) ph[e] = A.phi_in[row + t + TPV * e];
+  load_tw<N>(tw, A.tw4, tid, NT);
+  if (tid < 32) {
+    double sums[5];
+    sum_part0(A.part0, A.nb0, s, sums);
+    if (tid == 0) {
+      st[0] = sums[0] / P;
+      st[1] = sums[1] / P;
+      double c[3] = {0, 0, 0};
+      if (A.apply_plane) plane_from_sums(sums, A.minv, c);
+      st[2] = c[0];
+      st[3] = c[1];
+      st[4] = c[2];
+    }
+  }
+  __syncthreads();
+  const float mur = (float)st[0], mui = (float)st[1];
+  const float c0 = (float)st[2], c1 = (float)st[3], c2 = (float)st[4];
+  const int2 sp = __ldg(A.rowspan + i);
+  const float pyi = fmaf(c2, (float)(i - N / 2), c0);
+  float acc = 0.f;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = t + TPV * e;
+    const float2 d = p_sub(v[e], make_float2(mur, mui));
+    acc = fmaf(d.x, d.x, fmaf(d.y, d.y, acc));
+    float2 z = make_float2(0.f, 0.f);
+    if (j >= sp.x && j < sp.y) {
+      float sn, cs;
+      sincos_red(ph[e] - fmaf(c1, (float)(j - N / 2), pyi), sn, cs);
+      // (y - mu) e^{-j phi'} = d (cs - i sn), times chi = (-1)^(i+j)
+      const float sg = ((i + j) & 1) ? -1.f : 1.f;
+      z = p_fma(bc2(d.x * sg), make_float2(cs, -sn), p_mul(bc2(d.y * sg), make_float2(sn, cs)));
+    }
+    v[e] = z;
+  }
+  double a1[1] = {(double)acc};
+  block_sum<1>(a1, red);  // also: every thread is past its smem use before the FFT
+  if (tid == 0) A.part1[(size_t)s * A.nb1 + blockIdx.x] = a1[0];
+  fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) A.cbuf[row + t + TPV * out_comb<N>(e)] = v[e];
+}
+
+// ------------------------------------------------------------------ S2
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTC) ks_cols(StepArgs A) {
+  using C = SCfg<N>;
+  constexpr int E = C::E, TPV = C::TPV, W = C::W, NT = C::NTC, P = N * N;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;                                   // [N]
+  float2 *buf = reinterpret_cast<float2 *>(smem4 + N);  // [N][W]
+  __shared__ double st[1];
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int b = tid % W, t = tid / W;
+  const int col = blockIdx.x * W + b;
+  const size_t off = (size_t)s * P;
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = A.cbuf[off + (size_t)(t + TPV * e) * N + col];
+  float rp[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) rp[e] = A.r_state[off + (size_t)(t + TPV * out_comb<N>(e)) * N + col];
+  load_tw<N>(tw, A.tw4, tid, NT);
+  if (tid < 32) {
+    const double d2 = sum_part1(A.part1, A.nb1, s);
+    if (tid == 0) st[0] = d2;
+  }
+  __syncthreads();
+  const double d2 = st[0];
+  const bool degenerate = !(d2 > 0.0);
+  if (A.status && blockIdx.x == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
+  const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+  const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
+  fft_reg<N>(v, t, buf + b, [](int p) { return p * W; }, tw);
+  const bool warm = A.warm && !degenerate;
+  float2 w2[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int ki = t + TPV * out_comb<N>(e);
+    const size_t g = off + (size_t)ki * N + col;
+    const float sg = ((ki + col) & 1) ? -scale : scale;
+    const float2 u = p_mul(v[e], bc2(sg));
+    float r0 = rp[e];
+    if (warm) r0 = fmaxf(fmaf(A.oml, r0, A.la * fmaf(u.x, u.x, u.y * u.y)), A.r_min);  // Eq. 3
+    const float w = r0 * rcp_approx(r0 + A.s2);                                        // E-step (R1)
+    const float2 mu = p_mul(u, bc2(w));
+    A.rinit[g] = r0;
+    A.q[g] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+    // conj(chi mu) into input position out_comb(e) of the next FFT
+    const float cs = ((ki + col) & 1) ? -1.f : 1.f;
+    w2[out_comb<N>(e)] = make_float2(cs * mu.x, -cs * mu.y);
+  }
+  __syncthreads();  // exchange buffer free
+  fft_reg<N>(w2, t, buf + b, [](int p) { return p * W; }, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) A.cbuf[off + (size_t)(t + TPV * out_comb<N>(e)) * N + col] = w2[e];
+}
+
+// ------------------------------------------------------------------ S4
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
+  using C = SCfg<N>;
+  constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;
+  float2 *buf = reinterpret_cast<float2 *>(smem4 + N);
+  __shared__ double st[3];
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int t = tid % TPV, b = tid / TPV;
+  const int i = blockIdx.x * H + b;
+  const size_t row = (size_t)s * P + (size_t)i * N;
+  float2 v[E], yv[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = A.cbuf[row + t + TPV * e];
+#pragma unroll
+  for (int e = 0; e < E; ++e) yv[e] = A.y[row + t + TPV * out_comb<N>(e)];
+  load_tw<N>(tw, A.tw4, tid, NT);
+  if (tid < 32) {
+    double sums[5];
+    sum_part0(A.part0, A.nb0, s, sums);
+    const double d2 = sum_part1(A.part1, A.nb1, s);
+    if (tid == 0) {
+      st[0] = sums[0] / P;
+      st[1] = sums[1] / P;
+      st[2] = d2;
+    }
+  }
+  __syncthreads();
+  const float mur = (float)st[0], mui = (float)st[1];
+  const double d2 = st[2];
+  const float kappa = d2 > 0.0 ? (float)sqrt((double)P / d2) : 0.f;
+  fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
+  // v = G = conj(F) with F = inverse row DFT; f = chi F / N, so
+  // z = y-hat conj(f) = y-hat chi G / N
+  const int2 sp = __ldg(A.rowspan + i);
+  const float kn = kappa / (float)N, two_s2 = 2.f / A.s2;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = t + TPV * out_comb<N>(e);
+    float c = 0.f, th = 0.f;
+    if (j >= sp.x && j < sp.y) {
+      const float sg = ((i + j) & 1) ? -kn : kn;
+      const float2 yh = p_mul(p_sub(yv[e], make_float2(mur, mui)), bc2(sg));
+      const float2 g = v[e];
+      const float2 z = p_fma(bc2(yh.x), g, p_mul(bc2(yh.y), make_float2(-g.y, g.x)));  // yh * g
+      c = two_s2 * sqrt_approx(fmaf(z.x, z.x, z.y * z.y) + 1e-37f);
+      th = atan2f(z.y, z.x);
+    }
+    A.cc[row + j] = c;
+    A.theta[row + j] = th;
+  }
+}
+
+// ------------------------------------------------------------ ICD tiles
+
+namespace {
+constexpr int kTile = 64, kHalo = 4, kReg = kTile + 2 * kHalo, kSub = kReg / 2, kSubP = kSub + 1;
+// colour-separated tile: sub-grid c = 2 (i&1) + (j&1), element (i>>1, j>>1)
+__device__ __forceinline__ int sidx(int c, int a, int b) { return (c * kSub + a) * kSubP + b; }
+// neighbour (di, dj) of a pixel of colour (ci, cj) at sub coords (a, b):
+// colour ((ci+di)&1, (cj+dj)&1), sub coords (a + floor((ci+di)/2), b + floor((cj+dj)/2))
+template <int CI, int CJ, int DI, int DJ>
+__device__ __forceinline__ int nidx(int a, int b) {
+  constexpr int ti = CI + DI, tj = CJ + DJ;
+  constexpr int pi = ti & 1, pj = tj & 1;
+  constexpr int oa = (ti - pi) / 2, ob = (tj - pj) / 2;
+  return sidx(2 * pi + pj, a + oa, b + ob);
+}
+// sub-coordinate range of colour parity p updated in a phase covering local
+// rows [lo, hi): smallest a with 2a+p >= lo, first a with 2a+p >= hi
+__host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 2; }
+}  // namespace
+
+// r M-step: one 4-colour sweep of the qGGMRF ICD (R6-R9) for the 64x64 tile
+// (blockIdx.x, blockIdx.y) of stream blockIdx.z, from A.icd_in (r after Eq. 3,
+// or the previous sweep) and A.q, into A.icd_out (+ A.icd_copy).  The tile is
+// loaded with a 4-pixel periodic halo; colour phase c updates the pixels of
+// colour c in the region shrunk by c+1 on each side, so after the 4 phases the
+// 64x64 core equals the global colour-ordered sweep.
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, P = N * N;
+  __shared__ float rs[4 * kSub * kSubP];
+  __shared__ double st[1];
+  const int tid = threadIdx.x, s = blockIdx.z;
+  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
+  const size_t off = (size_t)s * P;
+  const float *__restrict__ rin = A.icd_in + off;
+  const float *__restrict__ qin = A.q + off;
+  if (tid < 32) {
+    const double d2 = sum_part1(A.part1, A.nb1, s);
+    if (tid == 0) st[0] = d2;
+  }
+  for (int idx = tid; idx < kReg * kReg; idx += kSThreads) {
+    const int li = idx / kReg, lj = idx - li * kReg;
+    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + lj) & (N - 1);
+    rs[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)] = rin[(size_t)gi * N + gj];
+  }
+  __syncthreads();
+  const bool degenerate = !(st[0] > 0.0);
+  if (A.r_prior && !degenerate) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      // colour (CI, CJ) as compile-time values through a switch-free unroll
+      const int ci = c >> 1, cj = c & 1;
+      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(kReg - c - 1, ci);
+      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(kReg - c - 1, cj);
+      const int na = ahi - alo, nbb = bhi - blo, cnt = na * nbb;
+      constexpr int KMAX = (35 * 35 + kSThreads - 1) / kSThreads;  // 5
+      float Bv[KMAX], Sv[KMAX], Rv[KMAX];
+      int ix[KMAX];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const int p = tid + k * kSThreads;
+        ix[k] = -1;
+        if (p < cnt) {
+          const int a = alo + p / nbb, bb = blo + p % nbb;
+          float ri, n0, n1, n2, n3, d0, d1, d2v, d3;
+#define DDH_NB(CI, CJ)                                                                       \
+  ri = rs[sidx(2 * CI + CJ, a, bb)];                                                          \
+  n0 = rs[nidx<CI, CJ, -1, 0>(a, bb)]; n1 = rs[nidx<CI, CJ, 1, 0>(a, bb)];                    \
+  n2 = rs[nidx<CI, CJ, 0, -1>(a, bb)]; n3 = rs[nidx<CI, CJ, 0, 1>(a, bb)];                    \
+  d0 = rs[nidx<CI, CJ, -1, -1>(a, bb)]; d1 = rs[nidx<CI, CJ, -1, 1>(a, bb)];                  \
+  d2v = rs[nidx<CI, CJ, 1, -1>(a, bb)]; d3 = rs[nidx<CI, CJ, 1, 1>(a, bb)];
+          if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
+#undef DDH_NB
+          const float2 nA = make_float2(n0, n1), nB = make_float2(n2, n3);
+          const float2 dA = make_float2(d0, d1), dB = make_float2(d2v, d3);
+          const float2 wA = qgg_w2(ri, nA, A.r_h, A.r_g, A.r_k), wB = qgg_w2(ri, nB, A.r_h, A.r_g, A.r_k);
+          const float2 wC = qgg_w2(ri, dA, A.r_h, A.r_g, A.r_k), wD = qgg_w2(ri, dB, A.r_h, A.r_g, A.r_k);
+          const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+          const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+          Bv[k] = A.r_b6 * (bs.x + bs.y);
+          Sv[k] = A.r_b6 * (ss.x + ss.y);
+          Rv[k] = ri;
+          ix[k] = sidx(c, a, bb);
+          const int gi = (i0 - kHalo + 2 * a + ci) & (N - 1), gj = (j0 - kHalo + 2 * bb + cj) & (N - 1);
+          Rv[k] = r_update(ri, __ldg(qin + (size_t)gi * N + gj), Bv[k], Sv[k], A.r_min);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (ix[k] >= 0) rs[ix[k]] = Rv[k];
+      __syncthreads();
+    }
+  }
+  // core -> out (prior off: r = max(q, r_min); degenerate: unchanged)
+  for (int idx = tid; idx < T * T; idx += kSThreads) {
+    const int oi = idx / T, oj = idx - oi * T;
+    const int li = oi + kHalo, lj = oj + kHalo;
+    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + oj);
+    float v = rs[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)];
+    if (!A.r_prior && !degenerate) v = fmaxf(A.q[g], A.r_min);
+    A.icd_out[g] = v;
+    if (A.icd_copy) A.icd_copy[g] = v;
+  }
+}
+
+// phi M-step: one 4-colour sweep of the GMRF ICD (R10-R11) on a 64x64 tile
+// with a 4-pixel halo; free boundary: neighbours outside the frame are absent
+// (value 0 in the tile, excluded from sum b).  The first sweep of a time step
+// subtracts the RemoveTipTilt plane (from the S0 sums) on load.
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, P = N * N;
+  __shared__ float ps[4 * kSub * kSubP];
+  __shared__ double st[4];
+  const int tid = threadIdx.x, s = blockIdx.z;
+  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
+  const size_t off = (size_t)s * P;
+  const float *__restrict__ pin = A.icd_in + off;
+  if (tid < 32) {
+    double sums[5];
+    sum_part0(A.part0, A.nb0, s, sums);
+    const double d2 = sum_part1(A.part1, A.nb1, s);
+    if (tid == 0) {
+      double c[3] = {0, 0, 0};
+      if (A.apply_plane) plane_from_sums(sums, A.minv, c);
+      st[0] = c[0];
+      st[1] = c[1];
+      st[2] = c[2];
+      st[3] = d2;
+    }
+  }
+  __syncthreads();
+  const bool degenerate = !(st[3] > 0.0);
+  const float c0 = degenerate ? 0.f : (float)st[0], c1 = degenerate ? 0.f : (float)st[1],
+              c2 = degenerate ? 0.f : (float)st[2];
+  for (int idx = tid; idx < kReg * kReg; idx += kSThreads) {
+    const int li = idx / kReg, lj = idx - li * kReg;
+    const int gi = i0 - kHalo + li, gj = j0 - kHalo + lj;
+    float v = 0.f;
+    if (gi >= 0 && gi < N && gj >= 0 && gj < N)
+      v = pin[(size_t)gi * N + gj] - (c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2));
+    ps[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)] = v;
+  }
+  __syncthreads();
+  if (!degenerate) {
+    const bool prior = A.phi_prior != 0;
+    const float w = A.phi_w;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ci = c >> 1, cj = c & 1;
+      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(kReg - c - 1, ci);
+      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(kReg - c - 1, cj);
+      const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
+      constexpr int KMAX = (35 * 35 + kSThreads - 1) / kSThreads;
+      float Rv[KMAX];
+      int ix[KMAX];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const int p = tid + k * kSThreads;
+        ix[k] = -1;
+        if (p < cnt) {
+          const int a = alo + p / nbb, bb = blo + p % nbb;
+          const int gi = i0 - kHalo + 2 * a + ci, gj = j0 - kHalo + 2 * bb + cj;
+          if (gi < 0 || gi >= N || gj < 0 || gj >= N) continue;  // outside the frame: absent
+          float pi_, n4, nd;
+#define DDH_NB(CI, CJ)                                                                           \
+  pi_ = ps[sidx(2 * CI + CJ, a, bb)];                                                             \
+  n4 = (ps[nidx<CI, CJ, -1, 0>(a, bb)] + ps[nidx<CI, CJ, 1, 0>(a, bb)]) +                         \
+       (ps[nidx<CI, CJ, 0, -1>(a, bb)] + ps[nidx<CI, CJ, 0, 1>(a, bb)]);                          \
+  nd = (ps[nidx<CI, CJ, -1, -1>(a, bb)] + ps[nidx<CI, CJ, -1, 1>(a, bb)]) +                       \
+       (ps[nidx<CI, CJ, 1, -1>(a, bb)] + ps[nidx<CI, CJ, 1, 1>(a, bb)]);
+          if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
+#undef DDH_NB
+          const size_t g = off + (size_t)gi * N + gj;
+          const float cv = __ldg(A.cc + g), tv = __ldg(A.theta + g);
+          const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
+          const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
+          const float sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+                           (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
+          Rv[k] = phi_update(pi_, cv, tv, nb, sb, w, prior);
+          ix[k] = sidx(c, a, bb);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (ix[k] >= 0) ps[ix[k]] = Rv[k];
+      __syncthreads();
+    }
+  }
+  for (int idx = tid; idx < T * T; idx += kSThreads) {
+    const int oi = idx / T, oj = idx - oi * T;
+    const int li = oi + kHalo, lj = oj + kHalo;
+    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + oj);
+    const float v = degenerate ? pin[(size_t)(i0 + oi) * N + (j0 + oj)] : ps[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)];
+    A.icd_out[g] = v;
+    if (A.icd_copy) A.icd_copy[g] = v;
+  }
+}
+
+// ------------------------------------------------------------- launchers
+
+#define DDH_SDISPATCH(n, CALL)                          \
+  switch (n) {                                          \
+    case 64: { constexpr int N = 64; CALL; } break;     \
+    case 128: { constexpr int N = 128; CALL; } break;   \
+    case 256: { constexpr int N = 256; CALL; } break;   \
+    case 512: { constexpr int N = 512; CALL; } break;   \
+    case 1024: { constexpr int N = 1024; CALL; } break; \
+    default: return cudaErrorInvalidValue;              \
+  }
+
+template <int N> static size_t srow_smem() { return N * sizeof(float4) + (size_t)SCfg<N>::H * SCfg<N>::RPITCH * sizeof(float2); }
+template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t)N * SCfg<N>::W * sizeof(float2); }
+
+template <int N>
+static cudaError_t init_stream_n() {
+  cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
+  cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
+  cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
+  return cudaGetLastError();
+}
+
+cudaError_t init_stream(int n) { DDH_SDISPATCH(n, return init_stream_n<N>()); }
+int stream_nb1(int n) { DDH_SDISPATCH(n, return N / SCfg<N>::H); }
+int stream_nb0(int n) { return n * n / 2048 < 1 ? 1 : n * n / 2048; }
+
+cudaError_t launch_s0(const StepArgs &a, cudaStream_t st) {
+  ks_stats<<<dim3(a.nb0, a.sc), kSThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, (ks_rows_fwd<N><<<dim3(N / SCfg<N>::H, a.sc), SCfg<N>::NTR, srow_smem<N>(), st>>>(a)));
+  return cudaGetLastError();
+}
+cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, (ks_cols<N><<<dim3(N / SCfg<N>::W, a.sc), SCfg<N>::NTC, scol_smem<N>(), st>>>(a)));
+  return cudaGetLastError();
+}
+cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  ks_ricd<N><<<dim3(N / T, N / T, a.sc), kSThreads, 0, st>>>(a);
+                }));
+  return cudaGetLastError();
+}
+cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, (ks_rows_inv<N><<<dim3(N / SCfg<N>::H, a.sc), SCfg<N>::NTR, srow_smem<N>(), st>>>(a)));
+  return cudaGetLastError();
+}
+cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  ks_phiicd<N><<<dim3(N / T, N / T, a.sc), kSThreads, 0, st>>>(a);
+                }));
+  return cudaGetLastError();
+}
+
+}  // namespace ddh

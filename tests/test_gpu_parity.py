@@ -48,10 +48,13 @@ def oracle_params(n, diam=None, **kw):
     return p
 
 
+PATH_FLAGS = {"stream": 0, "cluster": 4, "multipass": 2, False: 0, True: 2}
+
+
 def gpu_kwargs(p: O.OracleParams, unfused=False):
     return dict(aperture_diam=p.aperture_diam, noise_var=p.noise_var, lam=p.lam, alpha=p.alpha, n_k=p.n_k, r_min=p.r_min, r_sigma=p.r_sigma,
                 r_T=p.r_T, r_q=p.r_q, phi_sigma=p.phi_sigma, icd_sweeps=p.icd_sweeps, boot_period=p.boot_period,
-                boot_alpha=p.boot_alpha, flags=(0 if p.tiptilt else 1) | (2 if unfused else 0))
+                boot_alpha=p.boot_alpha, flags=(0 if p.tiptilt else 1) | PATH_FLAGS[unfused])
 
 
 def tie_mask(gaps, thr=1e-6, rad=2):
@@ -206,7 +209,9 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, unfused=
     return worst
 
 
-PATHS = [pytest.param(False, id="fused"), pytest.param(True, id="unfused")]
+# the three implementations of the EM iteration: streaming (default), cluster-fused, multi-pass
+PATHS = [pytest.param("stream", id="stream"), pytest.param("cluster", id="cluster"),
+         pytest.param("multipass", id="multipass")]
 
 
 @pytest.mark.parametrize("unfused", PATHS)
@@ -431,7 +436,11 @@ def test_kernel_launch_count_and_empty_call():
     assert ctx.kernel_launches == l0
     y, _, _ = frames(n, S, 1)
     ctx.step(torch.from_numpy(y).to(DEV))
-    assert ctx.kernel_launches - l0 == 3  # fused: KA KB KC
+    assert ctx.kernel_launches - l0 == 6  # streaming: S0 S1 S2 S3 S4 S5
+    f = DDH(n, S, noise_var=0.1, flags=4)
+    l0 = f.kernel_launches
+    f.step(torch.from_numpy(y).to(DEV))
+    assert f.kernel_launches - l0 == 3  # cluster-fused: KA KB KC
     u = DDH(n, S, noise_var=0.1, flags=2)
     l0 = u.kernel_launches
     u.step(torch.from_numpy(y).to(DEV))
@@ -439,20 +448,21 @@ def test_kernel_launch_count_and_empty_call():
 
 
 def test_fused_and_unfused_paths_agree():
-    """The cluster-fused and the multi-pass kernels compute the same step (FP32
-    rounding order differs: compare at the parity tolerance, 3 frames)."""
+    """The streaming, cluster-fused and multi-pass kernels compute the same step
+    (FP32 rounding order differs: compare at the parity tolerance, 3 frames)."""
     n, S = 256, 2
     y, _, _ = frames(n, S, 3)
     yt = torch.from_numpy(y).to(DEV)
     outs = []
-    for flags in (0, 2):
+    for flags in (2, 0, 4):
         ctx = DDH(n, S, noise_var=0.2, flags=flags)
         po = torch.empty((3, S, n, n), device=DEV)
         ro = torch.empty_like(po)
         ctx.step(yt, po, ro)
         outs.append((po.cpu().numpy(), ro.cpu().numpy()))
     a = O.aperture(n, n)
-    for t in range(3):
-        for s in range(S):
-            assert phi_err(outs[0][0][t, s], outs[1][0][t, s].astype(np.float64), a) < 1e-3
-            assert np.linalg.norm(outs[0][1][t, s] - outs[1][1][t, s]) / np.linalg.norm(outs[1][1][t, s]) < 1e-3
+    for o in outs[1:]:
+        for t in range(3):
+            for s in range(S):
+                assert phi_err(o[0][t, s], outs[0][0][t, s].astype(np.float64), a) < 1e-3
+                assert np.linalg.norm(o[1][t, s] - outs[0][1][t, s]) / np.linalg.norm(outs[0][1][t, s]) < 1e-3

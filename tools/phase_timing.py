@@ -4,14 +4,15 @@ import os, subprocess, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 code = r'''
-import sys, torch, numpy as np
+import os, sys, torch, numpy as np
 sys.path.insert(0, "%s")
 import synth
 from paper_2305_03284_b200 import DDH
 cfg = synth.CONFIGS["c3"]
-y, _ = synth.make_batch(cfg, streams=64, frames=3, want_phi=False)
+S = int(os.environ.get("S", "64"))
+y, _ = synth.make_batch(cfg, streams=S, frames=3, want_phi=False)
 yd = torch.from_numpy(y).cuda()
-ctx = DDH(256, 64, noise_var=synth.recon_noise_var(256, 256, 5.0))
+ctx = DDH(256, S, noise_var=synth.recon_noise_var(256, 256, 5.0), lanes=int(os.environ.get("LANES", "1")))
 for t in range(3):
     ctx.step(yd[t:t+1]); torch.cuda.synchronize()
 ''' % ROOT
