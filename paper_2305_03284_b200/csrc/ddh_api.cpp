@@ -42,6 +42,7 @@ struct ddh_ctx {
   float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
   double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
   bool fused = false;
+  bool mega = false;  // fused path as one persistent launch per EM iteration
   int cs = 0;  // CTAs per stream of the fused path
   bool streaming = false;  // cluster-free 6-kernel path (ddh_stream.cu)
   float4 *tw4 = nullptr;
@@ -95,11 +96,12 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
   } while (0)
 
 enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
-            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5 };
+            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
                                           "kf_rows_fwd", "kf_cols", "kf_rows_inv",
-                                          "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd"};
+                                          "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd",
+                                          "kf_mega"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
@@ -379,9 +381,13 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           b.r_copy = (last && r_out) ? r_out + go : nullptr;
           b.phi_copy = (last && phi_out) ? phi_out + go : nullptr;
-          DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
-          DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
-          DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
+          if (c->mega) {
+            DDH_LAUNCH_ON(c, K_KM, st, ddh::launch_km(b, st));
+          } else {
+            DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
+            DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
+            DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
+          }
           cl ^= 1;
         }
       }
@@ -620,8 +626,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const std::string path = pe ? pe : "";
     if (path == "multipass" || (path.empty() && (p.flags & DDH_F_UNFUSED))) {
       c->fused = c->streaming = false;
-    } else if (path == "cluster" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
+    } else if (path == "cluster3") {
       c->fused = ddh::fused_supported(n);
+    } else if (path == "cluster" || path == "mega" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
+      c->fused = ddh::fused_supported(n);
+      c->mega = c->fused;
     } else {
       c->streaming = true;
     }
@@ -630,7 +639,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (c->streaming || ddh::fused_supported(n)) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = ev ? std::atoi(ev) : p.lanes;
-    if (c->lanes <= 0) c->lanes = std::min(4, std::max(1, c->sc / 16));
+    if (c->lanes <= 0) c->lanes = c->mega ? 1 : std::min(4, std::max(1, c->sc / 16));
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));

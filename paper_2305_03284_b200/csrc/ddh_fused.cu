@@ -86,10 +86,15 @@ template <int N> __host__ __device__ constexpr size_t kc_smem() {
   return (size_t)C::H * (N + 1) * sizeof(float2) + (size_t)(C::H + 2) * (N + 8) * sizeof(float) + (size_t)N * sizeof(float2);
 }
 
+template <int N> __host__ __device__ constexpr size_t km_smem() {
+  return ka_smem<N>() > kb_smem<N>() ? (ka_smem<N>() > kc_smem<N>() ? ka_smem<N>() : kc_smem<N>())
+                                     : (kb_smem<N>() > kc_smem<N>() ? kb_smem<N>() : kc_smem<N>());
+}
+
 // ------------------------------------------------------------------- KA
 
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fwd(StepArgs A) {
+__device__ __forceinline__ void phase_a(const StepArgs &A, const int s) {
   using C = FusedCfg<N>;
   constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
   cg::cluster_group cl = cg::this_cluster();
@@ -101,10 +106,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   __shared__ double part[5];
   __shared__ double tot[5];
   const int tid = threadIdx.x;
-  const int s = blockIdx.y;
   const int i0 = rank * H;
   DDH_T0();
   const size_t off = (size_t)s * P;
+  __syncthreads();  // previous phase's shared-memory reads are done
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
   float ph[EPT];
   double v[5] = {0, 0, 0, 0, 0};
@@ -189,6 +194,11 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
   DDH_TPRINT("KA");
 }
 
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fwd(StepArgs A) {
+  phase_a<N>(A, blockIdx.y);
+}
+
 // ------------------------------------------------------------------- KB
 
 // Column slab of W columns x N rows.  Order: column DFT -> Eq. 3 + E-step
@@ -196,7 +206,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fw
 // updates exactly the pixels whose q it holds) -> write r -> inverse column
 // DFT of the tile -> write the spectrum slab.
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(StepArgs A) {
+__device__ __forceinline__ void phase_b(const StepArgs &A, const int s, const int s_next) {
   using C = FusedCfg<N>;
   constexpr int W = C::W, NT = C::NT, CS = C::CS, EPT = C::EPT, RP = C::RP, P = N * N;
   cg::cluster_group cl = cg::this_cluster();
@@ -210,11 +220,10 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   __shared__ double st[1];
   const int tid = threadIdx.x;
   const int c0 = rank * W;
+  __syncthreads();  // previous phase's shared-memory reads are done
   for (int k = tid; k < N; k += NT) tw[k] = A.tw[k];
-  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {  // persistent: one stream per iteration
-  __syncthreads();  // previous iteration's shared-memory reads are done
   {
-    const int sn = s + gridDim.y;  // next stream of this cluster: pull its inputs into L2 now
+    const int sn = s_next;  // next stream of this cluster: pull its inputs into L2 now
     if (sn < A.sc) {
       for (int i = tid; i < N; i += NT) {
         asm volatile("prefetch.global.L2 [%0];" ::"l"(A.cbuf + (size_t)sn * P + (size_t)i * N + c0));
@@ -372,13 +381,18 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(St
   DDH_TS();  // 8: final cluster barrier
   DDH_TPRINT("KB");
   DDH_SYNC_PRINT("KBsync");
-  }  // stream loop
+}
+
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(StepArgs A) {
+  for (int s = blockIdx.y; s < A.sc; s += gridDim.y)  // persistent: one stream per iteration
+    phase_b<N>(A, s, s + gridDim.y);
 }
 
 // ------------------------------------------------------------------- KC
 
 template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_inv(StepArgs A) {
+__device__ __forceinline__ void phase_c(const StepArgs &A, const int s) {
   using C = FusedCfg<N>;
   constexpr int H = C::H, NT = C::NT, CS = C::CS, EPT = C::EPT, PITCH = N + 1, P = N * N;
   cg::cluster_group cl = cg::this_cluster();
@@ -392,7 +406,7 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   float2 *tw = reinterpret_cast<float2 *>(phS + (H + 2) * PP);
   __shared__ double st[6];
   const int tid = threadIdx.x;
-  const int s = blockIdx.y;
+  __syncthreads();  // previous phase's shared-memory reads are done
   const int i0 = rank * H;
   DDH_T0();
   const size_t off = (size_t)s * P;
@@ -563,6 +577,33 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   DDH_SYNC_PRINT("KCsync");
 }
 
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_inv(StepArgs A) {
+  phase_c<N>(A, blockIdx.y);
+}
+
+// ------------------------------------------------------------- megakernel
+//
+// The whole EM iteration of a stream in one persistent cluster: phase A (rows),
+// cluster barrier, phase B (columns + r-ICD), cluster barrier, phase C (rows +
+// phi-ICD); then the next stream of this cluster.  The spectrum crosses
+// between phases through this stream's own cbuf slice (L2); the cluster
+// barrier (arrive.release / wait.acquire at cluster scope) orders those global
+// writes and reads.  One launch per EM iteration instead of three: no launch
+// ramps and tails between the phases, and the clusters drift out of phase so
+// the MUFU-bound r-ICD of one overlaps the FFTs of another.
+template <int N>
+__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_mega(StepArgs A) {
+  cg::cluster_group cl = cg::this_cluster();
+  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {
+    phase_a<N>(A, s);
+    cl.sync();  // cbuf rows of stream s (all CTAs) visible
+    phase_b<N>(A, s, s + gridDim.y);
+    cl.sync();  // cbuf columns of stream s visible
+    phase_c<N>(A, s);
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 template <typename... KArgs, typename... Args>
@@ -591,7 +632,9 @@ static cudaError_t init_fused_n() {
   cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ka_smem<N>());
   cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kb_smem<N>());
   cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kc_smem<N>());
+  cudaFuncSetAttribute(kf_mega<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)km_smem<N>());
   if (FusedCfg<N>::CS > 8) {
+    cudaFuncSetAttribute(kf_mega<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -613,7 +656,7 @@ cudaError_t init_fused(int n) { DDH_FDISPATCH(n, return init_fused_n<N>()); }
 
 // Persistent grids: as many clusters as can be co-resident (queried once per
 // kernel with cudaOccupancyMaxActiveClusters), each looping over streams.
-static int g_max_clusters[3][11];  // [kernel][log2 N]
+static int g_max_clusters[4][11];  // [kernel][log2 N]
 
 template <typename... KArgs>
 static int max_clusters(void (*kernel)(KArgs...), int cs, int nt, size_t smem) {
@@ -645,6 +688,7 @@ static void init_grids() {
   g_max_clusters[0][l] = 1 << 20;
   g_max_clusters[1][l] = max_clusters(kf_cols<N>, C::CS, C::NT, kb_smem<N>());
   g_max_clusters[2][l] = 1 << 20;
+  g_max_clusters[3][l] = max_clusters(kf_mega<N>, C::CS, C::NT, km_smem<N>());
 }
 
 static inline int grid_y(int which, int n, int sc) {
@@ -659,6 +703,10 @@ cudaError_t launch_ka(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st) {
   DDH_FDISPATCH(a.n, return launch_cluster(kf_cols<N>, dim3(FusedCfg<N>::CS, grid_y(1, N, a.sc)),
                                            dim3(FusedCfg<N>::NT), kb_smem<N>(), FusedCfg<N>::CS, st, a));
+}
+cudaError_t launch_km(const StepArgs &a, cudaStream_t st) {
+  DDH_FDISPATCH(a.n, return launch_cluster(kf_mega<N>, dim3(FusedCfg<N>::CS, grid_y(3, N, a.sc)),
+                                           dim3(FusedCfg<N>::NT), km_smem<N>(), FusedCfg<N>::CS, st, a));
 }
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st) {
   DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_inv<N>, dim3(FusedCfg<N>::CS, grid_y(2, N, a.sc)),

@@ -115,6 +115,7 @@ cudaError_t init_fused(int n);
 cudaError_t launch_ka(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_km(const StepArgs &a, cudaStream_t st);  // KA+KB+KC in one persistent launch
 
 // streaming (cluster-free) EM iteration, ddh_stream.cu: S0 stats, S1 rows,
 // S2 cols + E-step, S3 r-ICD tiles, S4 inverse rows + c/theta, S5 phi-ICD tiles

@@ -49,6 +49,30 @@ __device__ __forceinline__ void sincos_red(float p, float &sn, float &cs) {
   __sincosf(fmaf(-6.283185307179586f, rintf(p * 0.15915494309189535f), p), &sn, &cs);
 }
 
+// atan2(y, x) for the phase-correlation angle: octant reduction + odd
+// minimax polynomial (degree 13) of atan on [0, 1]; |error| < 5e-7 rad
+// (FP32, measured against FP64 atan).  atan2(0, 0) = 0 (c = 0 there, so
+// theta is irrelevant).
+__device__ __forceinline__ float atan2_fast(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  const float a = mx > 0.f ? mn * rcp_approx(mx) : 0.f;
+  const float s = a * a;
+  float p = 0.00681176f;
+  p = fmaf(p, s, -0.03360414f);
+  p = fmaf(p, s, 0.07962359f);
+  p = fmaf(p, s, -0.1323334f);
+  p = fmaf(p, s, 0.19807816f);
+  p = fmaf(p, s, -0.3331737f);
+  p = fmaf(p, s, 0.9999961f);
+  float r = p * a;
+  if (ay > ax) r = 1.5707963267948966f - r;
+  if (x < 0.f) r = 3.141592653589793f - r;
+  return copysignf(r, y);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // Warp 0: per-stream totals of the S0 partials (fixed order) -> out[0..4]
 __device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int nb0, int s, double *out) {
   const int lane = threadIdx.x & 31;
@@ -80,7 +104,10 @@ __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g
 // ------------------------------------------------------------------ S0
 
 // grid (nb0, sc), block 256: block b sums pixels [b P/nb0, (b+1) P/nb0) of
-// stream s, 8 consecutive pixels per thread and iteration (16-byte loads).
+// stream s in chunks of 8 consecutive pixels (16-byte loads).  y: each
+// chunk is summed as a balanced FP32 tree (exact for a constant frame, so the
+// degenerate test ||y - mu|| = 0 of R31 stays exact) and accumulated in FP64;
+// phi plane sums: FP32 per-thread partials; FP64 block sums.
 __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
   __shared__ double red[32 * 5];
   const int n = A.n, lg = 31 - __clz(n);
@@ -89,52 +116,50 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
   const size_t per = P / A.nb0;
   const size_t base = blockIdx.x * per;
   const size_t off = (size_t)s * P;
-  double v[5] = {0, 0, 0, 0, 0};
+  float v[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  double yr = 0.0, yi = 0.0;
   for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
-    const float4 *y4 = reinterpret_cast<const float4 *>(A.y + off + p0);
-    float sr = 0.f, si = 0.f;
     if (A.want_y) {
+      const float4 *y4 = reinterpret_cast<const float4 *>(A.y + off + p0);
       float4 a[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) a[k] = __ldg(y4 + k);  // kept in L2 for S1
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        sr += a[k].x + a[k].z;
-        si += a[k].y + a[k].w;
-      }
+      yr += (double)(((a[0].x + a[0].z) + (a[1].x + a[1].z)) + ((a[2].x + a[2].z) + (a[3].x + a[3].z)));
+      yi += (double)(((a[0].y + a[0].w) + (a[1].y + a[1].w)) + ((a[2].y + a[2].w) + (a[3].y + a[3].w)));
     }
-    v[0] += (double)sr;
-    v[1] += (double)si;
     if (A.apply_plane) {
       const int i = (int)(p0 >> lg), j0 = (int)(p0 & (n - 1));
       const int2 sp = __ldg(A.rowspan + i);
-      const float4 *f4 = reinterpret_cast<const float4 *>(A.phi_in + off + p0);
-      const float4 f0 = f4[0], f1 = f4[1];
-      const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-      float s0 = 0.f, sx = 0.f;
+      if (j0 + 8 > sp.x && j0 < sp.y) {
+        const float4 *f4 = reinterpret_cast<const float4 *>(A.phi_in + off + p0);
+        const float4 f0 = __ldg(f4), f1 = __ldg(f4 + 1);
+        const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        float s0 = 0.f, sx = 0.f;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int j = j0 + k;
-        const float fk = (j >= sp.x && j < sp.y) ? f[k] : 0.f;
-        s0 += fk;
-        sx = fmaf(fk, (float)(j - n / 2), sx);
+        for (int k = 0; k < 8; ++k) {
+          const int j = j0 + k;
+          const float fk = (j >= sp.x && j < sp.y) ? f[k] : 0.f;
+          s0 += fk;
+          sx = fmaf(fk, (float)(j - n / 2), sx);
+        }
+        v[2] += s0;
+        v[3] += sx;
+        v[4] = fmaf(s0, (float)(i - n / 2), v[4]);
       }
-      v[2] += (double)s0;
-      v[3] += (double)sx;
-      v[4] += (double)s0 * (double)(i - n / 2);
     }
   }
-  block_sum<5>(v, red);
+  double d[5] = {yr, yi, (double)v[2], (double)v[3], (double)v[4]};
+  block_sum<5>(d, red);
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int k = 0; k < 5; ++k) A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + k] = v[k];
+    for (int k = 0; k < 5; ++k) A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + k] = d[k];
   }
 }
 
 // ------------------------------------------------------------------ S1
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
+__global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
   using C = SCfg<N>;
   constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
   extern __shared__ float4 smem4[];
@@ -149,11 +174,11 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
   const size_t row = off + (size_t)i * N;
   // issue the loads first (y: 8 B, phi: 4 B per pixel, comb t + TPV e)
   float2 v[E];
-  float ph[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.y[row + t + TPV * e];
-#pragma unroll
-  for (int e = 0; e < E; ++e) ph[e] = A.phi_in[row + t + TPV * e];
+  if (t == 0) {  // phi row -> L2 (read after the stats)
+    for (int k = 0; k < N * 4; k += 128) prefetch_l2(reinterpret_cast<const char *>(A.phi_in + row) + k);
+  }
   load_tw<N>(tw, A.tw4, tid, NT);
   if (tid < 32) {
     double sums[5];
@@ -182,7 +207,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
     float2 z = make_float2(0.f, 0.f);
     if (j >= sp.x && j < sp.y) {
       float sn, cs;
-      sincos_red(ph[e] - fmaf(c1, (float)(j - N / 2), pyi), sn, cs);
+      sincos_red(A.phi_in[row + j] - fmaf(c1, (float)(j - N / 2), pyi), sn, cs);
       // (y - mu) e^{-j phi'} = d (cs - i sn), times chi = (-1)^(i+j)
       const float sg = ((i + j) & 1) ? -1.f : 1.f;
       z = p_fma(bc2(d.x * sg), make_float2(cs, -sn), p_mul(bc2(d.y * sg), make_float2(sn, cs)));
@@ -200,7 +225,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_fwd(StepArgs A) {
 // ------------------------------------------------------------------ S2
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTC) ks_cols(StepArgs A) {
+__global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(StepArgs A) {
   using C = SCfg<N>;
   constexpr int E = C::E, TPV = C::TPV, W = C::W, NT = C::NTC, P = N * N;
   extern __shared__ float4 smem4[];
@@ -214,9 +239,10 @@ __global__ void __launch_bounds__(SCfg<N>::NTC) ks_cols(StepArgs A) {
   float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.cbuf[off + (size_t)(t + TPV * e) * N + col];
-  float rp[E];
+  if (b == 0) {  // r_prev of this column slab -> L2 (read in the E-step)
 #pragma unroll
-  for (int e = 0; e < E; ++e) rp[e] = A.r_state[off + (size_t)(t + TPV * out_comb<N>(e)) * N + col];
+    for (int e = 0; e < E; ++e) prefetch_l2(A.r_state + off + (size_t)(t + TPV * e) * N + blockIdx.x * W);
+  }
   load_tw<N>(tw, A.tw4, tid, NT);
   if (tid < 32) {
     const double d2 = sum_part1(A.part1, A.nb1, s);
@@ -237,7 +263,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC) ks_cols(StepArgs A) {
     const size_t g = off + (size_t)ki * N + col;
     const float sg = ((ki + col) & 1) ? -scale : scale;
     const float2 u = p_mul(v[e], bc2(sg));
-    float r0 = rp[e];
+    float r0 = A.r_state[g];
     if (warm) r0 = fmaxf(fmaf(A.oml, r0, A.la * fmaf(u.x, u.x, u.y * u.y)), A.r_min);  // Eq. 3
     const float w = r0 * rcp_approx(r0 + A.s2);                                        // E-step (R1)
     const float2 mu = p_mul(u, bc2(w));
@@ -256,7 +282,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC) ks_cols(StepArgs A) {
 // ------------------------------------------------------------------ S4
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
+__global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
   using C = SCfg<N>;
   constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
   extern __shared__ float4 smem4[];
@@ -267,11 +293,12 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
   const int t = tid % TPV, b = tid / TPV;
   const int i = blockIdx.x * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
-  float2 v[E], yv[E];
+  float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.cbuf[row + t + TPV * e];
-#pragma unroll
-  for (int e = 0; e < E; ++e) yv[e] = A.y[row + t + TPV * out_comb<N>(e)];
+  if (t == 0) {  // y row -> L2 (read in the epilogue)
+    for (int k = 0; k < N * 8; k += 128) prefetch_l2(reinterpret_cast<const char *>(A.y + row) + k);
+  }
   load_tw<N>(tw, A.tw4, tid, NT);
   if (tid < 32) {
     double sums[5];
@@ -298,11 +325,11 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
     float c = 0.f, th = 0.f;
     if (j >= sp.x && j < sp.y) {
       const float sg = ((i + j) & 1) ? -kn : kn;
-      const float2 yh = p_mul(p_sub(yv[e], make_float2(mur, mui)), bc2(sg));
+      const float2 yh = p_mul(p_sub(A.y[row + j], make_float2(mur, mui)), bc2(sg));
       const float2 g = v[e];
       const float2 z = p_fma(bc2(yh.x), g, p_mul(bc2(yh.y), make_float2(-g.y, g.x)));  // yh * g
       c = two_s2 * sqrt_approx(fmaf(z.x, z.x, z.y * z.y) + 1e-37f);
-      th = atan2f(z.y, z.x);
+      th = atan2_fast(z.y, z.x);
     }
     A.cc[row + j] = c;
     A.theta[row + j] = th;
@@ -313,6 +340,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
 
 namespace {
 constexpr int kTile = 64, kHalo = 4, kReg = kTile + 2 * kHalo, kSub = kReg / 2, kSubP = kSub + 1;
+constexpr int kIcdGrid = 4 * kSub * kSubP;  // floats per colour-separated tile
 // colour-separated tile: sub-grid c = 2 (i&1) + (j&1), element (i>>1, j>>1)
 __device__ __forceinline__ int sidx(int c, int a, int b) { return (c * kSub + a) * kSubP + b; }
 // neighbour (di, dj) of a pixel of colour (ci, cj) at sub coords (a, b):
@@ -338,7 +366,8 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 template <int N>
 __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
-  __shared__ float rs[4 * kSub * kSubP];
+  extern __shared__ float icd_sm[];
+  float *rs = icd_sm, *qs = icd_sm + 4 * kSub * kSubP;
   __shared__ double st[1];
   const int tid = threadIdx.x, s = blockIdx.z;
   const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
@@ -349,10 +378,16 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
     const double d2 = sum_part1(A.part1, A.nb1, s);
     if (tid == 0) st[0] = d2;
   }
-  for (int idx = tid; idx < kReg * kReg; idx += kSThreads) {
-    const int li = idx / kReg, lj = idx - li * kReg;
-    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + lj) & (N - 1);
-    rs[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)] = rin[(size_t)gi * N + gj];
+  // region rows x column pairs (8-byte loads; pairs never straddle the wrap)
+  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
+    const int li = idx / kSub, pj = idx - li * kSub;
+    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
+    const float2 v = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
+    const float2 qv = *reinterpret_cast<const float2 *>(qin + (size_t)gi * N + gj);
+    rs[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
+    rs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
+    qs[sidx(2 * (li & 1), li >> 1, pj)] = qv.x;
+    qs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = qv.y;
   }
   __syncthreads();
   const bool degenerate = !(st[0] > 0.0);
@@ -392,8 +427,7 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
           Sv[k] = A.r_b6 * (ss.x + ss.y);
           Rv[k] = ri;
           ix[k] = sidx(c, a, bb);
-          const int gi = (i0 - kHalo + 2 * a + ci) & (N - 1), gj = (j0 - kHalo + 2 * bb + cj) & (N - 1);
-          Rv[k] = r_update(ri, __ldg(qin + (size_t)gi * N + gj), Bv[k], Sv[k], A.r_min);
+          Rv[k] = r_update(ri, qs[ix[k]], Bv[k], Sv[k], A.r_min);
         }
       }
 #pragma unroll
@@ -403,14 +437,17 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
     }
   }
   // core -> out (prior off: r = max(q, r_min); degenerate: unchanged)
-  for (int idx = tid; idx < T * T; idx += kSThreads) {
-    const int oi = idx / T, oj = idx - oi * T;
-    const int li = oi + kHalo, lj = oj + kHalo;
-    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + oj);
-    float v = rs[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)];
-    if (!A.r_prior && !degenerate) v = fmaxf(A.q[g], A.r_min);
-    A.icd_out[g] = v;
-    if (A.icd_copy) A.icd_copy[g] = v;
+  for (int idx = tid; idx < T * (T / 2); idx += kSThreads) {
+    const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
+    const int li = oi + kHalo;
+    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
+    float2 v = make_float2(rs[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)], rs[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
+    if (!A.r_prior && !degenerate) {
+      const float2 qv = *reinterpret_cast<const float2 *>(A.q + g);
+      v = make_float2(fmaxf(qv.x, A.r_min), fmaxf(qv.y, A.r_min));
+    }
+    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
+    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
   }
 }
 
@@ -421,7 +458,8 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
 template <int N>
 __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
-  __shared__ float ps[4 * kSub * kSubP];
+  extern __shared__ float icd_sm[];
+  float *ps = icd_sm;
   __shared__ double st[4];
   const int tid = threadIdx.x, s = blockIdx.z;
   const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
@@ -444,18 +482,23 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   const bool degenerate = !(st[3] > 0.0);
   const float c0 = degenerate ? 0.f : (float)st[0], c1 = degenerate ? 0.f : (float)st[1],
               c2 = degenerate ? 0.f : (float)st[2];
-  for (int idx = tid; idx < kReg * kReg; idx += kSThreads) {
-    const int li = idx / kReg, lj = idx - li * kReg;
-    const int gi = i0 - kHalo + li, gj = j0 - kHalo + lj;
-    float v = 0.f;
-    if (gi >= 0 && gi < N && gj >= 0 && gj < N)
-      v = pin[(size_t)gi * N + gj] - (c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2));
-    ps[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)] = v;
+  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
+    const int li = idx / kSub, pj = idx - li * kSub;
+    const int gi = i0 - kHalo + li, gj = j0 - kHalo + 2 * pj;
+    float2 v = make_float2(0.f, 0.f);
+    if (gi >= 0 && gi < N && gj >= 0 && gj < N) {  // pairs are both inside or both outside
+      const float2 f = *reinterpret_cast<const float2 *>(pin + (size_t)gi * N + gj);
+      const float pl = c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2);
+      v = make_float2(f.x - pl, f.y - (pl + c1));
+    }
+    ps[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
+    ps[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
   }
   __syncthreads();
   if (!degenerate) {
     const bool prior = A.phi_prior != 0;
     const float w = A.phi_w;
+    const bool edge = i0 == 0 || j0 == 0 || i0 + T == N || j0 + T == N;  // tile touches the frame edge
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int ci = c >> 1, cj = c & 1;
@@ -482,14 +525,18 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
        (ps[nidx<CI, CJ, 1, -1>(a, bb)] + ps[nidx<CI, CJ, 1, 1>(a, bb)]);
           if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
 #undef DDH_NB
+          const int me = sidx(c, a, bb);
           const size_t g = off + (size_t)gi * N + gj;
           const float cv = __ldg(A.cc + g), tv = __ldg(A.theta + g);
           const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
-          const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
-          const float sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
-                           (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
+          float sb = 1.f;  // sum of b over the existing neighbours
+          if (edge) {
+            const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
+            sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+                 (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
+          }
           Rv[k] = phi_update(pi_, cv, tv, nb, sb, w, prior);
-          ix[k] = sidx(c, a, bb);
+          ix[k] = me;
         }
       }
 #pragma unroll
@@ -498,13 +545,15 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
       __syncthreads();
     }
   }
-  for (int idx = tid; idx < T * T; idx += kSThreads) {
-    const int oi = idx / T, oj = idx - oi * T;
-    const int li = oi + kHalo, lj = oj + kHalo;
-    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + oj);
-    const float v = degenerate ? pin[(size_t)(i0 + oi) * N + (j0 + oj)] : ps[sidx(2 * (li & 1) + (lj & 1), li >> 1, lj >> 1)];
-    A.icd_out[g] = v;
-    if (A.icd_copy) A.icd_copy[g] = v;
+  for (int idx = tid; idx < T * (T / 2); idx += kSThreads) {
+    const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
+    const int li = oi + kHalo;
+    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
+    const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
+                                : make_float2(ps[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
+                                              ps[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
+    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
+    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
   }
 }
 
@@ -528,12 +577,14 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
+  cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
   return cudaGetLastError();
 }
 
 cudaError_t init_stream(int n) { DDH_SDISPATCH(n, return init_stream_n<N>()); }
 int stream_nb1(int n) { DDH_SDISPATCH(n, return N / SCfg<N>::H); }
-int stream_nb0(int n) { return n * n / 2048 < 1 ? 1 : n * n / 2048; }
+int stream_nb0(int n) { return n * n / 8192 < 1 ? 1 : n * n / 8192; }
 
 cudaError_t launch_s0(const StepArgs &a, cudaStream_t st) {
   ks_stats<<<dim3(a.nb0, a.sc), kSThreads, 0, st>>>(a);
@@ -550,7 +601,7 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
                   constexpr int T = N < kTile ? N : kTile;
-                  ks_ricd<N><<<dim3(N / T, N / T, a.sc), kSThreads, 0, st>>>(a);
+                  ks_ricd<N><<<dim3(N / T, N / T, a.sc), kSThreads, 2 * kIcdGrid * sizeof(float), st>>>(a);
                 }));
   return cudaGetLastError();
 }
@@ -561,7 +612,7 @@ cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
                   constexpr int T = N < kTile ? N : kTile;
-                  ks_phiicd<N><<<dim3(N / T, N / T, a.sc), kSThreads, 0, st>>>(a);
+                  ks_phiicd<N><<<dim3(N / T, N / T, a.sc), kSThreads, kIcdGrid * sizeof(float), st>>>(a);
                 }));
   return cudaGetLastError();
 }

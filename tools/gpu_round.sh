@@ -22,8 +22,8 @@ print({k: (round(v["ms_total"] / d["steps"] * 1000, 1), round(v.get("gbs", 0))) 
 PY
       ;;
     ncu)
-      CMD="python bench.py --steps 5 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity"
-      $CMD > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kf_|k[0-3]" -s 9 -c 3 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+      CMD="python bench.py --steps 5 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity ${BENCH_EXTRA:-}"
+      $CMD > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ks_|kf_" -s 12 -c 6 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
       echo "ncu rc=$?"; tail -2 gpurun_out/ncu_full.log ;;
     launches)
       CMD="python bench.py --steps 20 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity"
