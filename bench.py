@@ -358,7 +358,8 @@ def ctx_lanes(ctx):
     env = os.environ.get("DDH_LANES")
     L = int(env) if env else ctx.params.lanes
     if L <= 0:
-        L = min(4, max(1, ctx_chunk(ctx) // 16))
+        flags = ctx.params.flags
+        L = min(4, max(1, ctx_chunk(ctx) // 16)) if flags & 4 else min(2, max(1, ctx_chunk(ctx) // 32))
     return max(1, min(8, L))
 
 

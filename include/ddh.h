@@ -85,7 +85,8 @@ typedef struct {
   int32_t lanes;        /* fused path: concurrent sub-groups of a launch group, each on its
                            own CUDA stream forked from / joined to the ctx stream, so the
                            kernels of different sub-groups share the SMs; 1..8, 0 = auto
-                           (streams/16 clamped to [1,4]).  Results do not depend on it.   */
+                           (streaming path: streams/32 in [1,2]; cluster path: streams/16
+                           in [1,4]).  Results do not depend on it.                      */
 } ddh_params;
 
 /* Defaults: N=256, S=1, device 0, D=N, sigma^2=0.1, lambda=0.45, alpha=0.025,

@@ -62,6 +62,11 @@ struct ddh_ctx {
   int lanes = 1;
   cudaStream_t lane_st[8] = {};
   cudaEvent_t lane_ev[9] = {};
+  // streaming path: the r M-step (S3) of a lane runs on a side stream,
+  // concurrently with the phi branch (S4, S5) it does not depend on (R12)
+  bool split_r = false;
+  cudaStream_t side_st[8] = {};
+  cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // instrumentation
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -316,11 +321,17 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
+          cudaStream_t rst = st;
+          if (c->split_r) {  // fork: S3 after S2, beside S4/S5
+            rst = c->side_st[l];
+            DDH_CK(c, cudaEventRecord(c->side_fork[l], st));
+            DDH_CK(c, cudaStreamWaitEvent(rst, c->side_fork[l], 0));
+          }
           for (int k = 0; k < sw; ++k) {  // r M-step sweeps
             b.icd_in = k == 0 ? c->rinit + wo : c->rtmp[(k - 1) & 1] + wo;
             b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S3, st, ddh::launch_s3(b, st));
+            DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
           }
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
           const int plane_it = b.apply_plane;
@@ -330,6 +341,10 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
             b.apply_plane = k == 0 ? plane_it : 0;
             DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+          }
+          if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
+            DDH_CK(c, cudaEventRecord(c->side_join[l], rst));
+            DDH_CK(c, cudaStreamWaitEvent(st, c->side_join[l], 0));
           }
           cl ^= 1;
         }
@@ -454,6 +469,11 @@ void free_ctx(ddh_ctx *c) {
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : c->lane_st)
     if (s) cudaStreamDestroy(s);
+  for (int l = 0; l < 8; ++l) {
+    if (c->side_st[l]) cudaStreamDestroy(c->side_st[l]);
+    if (c->side_fork[l]) cudaEventDestroy(c->side_fork[l]);
+    if (c->side_join[l]) cudaEventDestroy(c->side_join[l]);
+  }
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
                   c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
@@ -639,11 +659,21 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (c->streaming || ddh::fused_supported(n)) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = ev ? std::atoi(ev) : p.lanes;
-    if (c->lanes <= 0) c->lanes = c->mega ? 1 : std::min(4, std::max(1, c->sc / 16));
+    if (c->lanes <= 0)  // measured at 256^2 x 64 streams: stream path 2, cluster path 4
+      c->lanes = c->mega ? 1 : c->streaming ? std::min(2, std::max(1, c->sc / 32)) : std::min(4, std::max(1, c->sc / 16));
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
+    }
+    const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
+    c->split_r = c->streaming && (sr ? std::atoi(sr) != 0 : true);
+    if (c->split_r) {
+      for (int l = 0; l < c->lanes; ++l) {
+        A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));
+        A(cudaEventCreateWithFlags(&c->side_fork[l], cudaEventDisableTiming));
+        A(cudaEventCreateWithFlags(&c->side_join[l], cudaEventDisableTiming));
+      }
     }
   }
   if (c->fused) {

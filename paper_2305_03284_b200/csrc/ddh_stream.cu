@@ -73,7 +73,8 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
-// Warp 0: per-stream totals of the S0 partials (fixed order) -> out[0..4]
+// Per warp (no barrier): per-stream totals of the S0 partials, fixed order,
+// identical in every warp and lane -> out[0..4]
 __device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int nb0, int s, double *out) {
   const int lane = threadIdx.x & 31;
   double v[5] = {0, 0, 0, 0, 0};
@@ -82,10 +83,7 @@ __device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int 
     for (int k = 0; k < 5; ++k) v[k] += part0[((size_t)s * nb0 + b) * 5 + k];
   }
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    v[k] = warp_sum(v[k]);
-    if (lane == 0) out[k] = v[k];
-  }
+  for (int k = 0; k < 5; ++k) out[k] = warp_sum(v[k]);  // xor tree: every lane holds the totals
 }
 __device__ __forceinline__ double sum_part1(const double *__restrict__ part1, int nb1, int s) {
   const int lane = threadIdx.x & 31;
@@ -165,7 +163,6 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
   extern __shared__ float4 smem4[];
   float4 *tw = smem4;                                             // [N]
   float2 *buf = reinterpret_cast<float2 *>(smem4 + N);            // [H][RPITCH]
-  __shared__ double st[5];
   __shared__ double red[32];
   const int tid = threadIdx.x, s = blockIdx.y;
   const int t = tid % TPV, b = tid / TPV;
@@ -180,22 +177,11 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
     for (int k = 0; k < N * 4; k += 128) prefetch_l2(reinterpret_cast<const char *>(A.phi_in + row) + k);
   }
   load_tw<N>(tw, A.tw4, tid, NT);
-  if (tid < 32) {
-    double sums[5];
-    sum_part0(A.part0, A.nb0, s, sums);
-    if (tid == 0) {
-      st[0] = sums[0] / P;
-      st[1] = sums[1] / P;
-      double c[3] = {0, 0, 0};
-      if (A.apply_plane) plane_from_sums(sums, A.minv, c);
-      st[2] = c[0];
-      st[3] = c[1];
-      st[4] = c[2];
-    }
-  }
-  __syncthreads();
-  const float mur = (float)st[0], mui = (float)st[1];
-  const float c0 = (float)st[2], c1 = (float)st[3], c2 = (float)st[4];
+  double sums[5], cpl[3] = {0, 0, 0};
+  sum_part0(A.part0, A.nb0, s, sums);
+  if (A.apply_plane) plane_from_sums(sums, A.minv, cpl);
+  const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
+  const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
   const int2 sp = __ldg(A.rowspan + i);
   const float pyi = fmaf(c2, (float)(i - N / 2), c0);
   float acc = 0.f;
@@ -244,12 +230,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
     for (int e = 0; e < E; ++e) prefetch_l2(A.r_state + off + (size_t)(t + TPV * e) * N + blockIdx.x * W);
   }
   load_tw<N>(tw, A.tw4, tid, NT);
-  if (tid < 32) {
-    const double d2 = sum_part1(A.part1, A.nb1, s);
-    if (tid == 0) st[0] = d2;
-  }
-  __syncthreads();
-  const double d2 = st[0];
+  const double d2 = sum_part1(A.part1, A.nb1, s);
   const bool degenerate = !(d2 > 0.0);
   if (A.status && blockIdx.x == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
@@ -288,33 +269,31 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv
   extern __shared__ float4 smem4[];
   float4 *tw = smem4;
   float2 *buf = reinterpret_cast<float2 *>(smem4 + N);
-  __shared__ double st[3];
+  float2 *ys = buf + H * C::RPITCH;  // [H][N]: y rows staged by cp.async (read in the epilogue)
   const int tid = threadIdx.x, s = blockIdx.y;
   const int t = tid % TPV, b = tid / TPV;
   const int i = blockIdx.x * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
+  {
+    const char *src = reinterpret_cast<const char *>(A.y + (size_t)s * P + (size_t)blockIdx.x * H * N);
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(ys);
+    for (int k = tid * 16; k < H * N * 8; k += NT * 16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k), "l"(src + k));
+    asm volatile("cp.async.commit_group;");
+  }
   float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.cbuf[row + t + TPV * e];
-  if (t == 0) {  // y row -> L2 (read in the epilogue)
-    for (int k = 0; k < N * 8; k += 128) prefetch_l2(reinterpret_cast<const char *>(A.y + row) + k);
-  }
   load_tw<N>(tw, A.tw4, tid, NT);
-  if (tid < 32) {
-    double sums[5];
-    sum_part0(A.part0, A.nb0, s, sums);
-    const double d2 = sum_part1(A.part1, A.nb1, s);
-    if (tid == 0) {
-      st[0] = sums[0] / P;
-      st[1] = sums[1] / P;
-      st[2] = d2;
-    }
-  }
-  __syncthreads();
-  const float mur = (float)st[0], mui = (float)st[1];
-  const double d2 = st[2];
+  double sums[5];
+  sum_part0(A.part0, A.nb0, s, sums);
+  const double d2 = sum_part1(A.part1, A.nb1, s);
+  const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
   const float kappa = d2 > 0.0 ? (float)sqrt((double)P / d2) : 0.f;
+  __syncthreads();  // twiddles
   fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
+  asm volatile("cp.async.wait_group 0;");
+  __syncthreads();  // y rows staged
   // v = G = conj(F) with F = inverse row DFT; f = chi F / N, so
   // z = y-hat conj(f) = y-hat chi G / N
   const int2 sp = __ldg(A.rowspan + i);
@@ -325,7 +304,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv
     float c = 0.f, th = 0.f;
     if (j >= sp.x && j < sp.y) {
       const float sg = ((i + j) & 1) ? -kn : kn;
-      const float2 yh = p_mul(p_sub(A.y[row + j], make_float2(mur, mui)), bc2(sg));
+      const float2 yh = p_mul(p_sub(ys[b * N + j], make_float2(mur, mui)), bc2(sg));
       const float2 g = v[e];
       const float2 z = p_fma(bc2(yh.x), g, p_mul(bc2(yh.y), make_float2(-g.y, g.x)));  // yh * g
       c = two_s2 * sqrt_approx(fmaf(z.x, z.x, z.y * z.y) + 1e-37f);
@@ -368,29 +347,42 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
   extern __shared__ float icd_sm[];
   float *rs = icd_sm, *qs = icd_sm + 4 * kSub * kSubP;
-  __shared__ double st[1];
   const int tid = threadIdx.x, s = blockIdx.z;
   const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
   const size_t off = (size_t)s * P;
   const float *__restrict__ rin = A.icd_in + off;
   const float *__restrict__ qin = A.q + off;
-  if (tid < 32) {
-    const double d2 = sum_part1(A.part1, A.nb1, s);
-    if (tid == 0) st[0] = d2;
+  // region rows x column pairs (8-byte loads; pairs never straddle the wrap),
+  // in two batches whose loads are all in flight before the smem stores
+  constexpr int NL = (kReg * kSub + kSThreads - 1) / kSThreads, NL0 = (NL + 1) / 2;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float2 rv[NL0], qv[NL0];
+#pragma unroll
+    for (int k = 0; k < NL0; ++k) {
+      const int idx = tid + (h * NL0 + k) * kSThreads;
+      if (h * NL0 + k < NL && idx < kReg * kSub) {
+        const int li = idx / kSub, pj = idx - li * kSub;
+        const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
+        rv[k] = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
+        qv[k] = *reinterpret_cast<const float2 *>(qin + (size_t)gi * N + gj);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NL0; ++k) {
+      const int idx = tid + (h * NL0 + k) * kSThreads;
+      if (h * NL0 + k < NL && idx < kReg * kSub) {
+        const int li = idx / kSub, pj = idx - li * kSub;
+        const int e0 = sidx(2 * (li & 1), li >> 1, pj), e1 = sidx(2 * (li & 1) + 1, li >> 1, pj);
+        rs[e0] = rv[k].x;
+        rs[e1] = rv[k].y;
+        qs[e0] = qv[k].x;
+        qs[e1] = qv[k].y;
+      }
+    }
   }
-  // region rows x column pairs (8-byte loads; pairs never straddle the wrap)
-  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
-    const int li = idx / kSub, pj = idx - li * kSub;
-    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
-    const float2 v = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
-    const float2 qv = *reinterpret_cast<const float2 *>(qin + (size_t)gi * N + gj);
-    rs[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
-    rs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
-    qs[sidx(2 * (li & 1), li >> 1, pj)] = qv.x;
-    qs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = qv.y;
-  }
+  const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   __syncthreads();
-  const bool degenerate = !(st[0] > 0.0);
   if (A.r_prior && !degenerate) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -460,28 +452,15 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
   extern __shared__ float icd_sm[];
   float *ps = icd_sm;
-  __shared__ double st[4];
   const int tid = threadIdx.x, s = blockIdx.z;
   const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
   const size_t off = (size_t)s * P;
   const float *__restrict__ pin = A.icd_in + off;
-  if (tid < 32) {
-    double sums[5];
-    sum_part0(A.part0, A.nb0, s, sums);
-    const double d2 = sum_part1(A.part1, A.nb1, s);
-    if (tid == 0) {
-      double c[3] = {0, 0, 0};
-      if (A.apply_plane) plane_from_sums(sums, A.minv, c);
-      st[0] = c[0];
-      st[1] = c[1];
-      st[2] = c[2];
-      st[3] = d2;
-    }
-  }
-  __syncthreads();
-  const bool degenerate = !(st[3] > 0.0);
-  const float c0 = degenerate ? 0.f : (float)st[0], c1 = degenerate ? 0.f : (float)st[1],
-              c2 = degenerate ? 0.f : (float)st[2];
+  double sums[5], cpl[3] = {0, 0, 0};
+  sum_part0(A.part0, A.nb0, s, sums);
+  const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
+  if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
+  const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
   for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
     const int li = idx / kSub, pj = idx - li * kSub;
     const int gi = i0 - kHalo + li, gj = j0 - kHalo + 2 * pj;
@@ -570,12 +549,13 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   }
 
 template <int N> static size_t srow_smem() { return N * sizeof(float4) + (size_t)SCfg<N>::H * SCfg<N>::RPITCH * sizeof(float2); }
+template <int N> static size_t srowi_smem() { return srow_smem<N>() + (size_t)SCfg<N>::H * N * sizeof(float2); }
 template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t)N * SCfg<N>::W * sizeof(float2); }
 
 template <int N>
 static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
-  cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
+  cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
   cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
@@ -606,7 +586,7 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
-  DDH_SDISPATCH(a.n, (ks_rows_inv<N><<<dim3(N / SCfg<N>::H, a.sc), SCfg<N>::NTR, srow_smem<N>(), st>>>(a)));
+  DDH_SDISPATCH(a.n, (ks_rows_inv<N><<<dim3(N / SCfg<N>::H, a.sc), SCfg<N>::NTR, srowi_smem<N>(), st>>>(a)));
   return cudaGetLastError();
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {

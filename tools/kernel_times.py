@@ -17,14 +17,19 @@ for S in map(int, sys.argv[2:]):
     for t in range(3):
         ctx.step(ys[t:t + 1])
     torch.cuda.synchronize()
-    ctx.profile(True); ctx.profile_read()
+    prof_on = os.environ.get("PROF", "1") == "1"
+    ctx.profile(prof_on); ctx.profile_read()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     K = 50
+    import time
     e0.record()
+    h0 = time.perf_counter()
     for k in range(K):
         ctx.step(ys[k % 4:k % 4 + 1])
+    h1 = time.perf_counter()
     e1.record(); torch.cuda.synchronize()
+    host_us = (h1 - h0) / K * 1e6
     prof = ctx.profile_read(); ctx.profile(False)
     tot = e0.elapsed_time(e1) / K * 1000
-    print(f"S={S:3d} step {tot:7.1f} us  " + "  ".join(f"{k} {v[0] / K * 1000:6.1f}" for k, v in prof.items()), flush=True)
+    print(f"S={S:3d} step {tot:7.1f} us (host enqueue {host_us:6.1f} us)  " + "  ".join(f"{k} {v[0] / K * 1000:6.1f}" for k, v in prof.items()), flush=True)
     del ctx
