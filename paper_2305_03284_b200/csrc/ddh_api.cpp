@@ -646,11 +646,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const std::string path = pe ? pe : "";
     if (path == "multipass" || (path.empty() && (p.flags & DDH_F_UNFUSED))) {
       c->fused = c->streaming = false;
-    } else if (path == "cluster3") {
-      c->fused = ddh::fused_supported(n);
-    } else if (path == "cluster" || path == "mega" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
+    } else if (path == "mega") {  // experimental: KA+KB+KC as one persistent launch (measured slower)
       c->fused = ddh::fused_supported(n);
       c->mega = c->fused;
+    } else if (path == "cluster" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
+      c->fused = ddh::fused_supported(n);
     } else {
       c->streaming = true;
     }
