@@ -56,6 +56,8 @@ typedef enum {
                                structure, used as a second implementation)      */
 #define DDH_F_CLUSTER 4u    /* force the cluster-fused 3-kernel iteration (N <= 512);
                                default: the streaming 6-kernel iteration          */
+#define DDH_F_SERIAL 8u     /* enqueue every kernel on the ctx stream in order (no
+                               lanes, no side stream): per-kernel event timing     */
 
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 

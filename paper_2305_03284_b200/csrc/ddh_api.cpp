@@ -658,7 +658,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (c->streaming) A(ddh::init_stream(n));
   if (c->streaming || ddh::fused_supported(n)) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
-    c->lanes = ev ? std::atoi(ev) : p.lanes;
+    c->lanes = (p.flags & DDH_F_SERIAL) ? 1 : ev ? std::atoi(ev) : p.lanes;
     if (c->lanes <= 0)  // measured at 256^2 x 64 streams: stream path 2, cluster path 4
       c->lanes = c->mega ? 1 : c->streaming ? std::min(2, std::max(1, c->sc / 32)) : std::min(4, std::max(1, c->sc / 16));
     c->lanes = std::max(1, std::min(8, c->lanes));
@@ -667,7 +667,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
-    c->split_r = c->streaming && (sr ? std::atoi(sr) != 0 : true);
+    c->split_r = c->streaming && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
         A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));
