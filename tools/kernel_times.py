@@ -12,7 +12,7 @@ yd = torch.from_numpy(y).cuda()
 nv = synth.recon_noise_var(256, 256, 5.0)
 lanes = int(os.environ.get("LANES", "1"))
 for S in map(int, sys.argv[2:]):
-    ctx = DDH(n, S, noise_var=nv, lanes=lanes, flags=int(os.environ.get("FLAGS", "0")))
+    ctx = DDH(n, S, noise_var=nv, lanes=lanes, flags=int(os.environ.get("FLAGS", "0")), chunk_streams=int(os.environ.get("CHUNK", "0")))
     ys = yd[:, :S].contiguous()
     for t in range(3):
         ctx.step(ys[t:t + 1])
