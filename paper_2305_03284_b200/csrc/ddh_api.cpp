@@ -65,6 +65,7 @@ struct ddh_ctx {
   // streaming path: the r M-step (S3) of a lane runs on a side stream,
   // concurrently with the phi branch (S4, S5) it does not depend on (R12)
   bool split_r = false;
+  bool mix34 = false;  // S3 and S4 as one interleaved launch
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // instrumentation
@@ -101,12 +102,12 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
   } while (0)
 
 enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
-            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM };
+            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM, K_S34 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
                                           "kf_rows_fwd", "kf_cols", "kf_rows_inv",
                                           "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd",
-                                          "kf_mega"};
+                                          "kf_mega", "ks_mix34"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
@@ -321,6 +322,18 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
+          if (c->mix34 && sw == 1) {  // S3 + S4 in one launch
+            b.icd_in = c->rinit + wo;
+            b.icd_out = c->r + go;
+            b.icd_copy = (last && r_out) ? r_out + go : nullptr;
+            DDH_LAUNCH_ON(c, K_S34, st, ddh::launch_s34(b, st));
+            b.icd_in = c->phi[cl] + go;
+            b.icd_out = c->phi[cl ^ 1] + go;
+            b.icd_copy = (last && phi_out) ? phi_out + go : nullptr;
+            DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+            cl ^= 1;
+            continue;
+          }
           cudaStream_t rst = st;
           if (c->split_r) {  // fork: S3 after S2, beside S4/S5
             rst = c->side_st[l];
@@ -667,7 +680,9 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
-    c->split_r = c->streaming && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
+    const char *mx = std::getenv("DDH_MIX34");  // diagnostic override
+    c->mix34 = c->streaming && (mx ? std::atoi(mx) != 0 : false);  // measured slower (3 CTAs/SM)
+    c->split_r = c->streaming && !c->mix34 && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
         A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));

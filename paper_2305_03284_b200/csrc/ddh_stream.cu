@@ -293,20 +293,20 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
 // ------------------------------------------------------------------ S4
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
+__device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, const int s) {
   using C = SCfg<N>;
   constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
   extern __shared__ float4 smem4[];
   float4 *tw = smem4;
   float2 *buf = reinterpret_cast<float2 *>(smem4 + N);
   float2 *ys = buf + H * C::RPITCH;  // [H][N]: y rows staged by cp.async (read in the epilogue)
-  const int tid = threadIdx.x, s = blockIdx.y;
+  const int tid = threadIdx.x;
   const int t = tid % TPV, b = tid / TPV;
-  const int i = blockIdx.x * H + b;
+  const int i = bx * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
   DDH_PDL_TRIGGER();
   {  // y is read-only user input: staged before the wait
-    const char *src = reinterpret_cast<const char *>(A.y + (size_t)s * P + (size_t)blockIdx.x * H * N);
+    const char *src = reinterpret_cast<const char *>(A.y + (size_t)s * P + (size_t)bx * H * N);
     const unsigned dst = (unsigned)__cvta_generic_to_shared(ys);
     for (int k = tid * 16; k < H * N * 8; k += NT * 16)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k), "l"(src + k));
@@ -347,6 +347,11 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv
   }
 }
 
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv(StepArgs A) {
+  rows_inv_body<N>(A, blockIdx.x, blockIdx.y);
+}
+
 // ------------------------------------------------------------ ICD tiles
 
 namespace {
@@ -375,12 +380,12 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 // colour c in the region shrunk by c+1 on each side, so after the 4 phases the
 // 64x64 core equals the global colour-ordered sweep.
 template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
+__device__ __forceinline__ void ricd_body(const StepArgs &A, const int bx, const int by, const int s) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
   extern __shared__ float icd_sm[];
   float *rs = icd_sm, *qs = icd_sm + 4 * kSub * kSubP;
-  const int tid = threadIdx.x, s = blockIdx.z;
-  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
+  const int tid = threadIdx.x;
+  const int i0 = by * T, j0 = bx * T;
   const size_t off = (size_t)s * P;
   const float *__restrict__ rin = A.icd_in + off;
   const float *__restrict__ qin = A.q + off;
@@ -474,6 +479,35 @@ __global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
     }
     *reinterpret_cast<float2 *>(A.icd_out + g) = v;
     if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
+  ricd_body<N>(A, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// S3 + S4 as one launch (one r-ICD sweep): the two are independent (R12), so
+// interleaving their CTAs (even: an r-ICD tile, odd: a row slab) puts the
+// MUFU/FMA-bound tiles and the memory-bound inverse row DFTs on the same SMs.
+template <int N>
+__global__ void __launch_bounds__(kSThreads, 4) ks_mix34(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, NTI = (N / T) * (N / T), NRS = N / SCfg<N>::H;
+  const int n3 = NTI * A.sc, n4 = NRS * A.sc, m = n3 < n4 ? n3 : n4;
+  const int b = blockIdx.x;
+  int kind, idx;
+  if (b < 2 * m) {
+    kind = b & 1;
+    idx = b >> 1;
+  } else {
+    kind = n3 > n4 ? 0 : 1;
+    idx = m + (b - 2 * m);
+  }
+  if (kind == 0) {
+    const int s = idx / NTI, r = idx - s * NTI;
+    ricd_body<N>(A, r % (N / T), r / (N / T), s);
+  } else {
+    rows_inv_body<N>(A, idx % NRS, idx / NRS);
   }
 }
 
@@ -594,6 +628,8 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
   cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_mix34<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(srowi_smem<N>() > 2 * kIcdGrid * sizeof(float) ? srowi_smem<N>() : 2 * kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
   return cudaGetLastError();
 }
@@ -635,6 +671,14 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
+}
+cudaError_t launch_s34(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  const int nb = ((N / T) * (N / T) + N / SCfg<N>::H) * a.sc;
+                  const size_t sm = srowi_smem<N>() > 2 * kIcdGrid * sizeof(float) ? srowi_smem<N>() : 2 * kIcdGrid * sizeof(float);
+                  return launch_pdl(ks_mix34<N>, dim3(nb), dim3(kSThreads), sm, st, a);
+                }));
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
