@@ -66,6 +66,7 @@ struct ddh_ctx {
   // concurrently with the phi branch (S4, S5) it does not depend on (R12)
   bool split_r = false;
   bool mix34 = false;  // S3 and S4 as one interleaved launch
+  bool icdp = true;    // pipelined persistent ICD tile kernels
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // instrumentation
@@ -344,7 +345,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_in = k == 0 ? c->rinit + wo : c->rtmp[(k - 1) & 1] + wo;
             b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
+            DDH_LAUNCH_ON(c, K_S3, rst, c->icdp ? ddh::launch_s3p(b, rst) : ddh::launch_s3(b, rst));
           }
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
           const int plane_it = b.apply_plane;
@@ -353,7 +354,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_out = k == sw - 1 ? c->phi[cl ^ 1] + go : c->ptmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
             b.apply_plane = k == 0 ? plane_it : 0;
-            DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+            DDH_LAUNCH_ON(c, K_S5, st, c->icdp ? ddh::launch_s5p(b, st) : ddh::launch_s5(b, st));
           }
           if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
             DDH_CK(c, cudaEventRecord(c->side_join[l], rst));
@@ -680,6 +681,8 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
+    const char *ip = std::getenv("DDH_ICDP");  // diagnostic override
+    c->icdp = ip ? std::atoi(ip) != 0 : true;
     const char *mx = std::getenv("DDH_MIX34");  // diagnostic override
     c->mix34 = c->streaming && (mx ? std::atoi(mx) != 0 : false);  // measured slower (3 CTAs/SM)
     c->split_r = c->streaming && !c->mix34 && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);

@@ -128,7 +128,9 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_s34(const StepArgs &a, cudaStream_t st);  // S3 + S4 in one launch (one sweep)
+cudaError_t launch_s34(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s3p(const StepArgs &a, cudaStream_t st);  // pipelined persistent r-ICD tiles
+cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st);  // pipelined persistent phi-ICD tiles  // S3 + S4 in one launch (one sweep)
 
 cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
                               cudaStream_t st);

@@ -606,6 +606,259 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   }
 }
 
+
+// ------------------------------------------- pipelined persistent ICD tiles
+//
+// Same sweep as ks_ricd / ks_phiicd, but each CTA loops over tiles and
+// double-buffers them: while it computes the 4 colour phases of tile k, the
+// 16-byte cp.async copies of tile k+1 (and L2 prefetches of its q or c/theta)
+// are in flight, so the memory time of one tile hides under the compute of
+// the previous one.  Plain row-major tile [kReg][kRP] (2-way bank conflicts on
+// the stride-2 colour accesses, in exchange for 5 copy instructions per thread).
+namespace {
+constexpr int kRP = kReg + 4;            // tile pitch in floats (16-byte rows)
+constexpr int kTileF = kReg * kRP;       // floats per tile stage
+constexpr int kChunks = kReg * kReg / 4; // 16-byte chunks per tile (18 per row)
+
+// Issue the copies of the tile (i0, j0) of field `src` into `dst`; periodic or
+// free (zero-filled outside the frame) boundary.
+template <int N, bool PERIODIC>
+__device__ __forceinline__ void tile_copy_async(float *dst, const float *__restrict__ src, int i0, int j0, int tid) {
+  for (int idx = tid; idx < kChunks; idx += kSThreads) {
+    const int row = idx / (kReg / 4), ch = idx - row * (kReg / 4);
+    int gi = i0 - kHalo + row, gj = j0 - kHalo + 4 * ch;
+    bool in = true;
+    if (PERIODIC) {
+      gi &= N - 1;
+      gj &= N - 1;
+    } else {
+      in = gi >= 0 && gi < N && gj >= 0 && gj < N;  // chunks are wholly inside or outside
+    }
+    const float *g = src + (in ? (size_t)gi * N + gj : 0);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst + row * kRP + 4 * ch)),
+                 "l"(g), "r"(in ? 16 : 0));
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void tile_prefetch_l2(const float *__restrict__ src, int i0, int j0, int tid) {
+  // rows of the 72-wide region (3 x 128-byte lines each, periodic rows)
+  for (int idx = tid; idx < kReg * 3; idx += kSThreads) {
+    const int row = idx / 3, k = idx - row * 3;
+    const int gi = (i0 - kHalo + row) & (N - 1), gj = (j0 - kHalo + 32 * k) & (N - 1);
+    prefetch_l2(src + (size_t)gi * N + gj);
+  }
+}
+
+// Pixels of colour C in phase C (plain tile), lanes on sub-columns, warps on rows.
+template <int C, class F>
+__device__ __forceinline__ void for_colour_p(int tid, F &&f) {
+  constexpr int ci = C >> 1, cj = C & 1, NW = kSThreads / 32;
+  constexpr int alo = sub_lo(C + 1, ci), ahi = sub_lo(kReg - C - 1, ci);
+  constexpr int blo = sub_lo(C + 1, cj), bhi = sub_lo(kReg - C - 1, cj);
+  constexpr int na = ahi - alo, nb = bhi - blo;
+  const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+  for (int k = 0; k < (na + NW - 1) / NW; ++k) {
+    const int a = alo + warp + NW * k;
+    if (a < ahi) f(2 * a + ci, 2 * (blo + lane) + cj);
+  }
+  if constexpr (nb > 32) {
+    constexpr int tc = nb - 32;
+    const int p = tid;
+    if (p < tc * na) f(2 * (alo + p / tc) + ci, 2 * (blo + 32 + p % tc) + cj);
+  }
+}
+}  // namespace
+
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_ricd_p(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, P = N * N, TPS = (N / T) * (N / T);
+  extern __shared__ float icd_sm[];
+  const int tid = threadIdx.x;
+  const int ntiles = TPS * A.sc;
+  DDH_PDL_TRIGGER();
+  DDH_PDL_WAIT();
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  auto tile_of = [&](int tt, int &s, int &i0, int &j0) {
+    s = tt / TPS;
+    const int r = tt - s * TPS;
+    i0 = (r / (N / T)) * T;
+    j0 = (r % (N / T)) * T;
+  };
+  {
+    int s, i0, j0;
+    tile_of(t, s, i0, j0);
+    tile_copy_async<N, true>(icd_sm, A.icd_in + (size_t)s * P, i0, j0, tid);
+    tile_prefetch_l2<N>(A.q + (size_t)s * P, i0, j0, tid);
+  }
+  const float h = A.r_h, g = A.r_g, kq = A.r_k, b6 = A.r_b6, rmin = A.r_min;
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    float *rs = icd_sm + (k & 1) * kTileF;
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) {  // next tile -> the other stage
+      int s, i0, j0;
+      tile_of(tn, s, i0, j0);
+      tile_copy_async<N, true>(icd_sm + ((k + 1) & 1) * kTileF, A.icd_in + (size_t)s * P, i0, j0, tid);
+      tile_prefetch_l2<N>(A.q + (size_t)s * P, i0, j0, tid);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    int s, i0, j0;
+    tile_of(t, s, i0, j0);
+    const size_t off = (size_t)s * P;
+    const float *__restrict__ qin = A.q + off;
+    const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
+    if (A.r_prior && !degenerate) {
+      auto phase = [&](auto cc) {
+        constexpr int C = decltype(cc)::value;
+        for_colour_p<C>(tid, [&](int li, int lj) {
+          const int me = li * kRP + lj;
+          const float ri = rs[me];
+          const float q = __ldg(qin + (size_t)((i0 - kHalo + li) & (N - 1)) * N + ((j0 - kHalo + lj) & (N - 1)));
+          const float2 nA = make_float2(rs[me - kRP], rs[me + kRP]);
+          const float2 nB = make_float2(rs[me - 1], rs[me + 1]);
+          const float2 dA = make_float2(rs[me - kRP - 1], rs[me - kRP + 1]);
+          const float2 dB = make_float2(rs[me + kRP - 1], rs[me + kRP + 1]);
+          const float2 wA = qgg_w2(ri, nA, h, g, kq), wB = qgg_w2(ri, nB, h, g, kq);
+          const float2 wC = qgg_w2(ri, dA, h, g, kq), wD = qgg_w2(ri, dB, h, g, kq);
+          const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+          const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+          rs[me] = r_update(ri, q, b6 * (bs.x + bs.y), b6 * (ss.x + ss.y), rmin);
+        });
+        __syncthreads();
+      };
+      phase(std::integral_constant<int, 0>());
+      phase(std::integral_constant<int, 1>());
+      phase(std::integral_constant<int, 2>());
+      phase(std::integral_constant<int, 3>());
+    }
+    // core -> out (prior off: r = max(q, r_min); degenerate: unchanged)
+    for (int idx = tid; idx < T * (T / 4); idx += kSThreads) {
+      const int oi = idx / (T / 4), c4 = idx - oi * (T / 4);
+      const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 4 * c4);
+      float4 v = *reinterpret_cast<const float4 *>(rs + (oi + kHalo) * kRP + kHalo + 4 * c4);
+      if (!A.r_prior && !degenerate) {
+        const float4 qv = *reinterpret_cast<const float4 *>(A.q + gidx);
+        v = make_float4(fmaxf(qv.x, rmin), fmaxf(qv.y, rmin), fmaxf(qv.z, rmin), fmaxf(qv.w, rmin));
+      }
+      *reinterpret_cast<float4 *>(A.icd_out + gidx) = v;
+      if (A.icd_copy) *reinterpret_cast<float4 *>(A.icd_copy + gidx) = v;
+    }
+    __syncthreads();  // stage k&1 is refilled by the prefetch of the next iteration
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_phiicd_p(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, P = N * N, TPS = (N / T) * (N / T);
+  extern __shared__ float icd_sm[];
+  const int tid = threadIdx.x;
+  const int ntiles = TPS * A.sc;
+  DDH_PDL_TRIGGER();
+  DDH_PDL_WAIT();
+  int t = blockIdx.x;
+  if (t >= ntiles) return;
+  auto tile_of = [&](int tt, int &s, int &i0, int &j0) {
+    s = tt / TPS;
+    const int r = tt - s * TPS;
+    i0 = (r / (N / T)) * T;
+    j0 = (r % (N / T)) * T;
+  };
+  auto prefetch_ct = [&](int s, int i0, int j0) {
+    tile_prefetch_l2<N>(A.cc + (size_t)s * P, i0, j0, tid);
+    tile_prefetch_l2<N>(A.theta + (size_t)s * P, i0, j0, tid);
+  };
+  {
+    int s, i0, j0;
+    tile_of(t, s, i0, j0);
+    tile_copy_async<N, false>(icd_sm, A.icd_in + (size_t)s * P, i0, j0, tid);
+    prefetch_ct(s, i0, j0);
+  }
+  const bool prior = A.phi_prior != 0;
+  const float w = A.phi_w;
+  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
+    float *ps = icd_sm + (k & 1) * kTileF;
+    const int tn = t + gridDim.x;
+    if (tn < ntiles) {
+      int s, i0, j0;
+      tile_of(tn, s, i0, j0);
+      tile_copy_async<N, false>(icd_sm + ((k + 1) & 1) * kTileF, A.icd_in + (size_t)s * P, i0, j0, tid);
+      prefetch_ct(s, i0, j0);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    int s, i0, j0;
+    tile_of(t, s, i0, j0);
+    const size_t off = (size_t)s * P;
+    double sums[5], cpl[3] = {0, 0, 0};
+    sum_part0(A.part0, A.nb0, s, sums);
+    const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
+    if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
+    __syncthreads();
+    if (cpl[0] != 0.0 || cpl[1] != 0.0 || cpl[2] != 0.0) {  // phi' = phi - plane (first sweep of a step)
+      const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
+      for (int idx = tid; idx < kChunks; idx += kSThreads) {
+        const int row = idx / (kReg / 4), ch = idx - row * (kReg / 4);
+        const int gi = i0 - kHalo + row, gj = j0 - kHalo + 4 * ch;
+        if (gi >= 0 && gi < N && gj >= 0 && gj < N) {
+          float4 *p4 = reinterpret_cast<float4 *>(ps + row * kRP + 4 * ch);
+          float4 v = *p4;
+          const float pl = c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2);
+          v.x -= pl;
+          v.y -= pl + c1;
+          v.z -= pl + 2.f * c1;
+          v.w -= pl + 3.f * c1;
+          *p4 = v;
+        }
+      }
+      __syncthreads();
+    }
+    if (!degenerate) {
+      const bool edge = i0 == 0 || j0 == 0 || i0 + T == N || j0 + T == N;
+      const float *__restrict__ ccs = A.cc + off;
+      const float *__restrict__ ths = A.theta + off;
+      auto phase = [&](auto cc) {
+        constexpr int C = decltype(cc)::value;
+        for_colour_p<C>(tid, [&](int li, int lj) {
+          const int gi = i0 - kHalo + li, gj = j0 - kHalo + lj;
+          float sb = 1.f;  // sum of b over the existing neighbours (free boundary)
+          if (edge) {
+            if (gi < 0 || gi >= N || gj < 0 || gj >= N) return;  // outside the frame: absent
+            const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
+            sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+                 (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
+          }
+          const int me = li * kRP + lj;
+          const size_t gg = (size_t)gi * N + gj;
+          const float cv = __ldg(ccs + gg), tv = __ldg(ths + gg);
+          const float n4 = (ps[me - kRP] + ps[me + kRP]) + (ps[me - 1] + ps[me + 1]);
+          const float nd = (ps[me - kRP - 1] + ps[me - kRP + 1]) + (ps[me + kRP - 1] + ps[me + kRP + 1]);
+          ps[me] = phi_update(ps[me], cv, tv, fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f)), sb, w, prior);
+        });
+        __syncthreads();
+      };
+      phase(std::integral_constant<int, 0>());
+      phase(std::integral_constant<int, 1>());
+      phase(std::integral_constant<int, 2>());
+      phase(std::integral_constant<int, 3>());
+    }
+    for (int idx = tid; idx < T * (T / 4); idx += kSThreads) {
+      const int oi = idx / (T / 4), c4 = idx - oi * (T / 4);
+      const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 4 * c4);
+      const float4 v = degenerate ? *reinterpret_cast<const float4 *>(A.icd_in + gidx)
+                                  : *reinterpret_cast<const float4 *>(ps + (oi + kHalo) * kRP + kHalo + 4 * c4);
+      *reinterpret_cast<float4 *>(A.icd_out + gidx) = v;
+      if (A.icd_copy) *reinterpret_cast<float4 *>(A.icd_copy + gidx) = v;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------- launchers
 
 #define DDH_SDISPATCH(n, CALL)                          \
@@ -623,7 +876,11 @@ template <int N> static size_t srowi_smem() { return srow_smem<N>() + (size_t)SC
 template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t)N * SCfg<N>::W * sizeof(float2); }
 
 template <int N>
+static void init_icdp();
+
+template <int N>
 static cudaError_t init_stream_n() {
+  init_icdp<N>();
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
@@ -672,6 +929,37 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
 }
+static int g_icdp_grid[2][11];  // persistent grid of ks_ricd_p / ks_phiicd_p per log2 N
+
+template <int N>
+static void init_icdp() {
+  const int l = 31 - __builtin_clz(N);
+  int dev = 0, sms = 148, nb = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(ks_ricd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kTileF * sizeof(float)));
+  cudaFuncSetAttribute(ks_phiicd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kTileF * sizeof(float)));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks_ricd_p<N>, kSThreads, 2 * kTileF * sizeof(float));
+  g_icdp_grid[0][l] = sms * (nb > 0 ? nb : 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks_phiicd_p<N>, kSThreads, 2 * kTileF * sizeof(float));
+  g_icdp_grid[1][l] = sms * (nb > 0 ? nb : 1);
+}
+
+cudaError_t launch_s3p(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  const int nt = (N / T) * (N / T) * a.sc, gp = g_icdp_grid[0][31 - __builtin_clz(N)];
+                  return launch_pdl(ks_ricd_p<N>, dim3(nt < gp ? nt : gp), dim3(kSThreads), 2 * kTileF * sizeof(float), st, a);
+                }));
+}
+cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  const int nt = (N / T) * (N / T) * a.sc, gp = g_icdp_grid[1][31 - __builtin_clz(N)];
+                  return launch_pdl(ks_phiicd_p<N>, dim3(nt < gp ? nt : gp), dim3(kSThreads), 2 * kTileF * sizeof(float), st, a);
+                }));
+}
+
 cudaError_t launch_s34(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
                   constexpr int T = N < kTile ? N : kTile;
