@@ -422,23 +422,28 @@ def quick_parity(ctx, y_dev, y_host, t, n, nv, dev):
 
 
 def e2e_leg(ctx, y_host, K, ws, dev, S, n):
+    """End to end through ddh_step_host: pinned host frames in, phi out; every
+    step's H2D copy and D2H read are inside the timed region.  Calls of T_c
+    frames let the library overlap the copies of neighbouring frames with the
+    step (double-buffered staging)."""
     import torch
     E = min(y_host.shape[0], 16)
-    Ke = min(K, 200)
+    Tc = E
+    Ke = max(Tc, min(K, 208) // Tc * Tc)
     y_pin = torch.from_numpy(np.ascontiguousarray(y_host[:E])).pin_memory()
-    phi_pin = torch.empty((1, S, n, n), dtype=torch.float32).pin_memory()
-    for k in range(2):
-        ctx.step_host(y_pin[k:k + 1], phi_out=phi_pin)
+    phi_pin = torch.empty((Tc, S, n, n), dtype=torch.float32).pin_memory()
+    ctx.step_host(y_pin[:2], phi_out=phi_pin[:2])
     barrier(ws)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(Ke):
-        ctx.step_host(y_pin[k % E:k % E + 1], phi_out=phi_pin)  # synchronous (D2H of phi inside)
+    for k in range(Ke // Tc):
+        ctx.step_host(y_pin[:Tc], phi_out=phi_pin)  # synchronous (all D2H of phi inside)
     dt = time.perf_counter() - t0
     dt = reduce_max(dt, ws, dev)
     P = n * n
     return {"value": Ke * S * ws / dt, "unit": UNIT, "h2d_bytes_per_step": S * P * 8, "d2h_bytes_per_step": S * P * 4,
-            "steps": Ke, "api": "ddh_step_host (pinned host y in, phi out), host wall clock, max over ranks"}
+            "steps": Ke, "frames_per_call": Tc,
+            "api": "ddh_step_host (pinned host y in, phi out; copies overlapped across frames), host wall clock, max over ranks"}
 
 
 def latency_leg(dev, local):

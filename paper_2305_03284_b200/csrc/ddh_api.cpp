@@ -52,10 +52,13 @@ struct ddh_ctx {
   float2 *tw = nullptr;
   double minv[9] = {};
   double strehl_den = 1.0;
-  // host-buffer path
-  float2 *y_stage = nullptr;
-  float *phi_stage = nullptr, *r_stage = nullptr;
-  uint8_t *status_stage = nullptr;
+  // host-buffer path: double-buffered staging, H2D / compute / D2H on three
+  // streams so the copies of frames t+1 and t-1 overlap the step of frame t
+  float2 *y_stage[2] = {nullptr, nullptr};
+  float *phi_stage[2] = {nullptr, nullptr}, *r_stage[2] = {nullptr, nullptr};
+  uint8_t *status_stage[2] = {nullptr, nullptr};
+  cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
+  cudaEvent_t h2d_ev[2] = {}, comp_ev[2] = {}, d2h_ev[2] = {};
   // concurrent launch lanes of the fused path: the streams of a launch group
   // are split over `lanes` CUDA streams so that the kernels of different
   // sub-groups (KA of one, KB of another, ...) share the SMs
@@ -483,6 +486,13 @@ void free_ctx(ddh_ctx *c) {
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : c->lane_st)
     if (s) cudaStreamDestroy(s);
+  for (int k = 0; k < 2; ++k) {
+    if (c->h2d_ev[k]) cudaEventDestroy(c->h2d_ev[k]);
+    if (c->comp_ev[k]) cudaEventDestroy(c->comp_ev[k]);
+    if (c->d2h_ev[k]) cudaEventDestroy(c->d2h_ev[k]);
+  }
+  if (c->h2d_st) cudaStreamDestroy(c->h2d_st);
+  if (c->d2h_st) cudaStreamDestroy(c->d2h_st);
   for (int l = 0; l < 8; ++l) {
     if (c->side_st[l]) cudaStreamDestroy(c->side_st[l]);
     if (c->side_fork[l]) cudaEventDestroy(c->side_fork[l]);
@@ -490,7 +500,8 @@ void free_ctx(ddh_ctx *c) {
   }
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
-                  c->y_stage, c->phi_stage, c->r_stage, c->status_stage};
+                  c->y_stage[0], c->phi_stage[0], c->r_stage[0], c->status_stage[0],
+                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1]};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -799,27 +810,51 @@ ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_o
   if (T < 0 || (!y_host && T > 0)) return fail(c, DDH_E_INVAL, "ddh_step_host: bad arguments");
   DDH_CK(c, cudaSetDevice(c->p.device));
   const size_t fs = (size_t)c->S * c->P;
-  if (!c->y_stage) {
-    cudaError_t e = dalloc(&c->y_stage, fs);
-    if (e == cudaSuccess) e = dalloc(&c->phi_stage, fs);
-    if (e == cudaSuccess) e = dalloc(&c->r_stage, fs);
-    if (e == cudaSuccess) e = dalloc(&c->status_stage, (size_t)c->S);
+  if (!c->y_stage[0]) {
+    cudaError_t e = cudaSuccess;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = dalloc(&c->y_stage[k], fs);
+      if (e == cudaSuccess) e = dalloc(&c->phi_stage[k], fs);
+      if (e == cudaSuccess) e = dalloc(&c->r_stage[k], fs);
+      if (e == cudaSuccess) e = dalloc(&c->status_stage[k], (size_t)c->S);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->h2d_ev[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->comp_ev[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->d2h_ev[k], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->h2d_st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h_st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(c, DDH_E_NOMEM, "ddh_step_host: staging allocation failed");
   }
+  // frame t uses stage k = t & 1: H2D(t) waits for the step of t-2 (reader of
+  // y_stage[k]); the step of t waits for H2D(t) and for D2H(t-2) (reader of
+  // the output stages); D2H(t) waits for the step of t.
+  DDH_CK(c, cudaEventRecord(c->comp_ev[0], c->st));  // order after prior work on the ctx stream
+  DDH_CK(c, cudaEventRecord(c->comp_ev[1], c->st));
+  DDH_CK(c, cudaEventRecord(c->d2h_ev[0], c->st));
+  DDH_CK(c, cudaEventRecord(c->d2h_ev[1], c->st));
   for (int t = 0; t < T; ++t) {
-    DDH_CK(c, cudaMemcpyAsync(c->y_stage, (const float2 *)y_host + t * fs, fs * sizeof(float2),
-                              cudaMemcpyHostToDevice, c->st));
-    s = run_frame(c, c->y_stage, phi_out ? c->phi_stage : nullptr, r_out ? c->r_stage : nullptr,
-                  status ? c->status_stage : nullptr, Mode::Step, c->p.n_k);
+    const int k = t & 1;
+    DDH_CK(c, cudaStreamWaitEvent(c->h2d_st, c->comp_ev[k], 0));
+    DDH_CK(c, cudaMemcpyAsync(c->y_stage[k], (const float2 *)y_host + t * fs, fs * sizeof(float2),
+                              cudaMemcpyHostToDevice, c->h2d_st));
+    DDH_CK(c, cudaEventRecord(c->h2d_ev[k], c->h2d_st));
+    DDH_CK(c, cudaStreamWaitEvent(c->st, c->h2d_ev[k], 0));
+    DDH_CK(c, cudaStreamWaitEvent(c->st, c->d2h_ev[k], 0));
+    s = run_frame(c, c->y_stage[k], phi_out ? c->phi_stage[k] : nullptr, r_out ? c->r_stage[k] : nullptr,
+                  status ? c->status_stage[k] : nullptr, Mode::Step, c->p.n_k);
     if (s != DDH_OK) return s;
     c->frame += 1;
+    DDH_CK(c, cudaEventRecord(c->comp_ev[k], c->st));
+    DDH_CK(c, cudaStreamWaitEvent(c->d2h_st, c->comp_ev[k], 0));
     if (phi_out)
-      DDH_CK(c, cudaMemcpyAsync(phi_out + t * fs, c->phi_stage, fs * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+      DDH_CK(c, cudaMemcpyAsync(phi_out + t * fs, c->phi_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
     if (r_out)
-      DDH_CK(c, cudaMemcpyAsync(r_out + t * fs, c->r_stage, fs * sizeof(float), cudaMemcpyDeviceToHost, c->st));
+      DDH_CK(c, cudaMemcpyAsync(r_out + t * fs, c->r_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
     if (status)
-      DDH_CK(c, cudaMemcpyAsync(status + (size_t)t * c->S, c->status_stage, c->S, cudaMemcpyDeviceToHost, c->st));
+      DDH_CK(c, cudaMemcpyAsync(status + (size_t)t * c->S, c->status_stage[k], c->S, cudaMemcpyDeviceToHost, c->d2h_st));
+    DDH_CK(c, cudaEventRecord(c->d2h_ev[k], c->d2h_st));
   }
+  DDH_CK(c, cudaStreamSynchronize(c->d2h_st));
   DDH_CK(c, cudaStreamSynchronize(c->st));
   return DDH_OK;
 }
