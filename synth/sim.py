@@ -46,6 +46,12 @@ CONFIGS: Dict[str, dict] = {
                flow=2.0, direction="cols", sigma_b=4.0, snr_db=2.0, n_k=1, k_b=0),
     "c5": dict(name="c5", n=1024, diam=1024, streams=1, frames=50, d_r0=30.0, d_r0_range=None,
                flow=2.0, direction="cols", sigma_b=4.0, snr_db=2.0, n_k=1, k_b=0),
+    # the paper's own simulation conditions (not a BASELINE config): N = 256,
+    # D/r0 = 10, f_g/f_s = 100 Hz / 10 kHz -> |v| = 0.595 px/frame along (1, 1)/sqrt 2
+    # (v = (0.421, 0.421)), SNR 10 dB, cold start; the USAF chart is replaced by R23's field
+    "paper": dict(name="paper", n=256, diam=256, streams=1, frames=300, d_r0=10.0, d_r0_range=None,
+                  flow=(1.0 / 0.43) * (100.0 / 10000.0) * (256 / 10.0), direction="angle", angle=math.pi / 4,
+                  sigma_b=3.0, snr_db=10.0, n_k=1, k_b=0, scene="bars"),
 }
 
 
@@ -129,6 +135,30 @@ def blurred_reflectance(n: int, sigma_b: float, rng: np.random.Generator, r_min:
     return np.maximum(rb, r_min)
 
 
+def bar_target(n: int, low: float = 0.02) -> np.ndarray:
+    """Procedural bar-target reflectance for the paper-conditions check (a
+    stand-in for a resolution chart, not a copy of one): groups of three bright
+    bars, alternately horizontal and vertical, halving in size group by group,
+    on a dark background (value `low`), scaled to the grid."""
+    r = np.full((n, n), low)
+    s = n / 256.0
+    x0, y0, w = int(24 * s), int(24 * s), 16.0 * s
+    k = 0
+    while w >= 1.0 and y0 < n - 2:
+        wi, L = max(1, int(round(w))), max(3, int(round(5 * w)))
+        for b in range(3):
+            if k % 2 == 0:  # horizontal bars
+                r[y0 + 2 * b * wi:y0 + (2 * b + 1) * wi, x0:x0 + L] = 1.0
+            else:           # vertical bars
+                r[y0:y0 + L, x0 + 2 * b * wi:x0 + (2 * b + 1) * wi] = 1.0
+        x0 += L + 3 * wi
+        if x0 + 5 * w > n - 8 * s:
+            x0, y0 = int(24 * s), y0 + L + 3 * wi
+        w /= 1.41421356
+        k += 1
+    return r
+
+
 def make_stream(cfg: dict, stream: int, frames: int = None, seed: int = SEED0,
                 snr_db: float = None, d_r0: float = None, r_true: np.ndarray = None):
     """Synthesize one stream of a config.  Returns (y [T][N][N] complex64,
@@ -140,7 +170,10 @@ def make_stream(cfg: dict, stream: int, frames: int = None, seed: int = SEED0,
     sd = seed + stream
     a = aperture_mask(n, diam)
     if r_true is None:
-        r_true = blurred_reflectance(n, cfg["sigma_b"], rng_for(sd, stream, 0, _P_SCENE))
+        if cfg.get("scene") == "bars":
+            r_true = bar_target(n)
+        else:
+            r_true = blurred_reflectance(n, cfg["sigma_b"], rng_for(sd, stream, 0, _P_SCENE))
     if d_r0 is None:
         if cfg.get("d_r0_range"):
             lo, hi = cfg["d_r0_range"]
@@ -149,8 +182,8 @@ def make_stream(cfg: dict, stream: int, frames: int = None, seed: int = SEED0,
             d_r0 = cfg["d_r0"]
     r0_px = diam / d_r0 if d_r0 > 0 else float("inf")
     v = cfg["flow"]
-    if cfg["direction"] == "random":
-        th = 2 * np.pi * rng_for(sd, stream, 0, _P_DIR).random()
+    if cfg["direction"] in ("random", "angle"):
+        th = cfg["angle"] if cfg["direction"] == "angle" else 2 * np.pi * rng_for(sd, stream, 0, _P_DIR).random()
         m = 2 * n
         coeffs = screen_coeffs(m, m, r0_px, rng_for(sd, stream, 0, _P_SCREEN)) if d_r0 > 0 else None
     else:
