@@ -70,6 +70,7 @@ struct ddh_ctx {
   bool split_r = false;
   bool mix34 = false;  // S3 and S4 as one interleaved launch
   bool icdp = true;    // pipelined persistent ICD tile kernels
+  bool mix35 = false;  // S3 and S5 as one interleaved launch
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // instrumentation
@@ -106,12 +107,12 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
   } while (0)
 
 enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
-            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM, K_S34 };
+            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM, K_S34, K_S35 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
                                           "kf_rows_fwd", "kf_cols", "kf_rows_inv",
                                           "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd",
-                                          "kf_mega", "ks_mix34"};
+                                          "kf_mega", "ks_mix34", "ks_mix35"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
@@ -326,6 +327,18 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
+          if (c->mix35 && sw == 1) {  // S4, then S3 + S5 in one launch
+            DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
+            b.icd_in = c->rinit + wo;
+            b.icd_out = c->r + go;
+            b.icd_copy = (last && r_out) ? r_out + go : nullptr;
+            b.icd2_in = c->phi[cl] + go;
+            b.icd2_out = c->phi[cl ^ 1] + go;
+            b.icd2_copy = (last && phi_out) ? phi_out + go : nullptr;
+            DDH_LAUNCH_ON(c, K_S35, st, ddh::launch_s35(b, st));
+            cl ^= 1;
+            continue;
+          }
           if (c->mix34 && sw == 1) {  // S3 + S4 in one launch
             b.icd_in = c->rinit + wo;
             b.icd_out = c->r + go;
@@ -694,6 +707,8 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
     const char *ip = std::getenv("DDH_ICDP");  // diagnostic override
     c->icdp = ip ? std::atoi(ip) != 0 : true;
+    const char *m5 = std::getenv("DDH_MIX35");  // diagnostic override
+    c->mix35 = c->streaming && (m5 ? std::atoi(m5) != 0 : false);  // measured slower
     const char *mx = std::getenv("DDH_MIX34");  // diagnostic override
     c->mix34 = c->streaming && (mx ? std::atoi(mx) != 0 : false);  // measured slower (3 CTAs/SM)
     c->split_r = c->streaming && !c->mix34 && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);

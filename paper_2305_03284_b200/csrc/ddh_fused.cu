@@ -196,6 +196,8 @@ __device__ __forceinline__ void phase_a(const StepArgs &A, const int s) {
 
 template <int N>
 __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_fwd(StepArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   phase_a<N>(A, blockIdx.y);
 }
 
@@ -385,6 +387,8 @@ __device__ __forceinline__ void phase_b(const StepArgs &A, const int s, const in
 
 template <int N>
 __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_cols(StepArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int s = blockIdx.y; s < A.sc; s += gridDim.y)  // persistent: one stream per iteration
     phase_b<N>(A, s, s + gridDim.y);
 }
@@ -579,6 +583,8 @@ __device__ __forceinline__ void phase_c(const StepArgs &A, const int s) {
 
 template <int N>
 __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_inv(StepArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   phase_c<N>(A, blockIdx.y);
 }
 
@@ -594,6 +600,8 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
 // the MUFU-bound r-ICD of one overlaps the FFTs of another.
 template <int N>
 __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_mega(StepArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   cg::cluster_group cl = cg::this_cluster();
   for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {
     phase_a<N>(A, s);
@@ -614,13 +622,15 @@ static cudaError_t launch_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 bloc
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cs;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL (griddepcontrol in the phases)
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 

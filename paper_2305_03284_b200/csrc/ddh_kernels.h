@@ -60,6 +60,8 @@ struct StepArgs {
   const float *icd_in;    // S3: r before the sweep; S5: phi before the sweep [sc][N][N]
   float *icd_out;         // S3 / S5 output [sc][N][N]
   float *icd_copy;        // optional user copy of the output or null
+  const float *icd2_in;   // S3+S5 launch: phi before the sweep (icd_* = r)
+  float *icd2_out, *icd2_copy;
 };
 
 struct IcdArgs {
@@ -128,7 +130,8 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_s34(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_s34(const StepArgs &a, cudaStream_t st);  // S3 + S4 in one launch (one sweep)
+cudaError_t launch_s35(const StepArgs &a, cudaStream_t st);  // S3 + S5 in one launch (one sweep)
 cudaError_t launch_s3p(const StepArgs &a, cudaStream_t st);  // pipelined persistent r-ICD tiles
 cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st);  // pipelined persistent phi-ICD tiles  // S3 + S4 in one launch (one sweep)
 

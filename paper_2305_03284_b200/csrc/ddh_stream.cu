@@ -516,14 +516,15 @@ __global__ void __launch_bounds__(kSThreads, 4) ks_mix34(StepArgs A) {
 // (value 0 in the tile, excluded from sum b).  The first sweep of a time step
 // subtracts the RemoveTipTilt plane (from the S0 sums) on load.
 template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
+__device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, const int by, const int s,
+                                            const float *phi_in, float *phi_out, float *phi_copy) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
   extern __shared__ float icd_sm[];
   float *ps = icd_sm;
-  const int tid = threadIdx.x, s = blockIdx.z;
-  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
+  const int tid = threadIdx.x;
+  const int i0 = by * T, j0 = bx * T;
   const size_t off = (size_t)s * P;
-  const float *__restrict__ pin = A.icd_in + off;
+  const float *__restrict__ pin = phi_in + off;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
   double sums[5], cpl[3] = {0, 0, 0};
@@ -601,9 +602,28 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
     const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
                                 : make_float2(ps[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
                                               ps[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
-    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
-    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+    *reinterpret_cast<float2 *>(phi_out + g) = v;
+    if (phi_copy) *reinterpret_cast<float2 *>(phi_copy + g) = v;
   }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
+  phiicd_body<N>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
+}
+
+// S3 + S5 as one launch: the r M-step (after S2) and the phi M-step (after S4)
+// are independent (R12); interleaving their 64x64 tiles (even CTA: r, odd: phi)
+// mixes the MUFU-bound r tiles with the lighter phi tiles on every SM.
+// r: A.icd_in/out/copy; phi: A.icd2_in/out/copy.
+template <int N>
+__global__ void __launch_bounds__(kSThreads) ks_mix35(StepArgs A) {
+  constexpr int T = N < kTile ? N : kTile, TPS = (N / T) * (N / T);
+  const int idx = blockIdx.x >> 1, s = idx / TPS, r = idx - s * TPS;
+  if (blockIdx.x & 1)
+    phiicd_body<N>(A, r % (N / T), r / (N / T), s, A.icd2_in, A.icd2_out, A.icd2_copy);
+  else
+    ricd_body<N>(A, r % (N / T), r / (N / T), s);
 }
 
 
@@ -888,6 +908,7 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_mix34<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(srowi_smem<N>() > 2 * kIcdGrid * sizeof(float) ? srowi_smem<N>() : 2 * kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_mix35<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
   return cudaGetLastError();
 }
 
@@ -957,6 +978,14 @@ cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st) {
                   constexpr int T = N < kTile ? N : kTile;
                   const int nt = (N / T) * (N / T) * a.sc, gp = g_icdp_grid[1][31 - __builtin_clz(N)];
                   return launch_pdl(ks_phiicd_p<N>, dim3(nt < gp ? nt : gp), dim3(kSThreads), 2 * kTileF * sizeof(float), st, a);
+                }));
+}
+
+cudaError_t launch_s35(const StepArgs &a, cudaStream_t st) {
+  DDH_SDISPATCH(a.n, ({
+                  constexpr int T = N < kTile ? N : kTile;
+                  return launch_pdl(ks_mix35<N>, dim3(2 * (N / T) * (N / T) * a.sc), dim3(kSThreads),
+                                    2 * kIcdGrid * sizeof(float), st, a);
                 }));
 }
 
