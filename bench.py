@@ -246,7 +246,7 @@ def run_ours(args):
         extra = dict(r_sigma=0.0, phi_sigma=0.0)
     if args.unfused:
         args.path = "multipass"
-    extra["flags"] = {"stream": 0, "cluster": 4, "multipass": 2}[args.path]
+    extra["flags"] = {"stream": 0, "cluster": 4, "multipass": 2}[args.path] | (8 if args.serial else 0)
     ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk, **extra)
     K, W = args.steps, args.warmup
     for w in range(W):
@@ -324,9 +324,13 @@ def run_ours(args):
     # 148 SMs x 4 schedulers x SM clock; warp instructions per
     # launch from the committed ncu capture of the same launch configuration
     inst = None
-    for k, v in summ.get("kernels", {}).items():
-        if k.split("<")[0] == dom:
-            inst = v.get("smsp__inst_executed.sum [inst]")
+    kn = {k.split("<")[0]: v for k, v in summ.get("kernels", {}).items()}
+    # the library's kind name covers both variants of a stage (e.g. ks_ricd / ks_ricd_p)
+    match = kn.get(dom) or next((v for k, v in kn.items() if k.startswith(dom + "_")), None)
+    if match:
+        inst = match.get("smsp__inst_executed.sum [inst]")
+    if traffic is None:
+        traffic = next((v for k, v in summ.get("dram_bytes_per_launch", {}).items() if k.startswith(dom)), None)
     if inst:
         sm_mhz = clocks.get("sm_mhz") or 1965.0
         ipeak = 148 * 4 * sm_mhz * 1e6
@@ -491,6 +495,9 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--priors-off", action="store_true", help="diagnostic: disable both priors")
     ap.add_argument("--unfused", action="store_true", help="diagnostic: multi-pass kernels (= --path multipass)")
+    ap.add_argument("--serial", action="store_true",
+                    help="profiling aid: DDH_F_SERIAL for the main ctx too (the launch configuration of the "
+                         "attribution pass, for ncu captures)")
     ap.add_argument("--path", choices=["stream", "cluster", "multipass"], default="stream",
                     help="EM-iteration implementation (default: streaming)")
     args = ap.parse_args()

@@ -22,11 +22,11 @@ print({k: (round(v["ms_total"] / d["steps"] * 1000, 1), round(v.get("gbs", 0))) 
 PY
       ;;
     ncu)
-      CMD="python bench.py --steps 5 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity ${BENCH_EXTRA:-}"
+      CMD="python bench.py --steps 5 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity --serial ${BENCH_EXTRA:-}"
       $CMD > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ks_|kf_" -s 12 -c 6 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
       echo "ncu rc=$?"; tail -2 gpurun_out/ncu_full.log ;;
     launches)
-      CMD="python bench.py --steps 20 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity"
+      CMD="python bench.py --steps 20 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity --serial"
       $CMD > gpurun_out/launch_plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
       echo "launches rc=$?" ;;
   esac

@@ -45,7 +45,7 @@ if os.path.exists(lcsv):
     allns = sum(tot.values())
     with open(os.path.join(out_dir, f"{rnd}_launches.txt"), "w") as f:
         f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none (launch list of\n"
-                f"# bench.py --steps 20 --warmup 3 --frames 8 ...); cold-cache, serialised launches:\n"
+                f"# bench.py --steps 20 --warmup 3 --frames 8 --serial ...); cold-cache, serialised launches:\n"
                 f"# compare SHARES with bench.py's live CUDA-event breakdown, not absolute times.\n")
         f.write(f"{'kernel':24s} {'launches':>8s} {'total_us':>10s} {'avg_us':>8s} {'share':>6s}\n")
         for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
@@ -85,8 +85,9 @@ if os.path.exists(rep):
         summary["dram_bytes_per_launch"][base] = rb + wb
         lines.append(f"{name}\n" + "\n".join(f"  {k}: {v}" for k, v in d.items()))
     with open(os.path.join(out_dir, f"{rnd}_ncu_full.txt"), "w") as f:
-        f.write("# ncu --set full --clock-control none --import-source on -k regex:'kf_|k[0-3]' -s 9 -c 3\n"
-                "# (bench.py --steps 5 --warmup 3 --frames 8, one launch of each kernel, 64 streams of c3)\n"
+        f.write("# ncu --set full --clock-control none --import-source on -k regex:'ks_|kf_' -s 12 -c 6\n"
+                "# (bench.py --steps 5 --warmup 3 --frames 8 --serial: one launch of each kernel, 64 streams of c3,\n"
+                "#  the launch configuration of bench.py's attribution pass)\n"
                 "# bytes in bytes; other units in brackets\n\n")
         f.write("\n\n".join(lines) + "\n")
     json.dump(summary, open(os.path.join(out_dir, "ncu_summary.json"), "w"), indent=1)
