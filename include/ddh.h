@@ -180,7 +180,7 @@ int64_t ddh_frame_index(const ddh_ctx *c);
  * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
  * 8 KA kf_rows_fwd, 9 KB kf_cols, 10 KC kf_rows_inv (cluster-fused path).
  * When enabled, every launch of the ctx is bracketed by two events. */
-#define DDH_KIND_COUNT 20
+#define DDH_KIND_COUNT 17
 ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable);
 /* Synchronises the ctx stream and ADDS the accumulated totals since the last
  * read into ms[k] (milliseconds) and launches[k] (host arrays of

@@ -42,7 +42,6 @@ struct ddh_ctx {
   float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
   double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
   bool fused = false;
-  bool mega = false;  // fused path as one persistent launch per EM iteration
   int cs = 0;  // CTAs per stream of the fused path
   bool streaming = false;  // cluster-free 6-kernel path (ddh_stream.cu)
   float4 *tw4 = nullptr;
@@ -68,9 +67,6 @@ struct ddh_ctx {
   // streaming path: the r M-step (S3) of a lane runs on a side stream,
   // concurrently with the phi branch (S4, S5) it does not depend on (R12)
   bool split_r = false;
-  bool mix34 = false;  // S3 and S4 as one interleaved launch
-  bool icdp = true;    // pipelined persistent ICD tile kernels
-  bool mix35 = false;  // S3 and S5 as one interleaved launch
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // instrumentation
@@ -107,12 +103,11 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
   } while (0)
 
 enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
-            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5, K_KM, K_S34, K_S35 };
+            K_S0, K_S1, K_S2, K_S3, K_S4, K_S5 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
                                           "kf_rows_fwd", "kf_cols", "kf_rows_inv",
-                                          "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd",
-                                          "kf_mega", "ks_mix34", "ks_mix35"};
+                                          "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
 cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
@@ -327,30 +322,6 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
-          if (c->mix35 && sw == 1) {  // S4, then S3 + S5 in one launch
-            DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
-            b.icd_in = c->rinit + wo;
-            b.icd_out = c->r + go;
-            b.icd_copy = (last && r_out) ? r_out + go : nullptr;
-            b.icd2_in = c->phi[cl] + go;
-            b.icd2_out = c->phi[cl ^ 1] + go;
-            b.icd2_copy = (last && phi_out) ? phi_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S35, st, ddh::launch_s35(b, st));
-            cl ^= 1;
-            continue;
-          }
-          if (c->mix34 && sw == 1) {  // S3 + S4 in one launch
-            b.icd_in = c->rinit + wo;
-            b.icd_out = c->r + go;
-            b.icd_copy = (last && r_out) ? r_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S34, st, ddh::launch_s34(b, st));
-            b.icd_in = c->phi[cl] + go;
-            b.icd_out = c->phi[cl ^ 1] + go;
-            b.icd_copy = (last && phi_out) ? phi_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
-            cl ^= 1;
-            continue;
-          }
           cudaStream_t rst = st;
           if (c->split_r) {  // fork: S3 after S2, beside S4/S5
             rst = c->side_st[l];
@@ -361,7 +332,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_in = k == 0 ? c->rinit + wo : c->rtmp[(k - 1) & 1] + wo;
             b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
-            DDH_LAUNCH_ON(c, K_S3, rst, c->icdp ? ddh::launch_s3p(b, rst) : ddh::launch_s3(b, rst));
+            DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
           }
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
           const int plane_it = b.apply_plane;
@@ -370,7 +341,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_out = k == sw - 1 ? c->phi[cl ^ 1] + go : c->ptmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
             b.apply_plane = k == 0 ? plane_it : 0;
-            DDH_LAUNCH_ON(c, K_S5, st, c->icdp ? ddh::launch_s5p(b, st) : ddh::launch_s5(b, st));
+            DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
           }
           if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
             DDH_CK(c, cudaEventRecord(c->side_join[l], rst));
@@ -426,13 +397,9 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           b.r_copy = (last && r_out) ? r_out + go : nullptr;
           b.phi_copy = (last && phi_out) ? phi_out + go : nullptr;
-          if (c->mega) {
-            DDH_LAUNCH_ON(c, K_KM, st, ddh::launch_km(b, st));
-          } else {
-            DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
-            DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
-            DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
-          }
+          DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
+          DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
+          DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
           cl ^= 1;
         }
       }
@@ -684,9 +651,6 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const std::string path = pe ? pe : "";
     if (path == "multipass" || (path.empty() && (p.flags & DDH_F_UNFUSED))) {
       c->fused = c->streaming = false;
-    } else if (path == "mega") {  // experimental: KA+KB+KC as one persistent launch (measured slower)
-      c->fused = ddh::fused_supported(n);
-      c->mega = c->fused;
     } else if (path == "cluster" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
       c->fused = ddh::fused_supported(n);
     } else {
@@ -698,20 +662,14 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = (p.flags & DDH_F_SERIAL) ? 1 : ev ? std::atoi(ev) : p.lanes;
     if (c->lanes <= 0)  // measured at 256^2 x 64 streams: stream path 2, cluster path 4
-      c->lanes = c->mega ? 1 : c->streaming ? std::min(2, std::max(1, c->sc / 32)) : std::min(4, std::max(1, c->sc / 16));
+      c->lanes = c->streaming ? std::min(2, std::max(1, c->sc / 32)) : std::min(4, std::max(1, c->sc / 16));
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
-    const char *ip = std::getenv("DDH_ICDP");  // diagnostic override
-    c->icdp = ip ? std::atoi(ip) != 0 : true;
-    const char *m5 = std::getenv("DDH_MIX35");  // diagnostic override
-    c->mix35 = c->streaming && (m5 ? std::atoi(m5) != 0 : false);  // measured slower
-    const char *mx = std::getenv("DDH_MIX34");  // diagnostic override
-    c->mix34 = c->streaming && (mx ? std::atoi(mx) != 0 : false);  // measured slower (3 CTAs/SM)
-    c->split_r = c->streaming && !c->mix34 && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
+    c->split_r = c->streaming && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
         A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));

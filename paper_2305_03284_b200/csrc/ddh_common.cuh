@@ -119,10 +119,14 @@ __device__ __forceinline__ float2 qgg_w2(float ri, float2 rj, float h, float g, 
   const float2 a = p_fma(d, d, bc2(1e-37f));
   const float2 e = p_fma(make_float2(lg2_approx(a.x), lg2_approx(a.y)), bc2(h), bc2(g));
   const float2 u = p_add(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(1.f));
+#ifdef DDH_QGG_MUFU_RCP
+  const float2 y = make_float2(rcp_approx(u.x), rcp_approx(u.y));
+#else
   float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(u.x)), __int_as_float(0x7EF311C3 - __float_as_int(u.y)));
   const float2 nu = make_float2(-u.x, -u.y);
 #pragma unroll
   for (int it = 0; it < 3; ++it) y = p_mul(y, p_fma(nu, y, bc2(2.f)));
+#endif
   return p_mul(p_fma(y, bc2(1.f - k), bc2(k)), y);  // (k + (1-k)/u) / u
 }
 

@@ -86,11 +86,6 @@ template <int N> __host__ __device__ constexpr size_t kc_smem() {
   return (size_t)C::H * (N + 1) * sizeof(float2) + (size_t)(C::H + 2) * (N + 8) * sizeof(float) + (size_t)N * sizeof(float2);
 }
 
-template <int N> __host__ __device__ constexpr size_t km_smem() {
-  return ka_smem<N>() > kb_smem<N>() ? (ka_smem<N>() > kc_smem<N>() ? ka_smem<N>() : kc_smem<N>())
-                                     : (kb_smem<N>() > kc_smem<N>() ? kb_smem<N>() : kc_smem<N>());
-}
-
 // ------------------------------------------------------------------- KA
 
 template <int N>
@@ -588,30 +583,6 @@ __global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_rows_in
   phase_c<N>(A, blockIdx.y);
 }
 
-// ------------------------------------------------------------- megakernel
-//
-// The whole EM iteration of a stream in one persistent cluster: phase A (rows),
-// cluster barrier, phase B (columns + r-ICD), cluster barrier, phase C (rows +
-// phi-ICD); then the next stream of this cluster.  The spectrum crosses
-// between phases through this stream's own cbuf slice (L2); the cluster
-// barrier (arrive.release / wait.acquire at cluster scope) orders those global
-// writes and reads.  One launch per EM iteration instead of three: no launch
-// ramps and tails between the phases, and the clusters drift out of phase so
-// the MUFU-bound r-ICD of one overlaps the FFTs of another.
-template <int N>
-__global__ void __launch_bounds__(FusedCfg<N>::NT, FusedCfg<N>::MINB) kf_mega(StepArgs A) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  cg::cluster_group cl = cg::this_cluster();
-  for (int s = blockIdx.y; s < A.sc; s += gridDim.y) {
-    phase_a<N>(A, s);
-    cl.sync();  // cbuf rows of stream s (all CTAs) visible
-    phase_b<N>(A, s, s + gridDim.y);
-    cl.sync();  // cbuf columns of stream s visible
-    phase_c<N>(A, s);
-  }
-}
-
 // ------------------------------------------------------------- launchers
 
 template <typename... KArgs, typename... Args>
@@ -642,9 +613,7 @@ static cudaError_t init_fused_n() {
   cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ka_smem<N>());
   cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kb_smem<N>());
   cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kc_smem<N>());
-  cudaFuncSetAttribute(kf_mega<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)km_smem<N>());
   if (FusedCfg<N>::CS > 8) {
-    cudaFuncSetAttribute(kf_mega<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_rows_fwd<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_cols<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kf_rows_inv<N>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -666,7 +635,7 @@ cudaError_t init_fused(int n) { DDH_FDISPATCH(n, return init_fused_n<N>()); }
 
 // Persistent grids: as many clusters as can be co-resident (queried once per
 // kernel with cudaOccupancyMaxActiveClusters), each looping over streams.
-static int g_max_clusters[4][11];  // [kernel][log2 N]
+static int g_max_clusters[3][11];  // [kernel][log2 N]
 
 template <typename... KArgs>
 static int max_clusters(void (*kernel)(KArgs...), int cs, int nt, size_t smem) {
@@ -698,7 +667,6 @@ static void init_grids() {
   g_max_clusters[0][l] = 1 << 20;
   g_max_clusters[1][l] = max_clusters(kf_cols<N>, C::CS, C::NT, kb_smem<N>());
   g_max_clusters[2][l] = 1 << 20;
-  g_max_clusters[3][l] = max_clusters(kf_mega<N>, C::CS, C::NT, km_smem<N>());
 }
 
 static inline int grid_y(int which, int n, int sc) {
@@ -713,10 +681,6 @@ cudaError_t launch_ka(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st) {
   DDH_FDISPATCH(a.n, return launch_cluster(kf_cols<N>, dim3(FusedCfg<N>::CS, grid_y(1, N, a.sc)),
                                            dim3(FusedCfg<N>::NT), kb_smem<N>(), FusedCfg<N>::CS, st, a));
-}
-cudaError_t launch_km(const StepArgs &a, cudaStream_t st) {
-  DDH_FDISPATCH(a.n, return launch_cluster(kf_mega<N>, dim3(FusedCfg<N>::CS, grid_y(3, N, a.sc)),
-                                           dim3(FusedCfg<N>::NT), km_smem<N>(), FusedCfg<N>::CS, st, a));
 }
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st) {
   DDH_FDISPATCH(a.n, return launch_cluster(kf_rows_inv<N>, dim3(FusedCfg<N>::CS, grid_y(2, N, a.sc)),

@@ -60,8 +60,6 @@ struct StepArgs {
   const float *icd_in;    // S3: r before the sweep; S5: phi before the sweep [sc][N][N]
   float *icd_out;         // S3 / S5 output [sc][N][N]
   float *icd_copy;        // optional user copy of the output or null
-  const float *icd2_in;   // S3+S5 launch: phi before the sweep (icd_* = r)
-  float *icd2_out, *icd2_copy;
 };
 
 struct IcdArgs {
@@ -117,7 +115,6 @@ cudaError_t init_fused(int n);
 cudaError_t launch_ka(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kb(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_kc(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_km(const StepArgs &a, cudaStream_t st);  // KA+KB+KC in one persistent launch
 
 // streaming (cluster-free) EM iteration, ddh_stream.cu: S0 stats, S1 rows,
 // S2 cols + E-step, S3 r-ICD tiles, S4 inverse rows + c/theta, S5 phi-ICD tiles
@@ -130,10 +127,6 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_s34(const StepArgs &a, cudaStream_t st);  // S3 + S4 in one launch (one sweep)
-cudaError_t launch_s35(const StepArgs &a, cudaStream_t st);  // S3 + S5 in one launch (one sweep)
-cudaError_t launch_s3p(const StepArgs &a, cudaStream_t st);  // pipelined persistent r-ICD tiles
-cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st);  // pipelined persistent phi-ICD tiles  // S3 + S4 in one launch (one sweep)
 
 cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
                               cudaStream_t st);

@@ -375,139 +375,77 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 
 // r M-step: one 4-colour sweep of the qGGMRF ICD (R6-R9) for the 64x64 tile
 // (blockIdx.x, blockIdx.y) of stream blockIdx.z, from A.icd_in (r after Eq. 3,
-// or the previous sweep) and A.q, into A.icd_out (+ A.icd_copy).  The tile is
-// loaded with a 4-pixel periodic halo; colour phase c updates the pixels of
-// colour c in the region shrunk by c+1 on each side, so after the 4 phases the
-// 64x64 core equals the global colour-ordered sweep.
+// or the previous sweep) into A.icd_out (+ A.icd_copy).  The tile is loaded
+// colour-separated with a 4-pixel periodic halo; colour phase c updates the
+// pixels of colour c in the region shrunk by c+1 on each side, so after the 4
+// phases the 64x64 core equals the global colour-ordered sweep.  q is read
+// from global (L2) at the pixel's update and only r is staged (21 KB smem),
+// within 32 registers: 8 CTAs (64 warps) per SM.
 template <int N>
-__device__ __forceinline__ void ricd_body(const StepArgs &A, const int bx, const int by, const int s) {
+__global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
   constexpr int T = N < kTile ? N : kTile, P = N * N;
   extern __shared__ float icd_sm[];
-  float *rs = icd_sm, *qs = icd_sm + 4 * kSub * kSubP;
-  const int tid = threadIdx.x;
-  const int i0 = by * T, j0 = bx * T;
+  float *rs = icd_sm;
+  const int tid = threadIdx.x, s = blockIdx.z;
+  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
   const size_t off = (size_t)s * P;
   const float *__restrict__ rin = A.icd_in + off;
   const float *__restrict__ qin = A.q + off;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
-  // region rows x column pairs (8-byte loads; pairs never straddle the wrap),
-  // in two batches whose loads are all in flight before the smem stores
-  constexpr int NL = (kReg * kSub + kSThreads - 1) / kSThreads, NL0 = (NL + 1) / 2;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    float2 rv[NL0], qv[NL0];
-#pragma unroll
-    for (int k = 0; k < NL0; ++k) {
-      const int idx = tid + (h * NL0 + k) * kSThreads;
-      if (h * NL0 + k < NL && idx < kReg * kSub) {
-        const int li = idx / kSub, pj = idx - li * kSub;
-        const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
-        rv[k] = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
-        qv[k] = *reinterpret_cast<const float2 *>(qin + (size_t)gi * N + gj);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NL0; ++k) {
-      const int idx = tid + (h * NL0 + k) * kSThreads;
-      if (h * NL0 + k < NL && idx < kReg * kSub) {
-        const int li = idx / kSub, pj = idx - li * kSub;
-        const int e0 = sidx(2 * (li & 1), li >> 1, pj), e1 = sidx(2 * (li & 1) + 1, li >> 1, pj);
-        rs[e0] = rv[k].x;
-        rs[e1] = rv[k].y;
-        qs[e0] = qv[k].x;
-        qs[e1] = qv[k].y;
-      }
-    }
+  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
+    const int li = idx / kSub, pj = idx - li * kSub;
+    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
+    const float2 v = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
+    rs[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
+    rs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
   }
   const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   __syncthreads();
   if (A.r_prior && !degenerate) {
+    const float h = A.r_h, g = A.r_g, kq = A.r_k, b6 = A.r_b6, rmin = A.r_min;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      // colour (CI, CJ) as compile-time values through a switch-free unroll
       const int ci = c >> 1, cj = c & 1;
       const int alo = sub_lo(c + 1, ci), ahi = sub_lo(kReg - c - 1, ci);
       const int blo = sub_lo(c + 1, cj), bhi = sub_lo(kReg - c - 1, cj);
-      const int na = ahi - alo, nbb = bhi - blo, cnt = na * nbb;
-      constexpr int KMAX = (35 * 35 + kSThreads - 1) / kSThreads;  // 5
-      float Bv[KMAX], Sv[KMAX], Rv[KMAX];
-      int ix[KMAX];
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        const int p = tid + k * kSThreads;
-        ix[k] = -1;
-        if (p < cnt) {
-          const int a = alo + p / nbb, bb = blo + p % nbb;
-          float ri, n0, n1, n2, n3, d0, d1, d2v, d3;
+      const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
+#pragma unroll 1
+      for (int p = tid; p < cnt; p += kSThreads) {
+        const int a = alo + p / nbb, bb = blo + p % nbb;
+        float ri, n0, n1, n2, n3, d0, d1, d2v, d3;
 #define DDH_NB(CI, CJ)                                                                       \
   ri = rs[sidx(2 * CI + CJ, a, bb)];                                                          \
   n0 = rs[nidx<CI, CJ, -1, 0>(a, bb)]; n1 = rs[nidx<CI, CJ, 1, 0>(a, bb)];                    \
   n2 = rs[nidx<CI, CJ, 0, -1>(a, bb)]; n3 = rs[nidx<CI, CJ, 0, 1>(a, bb)];                    \
   d0 = rs[nidx<CI, CJ, -1, -1>(a, bb)]; d1 = rs[nidx<CI, CJ, -1, 1>(a, bb)];                  \
   d2v = rs[nidx<CI, CJ, 1, -1>(a, bb)]; d3 = rs[nidx<CI, CJ, 1, 1>(a, bb)];
-          if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
+        if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
 #undef DDH_NB
-          const float2 nA = make_float2(n0, n1), nB = make_float2(n2, n3);
-          const float2 dA = make_float2(d0, d1), dB = make_float2(d2v, d3);
-          const float2 wA = qgg_w2(ri, nA, A.r_h, A.r_g, A.r_k), wB = qgg_w2(ri, nB, A.r_h, A.r_g, A.r_k);
-          const float2 wC = qgg_w2(ri, dA, A.r_h, A.r_g, A.r_k), wD = qgg_w2(ri, dB, A.r_h, A.r_g, A.r_k);
-          const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
-          const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
-          Bv[k] = A.r_b6 * (bs.x + bs.y);
-          Sv[k] = A.r_b6 * (ss.x + ss.y);
-          Rv[k] = ri;
-          ix[k] = sidx(c, a, bb);
-          Rv[k] = r_update(ri, qs[ix[k]], Bv[k], Sv[k], A.r_min);
-        }
+        const int gi = (i0 - kHalo + 2 * a + ci) & (N - 1), gj = (j0 - kHalo + 2 * bb + cj) & (N - 1);
+        const float q = __ldg(qin + (size_t)gi * N + gj);
+        const float2 nA = make_float2(n0, n1), nB = make_float2(n2, n3);
+        const float2 dA = make_float2(d0, d1), dB = make_float2(d2v, d3);
+        const float2 wA = qgg_w2(ri, nA, h, g, kq), wB = qgg_w2(ri, nB, h, g, kq);
+        const float2 wC = qgg_w2(ri, dA, h, g, kq), wD = qgg_w2(ri, dB, h, g, kq);
+        const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+        const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+        rs[sidx(c, a, bb)] = r_update(ri, q, b6 * (bs.x + bs.y), b6 * (ss.x + ss.y), rmin);
       }
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (ix[k] >= 0) rs[ix[k]] = Rv[k];
       __syncthreads();
     }
   }
-  // core -> out (prior off: r = max(q, r_min); degenerate: unchanged)
   for (int idx = tid; idx < T * (T / 2); idx += kSThreads) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
-    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
+    const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
     float2 v = make_float2(rs[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)], rs[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
     if (!A.r_prior && !degenerate) {
-      const float2 qv = *reinterpret_cast<const float2 *>(A.q + g);
+      const float2 qv = *reinterpret_cast<const float2 *>(A.q + gidx);
       v = make_float2(fmaxf(qv.x, A.r_min), fmaxf(qv.y, A.r_min));
     }
-    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
-    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
-  }
-}
-
-template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_ricd(StepArgs A) {
-  ricd_body<N>(A, blockIdx.x, blockIdx.y, blockIdx.z);
-}
-
-// S3 + S4 as one launch (one r-ICD sweep): the two are independent (R12), so
-// interleaving their CTAs (even: an r-ICD tile, odd: a row slab) puts the
-// MUFU/FMA-bound tiles and the memory-bound inverse row DFTs on the same SMs.
-template <int N>
-__global__ void __launch_bounds__(kSThreads, 4) ks_mix34(StepArgs A) {
-  constexpr int T = N < kTile ? N : kTile, NTI = (N / T) * (N / T), NRS = N / SCfg<N>::H;
-  const int n3 = NTI * A.sc, n4 = NRS * A.sc, m = n3 < n4 ? n3 : n4;
-  const int b = blockIdx.x;
-  int kind, idx;
-  if (b < 2 * m) {
-    kind = b & 1;
-    idx = b >> 1;
-  } else {
-    kind = n3 > n4 ? 0 : 1;
-    idx = m + (b - 2 * m);
-  }
-  if (kind == 0) {
-    const int s = idx / NTI, r = idx - s * NTI;
-    ricd_body<N>(A, r % (N / T), r / (N / T), s);
-  } else {
-    rows_inv_body<N>(A, idx % NRS, idx / NRS);
+    *reinterpret_cast<float2 *>(A.icd_out + gidx) = v;
+    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + gidx) = v;
   }
 }
 
@@ -612,273 +550,6 @@ __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
   phiicd_body<N>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
 }
 
-// S3 + S5 as one launch: the r M-step (after S2) and the phi M-step (after S4)
-// are independent (R12); interleaving their 64x64 tiles (even CTA: r, odd: phi)
-// mixes the MUFU-bound r tiles with the lighter phi tiles on every SM.
-// r: A.icd_in/out/copy; phi: A.icd2_in/out/copy.
-template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_mix35(StepArgs A) {
-  constexpr int T = N < kTile ? N : kTile, TPS = (N / T) * (N / T);
-  const int idx = blockIdx.x >> 1, s = idx / TPS, r = idx - s * TPS;
-  if (blockIdx.x & 1)
-    phiicd_body<N>(A, r % (N / T), r / (N / T), s, A.icd2_in, A.icd2_out, A.icd2_copy);
-  else
-    ricd_body<N>(A, r % (N / T), r / (N / T), s);
-}
-
-
-// ------------------------------------------- pipelined persistent ICD tiles
-//
-// Same sweep as ks_ricd / ks_phiicd, but each CTA loops over tiles and
-// double-buffers them: while it computes the 4 colour phases of tile k, the
-// 16-byte cp.async copies of tile k+1 (and L2 prefetches of its q or c/theta)
-// are in flight, so the memory time of one tile hides under the compute of
-// the previous one.  Plain row-major tile [kReg][kRP] (2-way bank conflicts on
-// the stride-2 colour accesses, in exchange for 5 copy instructions per thread).
-namespace {
-constexpr int kRP = kReg + 4;            // tile pitch in floats (16-byte rows)
-constexpr int kTileF = kReg * kRP;       // floats per tile stage
-constexpr int kChunks = kReg * kReg / 4; // 16-byte chunks per tile (18 per row)
-
-// Issue the copies of the tile (i0, j0) of field `src` into `dst`; periodic or
-// free (zero-filled outside the frame) boundary.
-template <int N, bool PERIODIC>
-__device__ __forceinline__ void tile_copy_async(float *dst, const float *__restrict__ src, int i0, int j0, int tid) {
-  for (int idx = tid; idx < kChunks; idx += kSThreads) {
-    const int row = idx / (kReg / 4), ch = idx - row * (kReg / 4);
-    int gi = i0 - kHalo + row, gj = j0 - kHalo + 4 * ch;
-    bool in = true;
-    if (PERIODIC) {
-      gi &= N - 1;
-      gj &= N - 1;
-    } else {
-      in = gi >= 0 && gi < N && gj >= 0 && gj < N;  // chunks are wholly inside or outside
-    }
-    const float *g = src + (in ? (size_t)gi * N + gj : 0);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((unsigned)__cvta_generic_to_shared(dst + row * kRP + 4 * ch)),
-                 "l"(g), "r"(in ? 16 : 0));
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void tile_prefetch_l2(const float *__restrict__ src, int i0, int j0, int tid) {
-  // rows of the 72-wide region (3 x 128-byte lines each, periodic rows)
-  for (int idx = tid; idx < kReg * 3; idx += kSThreads) {
-    const int row = idx / 3, k = idx - row * 3;
-    const int gi = (i0 - kHalo + row) & (N - 1), gj = (j0 - kHalo + 32 * k) & (N - 1);
-    prefetch_l2(src + (size_t)gi * N + gj);
-  }
-}
-
-// Pixels of colour C in phase C (plain tile), lanes on sub-columns, warps on rows.
-template <int C, class F>
-__device__ __forceinline__ void for_colour_p(int tid, F &&f) {
-  constexpr int ci = C >> 1, cj = C & 1, NW = kSThreads / 32;
-  constexpr int alo = sub_lo(C + 1, ci), ahi = sub_lo(kReg - C - 1, ci);
-  constexpr int blo = sub_lo(C + 1, cj), bhi = sub_lo(kReg - C - 1, cj);
-  constexpr int na = ahi - alo, nb = bhi - blo;
-  const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-  for (int k = 0; k < (na + NW - 1) / NW; ++k) {
-    const int a = alo + warp + NW * k;
-    if (a < ahi) f(2 * a + ci, 2 * (blo + lane) + cj);
-  }
-  if constexpr (nb > 32) {
-    constexpr int tc = nb - 32;
-    const int p = tid;
-    if (p < tc * na) f(2 * (alo + p / tc) + ci, 2 * (blo + 32 + p % tc) + cj);
-  }
-}
-}  // namespace
-
-template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_ricd_p(StepArgs A) {
-  constexpr int T = N < kTile ? N : kTile, P = N * N, TPS = (N / T) * (N / T);
-  extern __shared__ float icd_sm[];
-  const int tid = threadIdx.x;
-  const int ntiles = TPS * A.sc;
-  DDH_PDL_TRIGGER();
-  DDH_PDL_WAIT();
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
-  auto tile_of = [&](int tt, int &s, int &i0, int &j0) {
-    s = tt / TPS;
-    const int r = tt - s * TPS;
-    i0 = (r / (N / T)) * T;
-    j0 = (r % (N / T)) * T;
-  };
-  {
-    int s, i0, j0;
-    tile_of(t, s, i0, j0);
-    tile_copy_async<N, true>(icd_sm, A.icd_in + (size_t)s * P, i0, j0, tid);
-    tile_prefetch_l2<N>(A.q + (size_t)s * P, i0, j0, tid);
-  }
-  const float h = A.r_h, g = A.r_g, kq = A.r_k, b6 = A.r_b6, rmin = A.r_min;
-  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
-    float *rs = icd_sm + (k & 1) * kTileF;
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) {  // next tile -> the other stage
-      int s, i0, j0;
-      tile_of(tn, s, i0, j0);
-      tile_copy_async<N, true>(icd_sm + ((k + 1) & 1) * kTileF, A.icd_in + (size_t)s * P, i0, j0, tid);
-      tile_prefetch_l2<N>(A.q + (size_t)s * P, i0, j0, tid);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    int s, i0, j0;
-    tile_of(t, s, i0, j0);
-    const size_t off = (size_t)s * P;
-    const float *__restrict__ qin = A.q + off;
-    const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
-    if (A.r_prior && !degenerate) {
-      auto phase = [&](auto cc) {
-        constexpr int C = decltype(cc)::value;
-        for_colour_p<C>(tid, [&](int li, int lj) {
-          const int me = li * kRP + lj;
-          const float ri = rs[me];
-          const float q = __ldg(qin + (size_t)((i0 - kHalo + li) & (N - 1)) * N + ((j0 - kHalo + lj) & (N - 1)));
-          const float2 nA = make_float2(rs[me - kRP], rs[me + kRP]);
-          const float2 nB = make_float2(rs[me - 1], rs[me + 1]);
-          const float2 dA = make_float2(rs[me - kRP - 1], rs[me - kRP + 1]);
-          const float2 dB = make_float2(rs[me + kRP - 1], rs[me + kRP + 1]);
-          const float2 wA = qgg_w2(ri, nA, h, g, kq), wB = qgg_w2(ri, nB, h, g, kq);
-          const float2 wC = qgg_w2(ri, dA, h, g, kq), wD = qgg_w2(ri, dB, h, g, kq);
-          const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
-          const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
-          rs[me] = r_update(ri, q, b6 * (bs.x + bs.y), b6 * (ss.x + ss.y), rmin);
-        });
-        __syncthreads();
-      };
-      phase(std::integral_constant<int, 0>());
-      phase(std::integral_constant<int, 1>());
-      phase(std::integral_constant<int, 2>());
-      phase(std::integral_constant<int, 3>());
-    }
-    // core -> out (prior off: r = max(q, r_min); degenerate: unchanged)
-    for (int idx = tid; idx < T * (T / 4); idx += kSThreads) {
-      const int oi = idx / (T / 4), c4 = idx - oi * (T / 4);
-      const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 4 * c4);
-      float4 v = *reinterpret_cast<const float4 *>(rs + (oi + kHalo) * kRP + kHalo + 4 * c4);
-      if (!A.r_prior && !degenerate) {
-        const float4 qv = *reinterpret_cast<const float4 *>(A.q + gidx);
-        v = make_float4(fmaxf(qv.x, rmin), fmaxf(qv.y, rmin), fmaxf(qv.z, rmin), fmaxf(qv.w, rmin));
-      }
-      *reinterpret_cast<float4 *>(A.icd_out + gidx) = v;
-      if (A.icd_copy) *reinterpret_cast<float4 *>(A.icd_copy + gidx) = v;
-    }
-    __syncthreads();  // stage k&1 is refilled by the prefetch of the next iteration
-  }
-}
-
-template <int N>
-__global__ void __launch_bounds__(kSThreads) ks_phiicd_p(StepArgs A) {
-  constexpr int T = N < kTile ? N : kTile, P = N * N, TPS = (N / T) * (N / T);
-  extern __shared__ float icd_sm[];
-  const int tid = threadIdx.x;
-  const int ntiles = TPS * A.sc;
-  DDH_PDL_TRIGGER();
-  DDH_PDL_WAIT();
-  int t = blockIdx.x;
-  if (t >= ntiles) return;
-  auto tile_of = [&](int tt, int &s, int &i0, int &j0) {
-    s = tt / TPS;
-    const int r = tt - s * TPS;
-    i0 = (r / (N / T)) * T;
-    j0 = (r % (N / T)) * T;
-  };
-  auto prefetch_ct = [&](int s, int i0, int j0) {
-    tile_prefetch_l2<N>(A.cc + (size_t)s * P, i0, j0, tid);
-    tile_prefetch_l2<N>(A.theta + (size_t)s * P, i0, j0, tid);
-  };
-  {
-    int s, i0, j0;
-    tile_of(t, s, i0, j0);
-    tile_copy_async<N, false>(icd_sm, A.icd_in + (size_t)s * P, i0, j0, tid);
-    prefetch_ct(s, i0, j0);
-  }
-  const bool prior = A.phi_prior != 0;
-  const float w = A.phi_w;
-  for (int k = 0; t < ntiles; ++k, t += gridDim.x) {
-    float *ps = icd_sm + (k & 1) * kTileF;
-    const int tn = t + gridDim.x;
-    if (tn < ntiles) {
-      int s, i0, j0;
-      tile_of(tn, s, i0, j0);
-      tile_copy_async<N, false>(icd_sm + ((k + 1) & 1) * kTileF, A.icd_in + (size_t)s * P, i0, j0, tid);
-      prefetch_ct(s, i0, j0);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    int s, i0, j0;
-    tile_of(t, s, i0, j0);
-    const size_t off = (size_t)s * P;
-    double sums[5], cpl[3] = {0, 0, 0};
-    sum_part0(A.part0, A.nb0, s, sums);
-    const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
-    if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
-    __syncthreads();
-    if (cpl[0] != 0.0 || cpl[1] != 0.0 || cpl[2] != 0.0) {  // phi' = phi - plane (first sweep of a step)
-      const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
-      for (int idx = tid; idx < kChunks; idx += kSThreads) {
-        const int row = idx / (kReg / 4), ch = idx - row * (kReg / 4);
-        const int gi = i0 - kHalo + row, gj = j0 - kHalo + 4 * ch;
-        if (gi >= 0 && gi < N && gj >= 0 && gj < N) {
-          float4 *p4 = reinterpret_cast<float4 *>(ps + row * kRP + 4 * ch);
-          float4 v = *p4;
-          const float pl = c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2);
-          v.x -= pl;
-          v.y -= pl + c1;
-          v.z -= pl + 2.f * c1;
-          v.w -= pl + 3.f * c1;
-          *p4 = v;
-        }
-      }
-      __syncthreads();
-    }
-    if (!degenerate) {
-      const bool edge = i0 == 0 || j0 == 0 || i0 + T == N || j0 + T == N;
-      const float *__restrict__ ccs = A.cc + off;
-      const float *__restrict__ ths = A.theta + off;
-      auto phase = [&](auto cc) {
-        constexpr int C = decltype(cc)::value;
-        for_colour_p<C>(tid, [&](int li, int lj) {
-          const int gi = i0 - kHalo + li, gj = j0 - kHalo + lj;
-          float sb = 1.f;  // sum of b over the existing neighbours (free boundary)
-          if (edge) {
-            if (gi < 0 || gi >= N || gj < 0 || gj >= N) return;  // outside the frame: absent
-            const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
-            sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
-                 (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
-          }
-          const int me = li * kRP + lj;
-          const size_t gg = (size_t)gi * N + gj;
-          const float cv = __ldg(ccs + gg), tv = __ldg(ths + gg);
-          const float n4 = (ps[me - kRP] + ps[me + kRP]) + (ps[me - 1] + ps[me + 1]);
-          const float nd = (ps[me - kRP - 1] + ps[me - kRP + 1]) + (ps[me + kRP - 1] + ps[me + kRP + 1]);
-          ps[me] = phi_update(ps[me], cv, tv, fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f)), sb, w, prior);
-        });
-        __syncthreads();
-      };
-      phase(std::integral_constant<int, 0>());
-      phase(std::integral_constant<int, 1>());
-      phase(std::integral_constant<int, 2>());
-      phase(std::integral_constant<int, 3>());
-    }
-    for (int idx = tid; idx < T * (T / 4); idx += kSThreads) {
-      const int oi = idx / (T / 4), c4 = idx - oi * (T / 4);
-      const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 4 * c4);
-      const float4 v = degenerate ? *reinterpret_cast<const float4 *>(A.icd_in + gidx)
-                                  : *reinterpret_cast<const float4 *>(ps + (oi + kHalo) * kRP + kHalo + 4 * c4);
-      *reinterpret_cast<float4 *>(A.icd_out + gidx) = v;
-      if (A.icd_copy) *reinterpret_cast<float4 *>(A.icd_copy + gidx) = v;
-    }
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------- launchers
 
 #define DDH_SDISPATCH(n, CALL)                          \
@@ -896,19 +567,12 @@ template <int N> static size_t srowi_smem() { return srow_smem<N>() + (size_t)SC
 template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t)N * SCfg<N>::W * sizeof(float2); }
 
 template <int N>
-static void init_icdp();
-
-template <int N>
 static cudaError_t init_stream_n() {
-  init_icdp<N>();
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
-  cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
-  cudaFuncSetAttribute(ks_mix34<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(srowi_smem<N>() > 2 * kIcdGrid * sizeof(float) ? srowi_smem<N>() : 2 * kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
-  cudaFuncSetAttribute(ks_mix35<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
   return cudaGetLastError();
 }
 
@@ -941,60 +605,13 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a));
 }
-cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
-  DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  return launch_pdl(ks_ricd<N>, dim3(N / T, N / T, a.sc), dim3(kSThreads), 2 * kIcdGrid * sizeof(float), st, a);
-                }));
-}
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
 }
-static int g_icdp_grid[2][11];  // persistent grid of ks_ricd_p / ks_phiicd_p per log2 N
-
-template <int N>
-static void init_icdp() {
-  const int l = 31 - __builtin_clz(N);
-  int dev = 0, sms = 148, nb = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(ks_ricd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kTileF * sizeof(float)));
-  cudaFuncSetAttribute(ks_phiicd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kTileF * sizeof(float)));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks_ricd_p<N>, kSThreads, 2 * kTileF * sizeof(float));
-  g_icdp_grid[0][l] = sms * (nb > 0 ? nb : 1);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks_phiicd_p<N>, kSThreads, 2 * kTileF * sizeof(float));
-  g_icdp_grid[1][l] = sms * (nb > 0 ? nb : 1);
-}
-
-cudaError_t launch_s3p(const StepArgs &a, cudaStream_t st) {
+cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
                   constexpr int T = N < kTile ? N : kTile;
-                  const int nt = (N / T) * (N / T) * a.sc, gp = g_icdp_grid[0][31 - __builtin_clz(N)];
-                  return launch_pdl(ks_ricd_p<N>, dim3(nt < gp ? nt : gp), dim3(kSThreads), 2 * kTileF * sizeof(float), st, a);
-                }));
-}
-cudaError_t launch_s5p(const StepArgs &a, cudaStream_t st) {
-  DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  const int nt = (N / T) * (N / T) * a.sc, gp = g_icdp_grid[1][31 - __builtin_clz(N)];
-                  return launch_pdl(ks_phiicd_p<N>, dim3(nt < gp ? nt : gp), dim3(kSThreads), 2 * kTileF * sizeof(float), st, a);
-                }));
-}
-
-cudaError_t launch_s35(const StepArgs &a, cudaStream_t st) {
-  DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  return launch_pdl(ks_mix35<N>, dim3(2 * (N / T) * (N / T) * a.sc), dim3(kSThreads),
-                                    2 * kIcdGrid * sizeof(float), st, a);
-                }));
-}
-
-cudaError_t launch_s34(const StepArgs &a, cudaStream_t st) {
-  DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  const int nb = ((N / T) * (N / T) + N / SCfg<N>::H) * a.sc;
-                  const size_t sm = srowi_smem<N>() > 2 * kIcdGrid * sizeof(float) ? srowi_smem<N>() : 2 * kIcdGrid * sizeof(float);
-                  return launch_pdl(ks_mix34<N>, dim3(nb), dim3(kSThreads), sm, st, a);
+                  return launch_pdl(ks_ricd<N>, dim3(N / T, N / T, a.sc), dim3(kSThreads), kIcdGrid * sizeof(float), st, a);
                 }));
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {

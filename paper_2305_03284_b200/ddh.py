@@ -54,7 +54,7 @@ EXPORTS = [
     "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_ricd", "ddh_test_phiicd",
     "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
 ]
-KIND_COUNT = 20
+KIND_COUNT = 17
 
 _lib = None
 
