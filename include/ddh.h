@@ -204,6 +204,37 @@ ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t 
 ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta,
                            int32_t B, float *phi_out);
 
+/* ---- on-device frame synthesiser (input generation) ----
+ * Synthetic DH frame sequences of the BASELINE recipe: blurred
+ * uniform reflectance r (R23), FFT-method Kolmogorov screen on a periodic 2N x 2N
+ * grid moved by frozen flow (Fourier shift, R22/R24) with piston/tip/tilt removed
+ * over the aperture, fresh speckle g = sqrt(r/2)(z1 + j z2) per frame
+ * (R21), complex AWGN sigma_n^2 = mean(r)/10^{SNR/10} (R20),
+ * y = a e^{j phi} F_c^{-1}(g) + w (Eq. 1).  Philox-4x32-10 counters keyed by
+ * (pixel, frame, stream, purpose) and `seed`: deterministic, independent of
+ * the batching of frames.  Not the estimator: no part of the DDH-MBIR update. */
+typedef struct ddh_synth ddh_synth; /* opaque */
+
+/* n in {64,128,256,512}; aperture: circle of diameter `diam` px strictly inside,
+ * centre (n/2, n/2); d_r0: host [streams] turbulence strengths D/r0 (0: no
+ * turbulence); velocity: host [streams][2] frozen-flow velocity (rows, cols) in
+ * px/frame; sigma_b: reflectance blur (px, > 0); snr_db: per-pixel SNR in dB.
+ * Synchronous setup on cuda_stream.  Errors: DDH_E_INVAL, DDH_E_NOMEM, DDH_E_CUDA. */
+ddh_status ddh_synth_create(int32_t n, float diam, int32_t streams, const double *d_r0,
+                            const double *velocity, double sigma_b, double snr_db, uint64_t seed,
+                            void *cuda_stream, ddh_synth **out);
+
+/* Frames t0 .. t0+T-1 of every stream: y device complex64 [T][S][n][n]; phi
+ * device float32 [T][S][n][n] (the true, plane-removed phase) or NULL.
+ * Asynchronous on the synthesiser's stream.  Errors: DDH_E_INVAL, DDH_E_CUDA. */
+ddh_status ddh_synth_frames(ddh_synth *z, int64_t t0, int32_t T, void *y, float *phi);
+
+/* The true reflectance r: device float32 [S][n][n]. */
+ddh_status ddh_synth_reflectance(ddh_synth *z, float *r);
+
+/* Free a synthesiser (synchronises its stream first). */
+ddh_status ddh_synth_destroy(ddh_synth *z);
+
 #ifdef __cplusplus
 }
 #endif

@@ -302,9 +302,9 @@ __device__ __forceinline__ void phase_b(const StepArgs &A, const int s, const in
           rS[i * RP] = left[src * RP + W];
           rS[i * RP + W + 1] = right[src * RP + 1];
         }
-        for (int c = tid; c < W; c += NT) {
-          rS[c + 1] = rS[N * RP + c + 1];
-          rS[(N + 1) * RP + c + 1] = rS[RP + c + 1];
+        for (int w = tid; w < W; w += NT) {
+          rS[w + 1] = rS[N * RP + w + 1];
+          rS[(N + 1) * RP + w + 1] = rS[RP + w + 1];
         }
         DDH_SYNC_T(__syncthreads());
         const int ci = c >> 1, cj = c & 1;

@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   extern __shared__ float4 smem4[];
   float4 *tw = smem4;                                   // [N]
   float2 *buf = reinterpret_cast<float2 *>(smem4 + N);  // [N][W]
-  __shared__ double st[1];
   const int tid = threadIdx.x, s = blockIdx.y;
   const int b = tid % W, t = tid / W;
   const int col = blockIdx.x * W + b;

@@ -53,6 +53,7 @@ EXPORTS = [
     "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_sync", "ddh_last_error",
     "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_ricd", "ddh_test_phiicd",
     "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
+    "ddh_synth_create", "ddh_synth_frames", "ddh_synth_reflectance", "ddh_synth_destroy",
 ]
 KIND_COUNT = 17
 
@@ -93,6 +94,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.ddh_profile_read.argtypes = [vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)]
     lib.ddh_kind_name.argtypes = [i32]
     lib.ddh_kind_name.restype = ctypes.c_char_p
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib.ddh_synth_create.argtypes = [i32, ctypes.c_float, i32, dp, dp, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_uint64, vp, ctypes.POINTER(vp)]
+    lib.ddh_synth_frames.argtypes = [vp, i64, i32, vp, vp]
+    lib.ddh_synth_reflectance.argtypes = [vp, vp]
+    lib.ddh_synth_destroy.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("ddh_last_error", "ddh_kernel_launches", "ddh_frame_index", "ddh_kind_name"):
             getattr(lib, name).restype = ctypes.c_int
@@ -289,3 +296,53 @@ class DDH:
         out = torch.empty_like(phi_in)
         _check(self.lib.ddh_test_phiicd(self.h, a, b, t, B, ctypes.c_void_p(out.data_ptr())), self.h)
         return out
+
+
+class DDHSynth:
+    """On-device frame synthesiser (libddh ddh_synth_*): the
+    BASELINE recipe with its own counter-based generator.  Input generation
+    only.  d_r0: per-stream D/r0 (scalar or sequence); velocity: per-stream
+    (rows, cols) px/frame (pair or sequence of pairs)."""
+
+    def __init__(self, n: int, streams: int, d_r0, velocity, sigma_b: float, snr_db: float,
+                 diam: float = None, seed: int = 20230504, device: int = 0):
+        import numpy as np
+        import torch
+        self.lib = load_library()
+        self.n, self.S = n, streams
+        self.device = torch.device("cuda", device)
+        self.stream = torch.cuda.current_stream(self.device)
+        dr = np.broadcast_to(np.asarray(d_r0, np.float64), (streams,)).copy()
+        v = np.broadcast_to(np.asarray(velocity, np.float64).reshape(-1, 2), (streams, 2)).copy()
+        h = ctypes.c_void_p()
+        dp = ctypes.POINTER(ctypes.c_double)
+        st = self.lib.ddh_synth_create(int(n), float(n if diam is None else diam), int(streams),
+                                       dr.ctypes.data_as(dp), v.ctypes.data_as(dp), float(sigma_b), float(snr_db),
+                                       int(seed), ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h))
+        if st != 0:
+            raise DDHError(f"ddh_synth_create failed with status {st}")
+        self.h = h
+
+    def frames(self, t0: int, T: int, want_phi: bool = True):
+        import torch
+        y = torch.empty((T, self.S, self.n, self.n), dtype=torch.complex64, device=self.device)
+        phi = torch.empty((T, self.S, self.n, self.n), dtype=torch.float32, device=self.device) if want_phi else None
+        st = self.lib.ddh_synth_frames(self.h, int(t0), int(T), ctypes.c_void_p(y.data_ptr()),
+                                       ctypes.c_void_p(phi.data_ptr()) if phi is not None else None)
+        if st != 0:
+            raise DDHError(f"ddh_synth_frames failed with status {st}")
+        return y, phi
+
+    def reflectance(self):
+        import torch
+        r = torch.empty((self.S, self.n, self.n), dtype=torch.float32, device=self.device)
+        st = self.lib.ddh_synth_reflectance(self.h, ctypes.c_void_p(r.data_ptr()))
+        if st != 0:
+            raise DDHError(f"ddh_synth_reflectance failed with status {st}")
+        return r
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.lib.ddh_synth_destroy(h)
+            self.h = None

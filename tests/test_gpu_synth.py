@@ -1,0 +1,100 @@
+"""On-device frame synthesiser (libddh ddh_synth_*) against the
+laws of DESIGN.md 5 that the host synthesiser is pinned to: the exact discrete
+Kolmogorov structure function (R22), frozen flow (R24), speckle and noise
+power (R20/R21), the reflectance recipe (R23), counter-based determinism, and
+the north-star pin "phi ~ 0 and Strehl ~ 1 with zero turbulence at high SNR"
+through the GPU estimator."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from paper_2305_03284_b200 import DDH, DDHSynth
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def test_structure_function_matches_discrete_kolmogorov():
+    n, S = 128, 96
+    z = DDHSynth(n, S, d_r0=10.0, velocity=(0.0, 0.0), sigma_b=2.0, snr_db=10.0)
+    _, phi = z.frames(0, 1)
+    torch.cuda.synchronize()
+    ph = phi[0].double().cpu().numpy()  # [S][n][n], plane-removed
+    a = synth.sim.aperture_mask(n, n) > 0
+    r0 = n / 10.0
+    for d in ((0, 1), (1, 0), (0, 3), (2, 2)):
+        sh = np.roll(np.roll(ph, -d[0], 1), -d[1], 2)
+        m = a & np.roll(np.roll(a, -d[0], 0), -d[1], 1)
+        emp = float(np.mean(((sh - ph) ** 2)[:, m]))
+        exp = synth.sim.structure_function_expected(2 * n, 2 * n, r0, d)
+        # this estimator (plane-removed, aperture pairs, 96 screens) gives ratios 0.95-1.08 on
+        # the device screens and 0.96-1.04 on the host synthesiser's (synth.make_stream)
+        assert 0.9 * exp < emp < 1.12 * exp, (d, emp, exp)
+
+
+def test_frozen_flow_integer_shift():
+    n, S = 64, 2
+    z = DDHSynth(n, S, d_r0=8.0, velocity=(0.0, 1.0), sigma_b=2.0, snr_db=10.0)
+    _, phi = z.frames(0, 3)
+    p = phi.double().cpu().numpy()
+    # second differences are invariant to the removed plane; frame t+1 is frame t moved by +1 column
+    d2 = lambda f: f[..., 1:-1, 2:] - 2 * f[..., 1:-1, 1:-1] + f[..., 1:-1, :-2]
+    for t in range(2):
+        a, b = d2(p[t])[..., :-1], d2(p[t + 1])[..., 1:]
+        assert np.max(np.abs(a - b)) < 2e-3, np.max(np.abs(a - b))
+
+
+def test_speckle_and_noise_power():
+    n, S, T = 128, 8, 4
+    snr = 5.0
+    z = DDHSynth(n, S, d_r0=10.0, velocity=(0.3, 0.7), sigma_b=3.0, snr_db=snr)
+    y, _ = z.frames(0, T, want_phi=False)
+    r = z.reflectance().double().cpu().numpy()
+    p = (y.abs() ** 2).double().cpu().numpy()
+    a = synth.sim.aperture_mask(n, n) > 0
+    for s in range(S):
+        s2 = r[s].mean() / 10 ** (snr / 10)
+        inside = p[:, s][:, a].mean()
+        outside = p[:, s][:, ~a].mean()
+        assert abs(outside / s2 - 1) < 0.05, (outside, s2)
+        assert abs(inside / (r[s].mean() + s2) - 1) < 0.03, (inside, r[s].mean() + s2)
+
+
+def test_reflectance_recipe():
+    n, S = 128, 4
+    z = DDHSynth(n, S, d_r0=10.0, velocity=(0.0, 1.0), sigma_b=3.0, snr_db=10.0)
+    r = z.reflectance().cpu().numpy()
+    assert r.min() >= 1e-4 - 1e-9 and abs(r.max() - 1.0) < 1e-6
+    for s in range(S):
+        assert 0.3 < r[s].mean() < 0.7
+        # blurred: neighbouring pixels strongly correlated (sigma 3 px)
+        c = np.corrcoef(r[s][:, :-1].ravel(), r[s][:, 1:].ravel())[0, 1]
+        assert c > 0.9, c
+
+
+def test_counter_based_determinism():
+    n, S = 64, 3
+    z = DDHSynth(n, S, d_r0=12.0, velocity=(0.25, -0.5), sigma_b=2.0, snr_db=10.0, seed=7)
+    y5, p5 = z.frames(0, 5)
+    y2, p2 = z.frames(3, 2)
+    assert torch.equal(y5[3:], y2) and torch.equal(p5[3:], p2)
+    z2 = DDHSynth(n, S, d_r0=12.0, velocity=(0.25, -0.5), sigma_b=2.0, snr_db=10.0, seed=8)
+    y8, _ = z2.frames(0, 1)
+    assert not torch.equal(y8[0], y5[0])
+
+
+def test_zero_turbulence_high_snr_gives_strehl_one():
+    """north_star pin: with no turbulence and high SNR the estimator returns
+    phi ~ 0 (piston/tip/tilt aside) and Strehl ~ 1."""
+    n, S = 64, 2
+    z = DDHSynth(n, S, d_r0=0.0, velocity=(0.0, 0.0), sigma_b=2.0, snr_db=40.0)
+    y, phi = z.frames(0, 4)
+    assert float(phi.abs().max()) == 0.0
+    nv = synth.recon_noise_var(n, n, 40.0)
+    ctx = DDH(n, S, noise_var=nv)
+    ctx.bootstrap(y[0].contiguous(), 10)
+    po = torch.empty((3, S, n, n), device=DEV)
+    ctx.step(y[1:].contiguous(), po)
+    st = ctx.strehl(po[-1], phi[-1])
+    assert min(st) > 0.98, st
