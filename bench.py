@@ -233,13 +233,18 @@ def run_ours(args):
     # ---- weak scaling: cfg["streams"] streams per GPU; rank r owns global
     # streams [first, first + S) (sched.shard of S * ws streams), seeds per stream
     first, S = sched.shard(cfg["streams"] * ws, ws, rank)
-    t0 = time.time()
-    y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=first, want_phi=False)
-    gen_s = time.time() - t0
     ws, rank, local = dist_setup("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    y_dev = torch.from_numpy(y_host).to(dev)
+    t0 = time.time()
+    if args.synth == "device":  # on-device synthesiser (libddh ddh_synth_*), same recipe as synth/
+        y_dev = device_frames(cfg, S, F, first, local)
+        torch.cuda.synchronize()
+        y_host = y_dev.cpu().numpy()
+    else:
+        y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=first, want_phi=False)
+        y_dev = torch.from_numpy(y_host).to(dev)
+    gen_s = time.time() - t0
     stream = torch.cuda.current_stream(dev)
     extra = {}
     if args.priors_off:  # diagnostic only (isolates the ICD cost); never the reported configuration
@@ -346,7 +351,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": dict(workload_config(cfg), parallelism=f"streams x{ws} GPUs",
-                                                           lanes=lanes, path=args.path,
+                                                           lanes=lanes, path=args.path, synth=args.synth,
                                                            synth_seconds=round(gen_s, 1)),
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks,
         "attribution_pass": {"value": frames_total / (ms_attr * 1e-3), "ms_per_step": ms_attr / K, "lanes": 1,
@@ -373,6 +378,31 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     del ctx
     return 0
+
+
+def device_frames(cfg, S, F, first, local):
+    """Frames of config `cfg` for global streams [first, first+S) from the
+    on-device synthesiser: per-stream D/r0 and flow direction drawn like
+    synth/ (uniform D/r0 range, uniform direction for "random")."""
+    import math
+
+    from paper_2305_03284_b200 import DDHSynth
+    d_r0, vel = [], []
+    for k in range(first, first + S):
+        g = np.random.default_rng([20230504, k])
+        lo_hi = cfg.get("d_r0_range")
+        d_r0.append(lo_hi[0] + (lo_hi[1] - lo_hi[0]) * g.random() if lo_hi else cfg["d_r0"])
+        if cfg["direction"] == "random":
+            th = 2 * math.pi * g.random()
+        elif cfg["direction"] == "angle":
+            th = cfg["angle"]
+        else:
+            th = math.pi / 2  # along +columns
+        vel.append((cfg["flow"] * math.sin(th), cfg["flow"] * math.cos(th)))
+    z = DDHSynth(cfg["n"], S, d_r0=d_r0, velocity=vel, sigma_b=cfg["sigma_b"], snr_db=cfg["snr_db"],
+                 diam=cfg["diam"], seed=20230504 + first, device=local)
+    y, _ = z.frames(0, F, want_phi=False)
+    return y
 
 
 def ctx_lanes(ctx):
@@ -495,6 +525,8 @@ def main():
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--priors-off", action="store_true", help="diagnostic: disable both priors")
     ap.add_argument("--unfused", action="store_true", help="diagnostic: multi-pass kernels (= --path multipass)")
+    ap.add_argument("--synth", choices=["device", "host"], default="device",
+                    help="frame generator: the on-device synthesiser (default) or synth/ on the host")
     ap.add_argument("--serial", action="store_true",
                     help="profiling aid: DDH_F_SERIAL for the main ctx too (the launch configuration of the "
                          "attribution pass, for ncu captures)")
