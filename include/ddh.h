@@ -58,6 +58,9 @@ typedef enum {
                                default: the streaming 6-kernel iteration          */
 #define DDH_F_SERIAL 8u     /* enqueue every kernel on the ctx stream in order (no
                                lanes, no side stream): per-kernel event timing     */
+#define DDH_F_NO_GRAPHS 16u /* never replay a recurring single-frame ddh_step from a
+                               captured CUDA graph (default: a call with the same
+                               frame/output pointers seen twice is captured once)  */
 
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 

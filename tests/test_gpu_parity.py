@@ -466,3 +466,28 @@ def test_fused_and_unfused_paths_agree():
             for s in range(S):
                 assert phi_err(o[0][t, s], outs[0][0][t, s].astype(np.float64), a) < 1e-3
                 assert np.linalg.norm(o[1][t, s] - outs[0][1][t, s]) / np.linalg.norm(outs[0][1][t, s]) < 1e-3
+
+
+@pytest.mark.parametrize("flags", [0, 4])
+def test_graph_replay_bit_exact(flags):
+    """A recurring single-frame call (fixed frame and output buffers) is
+    captured into a CUDA graph on its second occurrence and replayed; results
+    equal the launch-by-launch path bit for bit (phi ping-pong included)."""
+    n, S, T = 128, 2, 6
+    y, _, _ = frames(n, S, T)
+    yt = torch.from_numpy(y).to(DEV)
+    ctxs = [DDH(n, S, noise_var=0.1, flags=flags), DDH(n, S, noise_var=0.1, flags=flags | 16)]
+    bufs = [torch.empty((1, S, n, n), dtype=torch.complex64, device=DEV) for _ in ctxs]
+    outs = [(torch.empty((1, S, n, n), device=DEV), torch.empty((1, S, n, n), device=DEV)) for _ in ctxs]
+    for t in range(T):
+        res = []
+        for c, b, (po, ro) in zip(ctxs, bufs, outs):
+            b.copy_(yt[t:t + 1])
+            c.step(b, po, ro)
+            res.append((po.clone(), ro.clone()))
+        torch.cuda.synchronize()
+        assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1]), t
+    r0, p0, f0 = ctxs[0].get_state()
+    r1, p1, f1 = ctxs[1].get_state()
+    assert torch.equal(r0, r1) and torch.equal(p0, p1) and f0 == f1 == T
+    assert ctxs[0].kernel_launches == ctxs[1].kernel_launches
