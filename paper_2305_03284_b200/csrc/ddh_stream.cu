@@ -354,19 +354,24 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_inv
 // ------------------------------------------------------------ ICD tiles
 
 namespace {
-constexpr int kTile = 64, kHalo = 4, kReg = kTile + 2 * kHalo, kSub = kReg / 2, kSubP = kSub + 1;
-constexpr int kIcdGrid = 4 * kSub * kSubP;  // floats per colour-separated tile
-// colour-separated tile: sub-grid c = 2 (i&1) + (j&1), element (i>>1, j>>1)
-__device__ __forceinline__ int sidx(int c, int a, int b) { return (c * kSub + a) * kSubP + b; }
-// neighbour (di, dj) of a pixel of colour (ci, cj) at sub coords (a, b):
-// colour ((ci+di)&1, (cj+dj)&1), sub coords (a + floor((ci+di)/2), b + floor((cj+dj)/2))
-template <int CI, int CJ, int DI, int DJ>
-__device__ __forceinline__ int nidx(int a, int b) {
-  constexpr int ti = CI + DI, tj = CJ + DJ;
-  constexpr int pi = ti & 1, pj = tj & 1;
-  constexpr int oa = (ti - pi) / 2, ob = (tj - pj) / 2;
-  return sidx(2 * pi + pj, a + oa, b + ob);
-}
+constexpr int kHalo = 4;  // = 4 colour phases x 1 sweep (R8)
+// Tile geometry: TILE x TILE core, region TILE + 2 kHalo, stored colour-separated:
+// sub-grid c = 2 (i&1) + (j&1), element (i>>1, j>>1).  64 for throughput, 32 when
+// a launch has too few 64-tiles to fill the SMs (single-stream latency).
+template <int TILE> struct Icd {
+  static constexpr int kReg = TILE + 2 * kHalo, kSub = kReg / 2, kSubP = kSub + 1;
+  static constexpr int kIcdGrid = 4 * kSub * kSubP;  // floats per colour-separated tile
+  static __device__ __forceinline__ int sidx(int c, int a, int b) { return (c * kSub + a) * kSubP + b; }
+  // neighbour (di, dj) of a pixel of colour (ci, cj) at sub coords (a, b):
+  // colour ((ci+di)&1, (cj+dj)&1), sub coords (a + floor((ci+di)/2), b + floor((cj+dj)/2))
+  template <int CI, int CJ, int DI, int DJ>
+  static __device__ __forceinline__ int nidx(int a, int b) {
+    constexpr int ti = CI + DI, tj = CJ + DJ;
+    constexpr int pi = ti & 1, pj = tj & 1;
+    constexpr int oa = (ti - pi) / 2, ob = (tj - pj) / 2;
+    return sidx(2 * pi + pj, a + oa, b + ob);
+  }
+};
 // sub-coordinate range of colour parity p updated in a phase covering local
 // rows [lo, hi): smallest a with 2a+p >= lo, first a with 2a+p >= hi
 __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 2; }
@@ -380,9 +385,10 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 // phases the 64x64 core equals the global colour-ordered sweep.  q is read
 // from global (L2) at the pixel's update and only r is staged (21 KB smem),
 // within 32 registers: 8 CTAs (64 warps) per SM.
-template <int N>
+template <int N, int TILE>
 __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
-  constexpr int T = N < kTile ? N : kTile, P = N * N;
+  using G = Icd<TILE>;
+  constexpr int T = N < TILE ? N : TILE, P = N * N;
   extern __shared__ float icd_sm[];
   float *rs = icd_sm;
   const int tid = threadIdx.x, s = blockIdx.z;
@@ -392,12 +398,12 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
   const float *__restrict__ qin = A.q + off;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
-  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
-    const int li = idx / kSub, pj = idx - li * kSub;
+  for (int idx = tid; idx < G::kReg * G::kSub; idx += kSThreads) {
+    const int li = idx / G::kSub, pj = idx - li * G::kSub;
     const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
     const float2 v = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
-    rs[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
-    rs[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
+    rs[G::sidx(2 * (li & 1), li >> 1, pj)] = v.x;
+    rs[G::sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
   }
   const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   __syncthreads();
@@ -406,19 +412,19 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int ci = c >> 1, cj = c & 1;
-      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(kReg - c - 1, ci);
-      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(kReg - c - 1, cj);
+      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(G::kReg - c - 1, ci);
+      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(G::kReg - c - 1, cj);
       const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
 #pragma unroll 1
       for (int p = tid; p < cnt; p += kSThreads) {
         const int a = alo + p / nbb, bb = blo + p % nbb;
         float ri, n0, n1, n2, n3, d0, d1, d2v, d3;
 #define DDH_NB(CI, CJ)                                                                       \
-  ri = rs[sidx(2 * CI + CJ, a, bb)];                                                          \
-  n0 = rs[nidx<CI, CJ, -1, 0>(a, bb)]; n1 = rs[nidx<CI, CJ, 1, 0>(a, bb)];                    \
-  n2 = rs[nidx<CI, CJ, 0, -1>(a, bb)]; n3 = rs[nidx<CI, CJ, 0, 1>(a, bb)];                    \
-  d0 = rs[nidx<CI, CJ, -1, -1>(a, bb)]; d1 = rs[nidx<CI, CJ, -1, 1>(a, bb)];                  \
-  d2v = rs[nidx<CI, CJ, 1, -1>(a, bb)]; d3 = rs[nidx<CI, CJ, 1, 1>(a, bb)];
+  ri = rs[G::sidx(2 * CI + CJ, a, bb)];                                                          \
+  n0 = rs[G::template nidx<CI, CJ, -1, 0>(a, bb)]; n1 = rs[G::template nidx<CI, CJ, 1, 0>(a, bb)];                    \
+  n2 = rs[G::template nidx<CI, CJ, 0, -1>(a, bb)]; n3 = rs[G::template nidx<CI, CJ, 0, 1>(a, bb)];                    \
+  d0 = rs[G::template nidx<CI, CJ, -1, -1>(a, bb)]; d1 = rs[G::template nidx<CI, CJ, -1, 1>(a, bb)];                  \
+  d2v = rs[G::template nidx<CI, CJ, 1, -1>(a, bb)]; d3 = rs[G::template nidx<CI, CJ, 1, 1>(a, bb)];
         if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
 #undef DDH_NB
         const int gi = (i0 - kHalo + 2 * a + ci) & (N - 1), gj = (j0 - kHalo + 2 * bb + cj) & (N - 1);
@@ -429,7 +435,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
         const float2 wC = qgg_w2(ri, dA, h, g, kq), wD = qgg_w2(ri, dB, h, g, kq);
         const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
         const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
-        rs[sidx(c, a, bb)] = r_update(ri, q, b6 * (bs.x + bs.y), b6 * (ss.x + ss.y), rmin);
+        rs[G::sidx(c, a, bb)] = r_update(ri, q, b6 * (bs.x + bs.y), b6 * (ss.x + ss.y), rmin);
       }
       __syncthreads();
     }
@@ -438,7 +444,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
     const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
-    float2 v = make_float2(rs[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)], rs[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
+    float2 v = make_float2(rs[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)], rs[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
     if (!A.r_prior && !degenerate) {
       const float2 qv = *reinterpret_cast<const float2 *>(A.q + gidx);
       v = make_float2(fmaxf(qv.x, A.r_min), fmaxf(qv.y, A.r_min));
@@ -452,10 +458,11 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
 // with a 4-pixel halo; free boundary: neighbours outside the frame are absent
 // (value 0 in the tile, excluded from sum b).  The first sweep of a time step
 // subtracts the RemoveTipTilt plane (from the S0 sums) on load.
-template <int N>
+template <int N, int TILE>
 __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, const int by, const int s,
                                             const float *phi_in, float *phi_out, float *phi_copy) {
-  constexpr int T = N < kTile ? N : kTile, P = N * N;
+  using G = Icd<TILE>;
+  constexpr int T = N < TILE ? N : TILE, P = N * N;
   extern __shared__ float icd_sm[];
   float *ps = icd_sm;
   const int tid = threadIdx.x;
@@ -469,8 +476,8 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
   const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
   const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
-  for (int idx = tid; idx < kReg * kSub; idx += kSThreads) {
-    const int li = idx / kSub, pj = idx - li * kSub;
+  for (int idx = tid; idx < G::kReg * G::kSub; idx += kSThreads) {
+    const int li = idx / G::kSub, pj = idx - li * G::kSub;
     const int gi = i0 - kHalo + li, gj = j0 - kHalo + 2 * pj;
     float2 v = make_float2(0.f, 0.f);
     if (gi >= 0 && gi < N && gj >= 0 && gj < N) {  // pairs are both inside or both outside
@@ -478,8 +485,8 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
       const float pl = c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2);
       v = make_float2(f.x - pl, f.y - (pl + c1));
     }
-    ps[sidx(2 * (li & 1), li >> 1, pj)] = v.x;
-    ps[sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
+    ps[G::sidx(2 * (li & 1), li >> 1, pj)] = v.x;
+    ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
   }
   __syncthreads();
   if (!degenerate) {
@@ -489,8 +496,8 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       const int ci = c >> 1, cj = c & 1;
-      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(kReg - c - 1, ci);
-      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(kReg - c - 1, cj);
+      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(G::kReg - c - 1, ci);
+      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(G::kReg - c - 1, cj);
       const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
       constexpr int KMAX = (35 * 35 + kSThreads - 1) / kSThreads;
       float Rv[KMAX];
@@ -505,14 +512,14 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
           if (gi < 0 || gi >= N || gj < 0 || gj >= N) continue;  // outside the frame: absent
           float pi_, n4, nd;
 #define DDH_NB(CI, CJ)                                                                           \
-  pi_ = ps[sidx(2 * CI + CJ, a, bb)];                                                             \
-  n4 = (ps[nidx<CI, CJ, -1, 0>(a, bb)] + ps[nidx<CI, CJ, 1, 0>(a, bb)]) +                         \
-       (ps[nidx<CI, CJ, 0, -1>(a, bb)] + ps[nidx<CI, CJ, 0, 1>(a, bb)]);                          \
-  nd = (ps[nidx<CI, CJ, -1, -1>(a, bb)] + ps[nidx<CI, CJ, -1, 1>(a, bb)]) +                       \
-       (ps[nidx<CI, CJ, 1, -1>(a, bb)] + ps[nidx<CI, CJ, 1, 1>(a, bb)]);
+  pi_ = ps[G::sidx(2 * CI + CJ, a, bb)];                                                             \
+  n4 = (ps[G::template nidx<CI, CJ, -1, 0>(a, bb)] + ps[G::template nidx<CI, CJ, 1, 0>(a, bb)]) +                         \
+       (ps[G::template nidx<CI, CJ, 0, -1>(a, bb)] + ps[G::template nidx<CI, CJ, 0, 1>(a, bb)]);                          \
+  nd = (ps[G::template nidx<CI, CJ, -1, -1>(a, bb)] + ps[G::template nidx<CI, CJ, -1, 1>(a, bb)]) +                       \
+       (ps[G::template nidx<CI, CJ, 1, -1>(a, bb)] + ps[G::template nidx<CI, CJ, 1, 1>(a, bb)]);
           if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
 #undef DDH_NB
-          const int me = sidx(c, a, bb);
+          const int me = G::sidx(c, a, bb);
           const size_t g = off + (size_t)gi * N + gj;
           const float cv = __ldg(A.cc + g), tv = __ldg(A.theta + g);
           const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
@@ -537,16 +544,16 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
     const int li = oi + kHalo;
     const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
     const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
-                                : make_float2(ps[sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
-                                              ps[sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
+                                : make_float2(ps[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
+                                              ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
     *reinterpret_cast<float2 *>(phi_out + g) = v;
     if (phi_copy) *reinterpret_cast<float2 *>(phi_copy + g) = v;
   }
 }
 
-template <int N>
+template <int N, int TILE>
 __global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
-  phiicd_body<N>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
+  phiicd_body<N, TILE>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
 }
 
 // ------------------------------------------------------------- launchers
@@ -570,8 +577,10 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
-  cudaFuncSetAttribute(ks_phiicd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
-  cudaFuncSetAttribute(ks_ricd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_phiicd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_ricd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_phiicd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_ricd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
   return cudaGetLastError();
 }
 
@@ -607,16 +616,35 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
 }
+// ICD tile size: 64 (throughput) unless a launch would have fewer 64-tiles
+// than two per SM, then 32 (4x the tiles: shorter per-CTA chains, lower
+// single-stream latency, +20 % halo recomputation)
+template <int N>
+static bool small_tiles(int sc) {
+  return N >= 64 && (N / 64) * (N / 64) * sc < 2 * 148;
+}
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  return launch_pdl(ks_ricd<N>, dim3(N / T, N / T, a.sc), dim3(kSThreads), kIcdGrid * sizeof(float), st, a);
+                  if (small_tiles<N>(a.sc)) {
+                    constexpr int T = N < 32 ? N : 32;
+                    return launch_pdl(ks_ricd<N, 32>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
+                                      Icd<32>::kIcdGrid * sizeof(float), st, a);
+                  }
+                  constexpr int T = N < 64 ? N : 64;
+                  return launch_pdl(ks_ricd<N, 64>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
+                                    Icd<64>::kIcdGrid * sizeof(float), st, a);
                 }));
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
-                  constexpr int T = N < kTile ? N : kTile;
-                  return launch_pdl(ks_phiicd<N>, dim3(N / T, N / T, a.sc), dim3(kSThreads), kIcdGrid * sizeof(float), st, a);
+                  if (small_tiles<N>(a.sc)) {
+                    constexpr int T = N < 32 ? N : 32;
+                    return launch_pdl(ks_phiicd<N, 32>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
+                                      Icd<32>::kIcdGrid * sizeof(float), st, a);
+                  }
+                  constexpr int T = N < 64 ? N : 64;
+                  return launch_pdl(ks_phiicd<N, 64>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
+                                    Icd<64>::kIcdGrid * sizeof(float), st, a);
                 }));
 }
 
