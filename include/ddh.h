@@ -58,9 +58,12 @@ typedef enum {
                                default: the streaming 6-kernel iteration          */
 #define DDH_F_SERIAL 8u     /* enqueue every kernel on the ctx stream in order (no
                                lanes, no side stream): per-kernel event timing     */
-#define DDH_F_NO_GRAPHS 16u /* never replay a recurring single-frame ddh_step from a
-                               captured CUDA graph (default: a call with the same
-                               frame/output pointers seen twice is captured once)  */
+#define DDH_F_GRAPHS 32u    /* latency mode for synchronous per-frame calls: a single-
+                               frame ddh_step whose frame/output pointers recur is
+                               captured once into a CUDA graph and replayed (fewer
+                               host launch gaps); back-to-back calls are faster
+                               without it (graph boundaries stop the overlap of
+                               consecutive steps)                                 */
 
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 

@@ -69,10 +69,10 @@ struct ddh_ctx {
   bool split_r = false;
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
-  // CUDA graphs of single-frame steps: a key (frame, outputs, phi parity)
-  // seen twice within the last kKeyWindow calls is captured once and replayed
-  // afterwards (the host then enqueues one graph instead of ~10 launches and
-  // events, so a synchronous per-frame call is not host-bound)
+  // CUDA graphs of single-frame steps (DDH_F_GRAPHS): a key (frame, outputs,
+  // phi parity) seen twice within the last kKeyWindow calls is captured once
+  // and replayed afterwards (the host then enqueues one graph instead of ~10
+  // launches and events, so a synchronous per-frame call is not host-bound)
   struct GraphKey {
     const void *y;
     const void *phi, *r, *st;
@@ -84,7 +84,7 @@ struct ddh_ctx {
     cudaGraphExec_t exec;
     uint64_t launches, last;
   };
-  bool graphs = true;
+  bool graphs = false;
   cudaStream_t cap_st = nullptr;  // capture stream (the ctx stream may be the legacy default stream)
   std::vector<GraphEntry> gcache;
   std::vector<GraphKey> gseen;
@@ -467,6 +467,10 @@ constexpr size_t kGraphCache = 16, kKeyWindow = 64;
 // One DDH step of one frame batch, replayed from a CUDA graph when this exact
 // call (same frame and output pointers, same phi parity) recurs.
 ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status) {
+  // Opt-in (DDH_F_GRAPHS) for synchronous per-frame use, where a graph removes
+  // the host launch gaps from the frame's latency.  Back-to-back calls are
+  // better served by direct launches, whose programmatic dependent launches
+  // overlap one step's tail with the next step's head (graph boundaries do not).
   if (!c->graphs || c->profiling) return run_frame(c, y, phi_out, r_out, status, Mode::Step, c->p.n_k);
   const ddh_ctx::GraphKey key{y, phi_out, r_out, status, c->cur};
   ++c->gclock;
@@ -741,7 +745,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   }
   {
     const char *gr = std::getenv("DDH_GRAPHS");  // diagnostic override
-    c->graphs = !(p.flags & DDH_F_NO_GRAPHS) && (gr ? std::atoi(gr) != 0 : true);
+    c->graphs = gr ? std::atoi(gr) != 0 : (p.flags & DDH_F_GRAPHS) != 0;
   }
   if (c->streaming) A(ddh::init_stream(n));
   if (c->streaming || ddh::fused_supported(n)) {

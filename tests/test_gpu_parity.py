@@ -476,7 +476,7 @@ def test_graph_replay_bit_exact(flags):
     n, S, T = 128, 2, 6
     y, _, _ = frames(n, S, T)
     yt = torch.from_numpy(y).to(DEV)
-    ctxs = [DDH(n, S, noise_var=0.1, flags=flags), DDH(n, S, noise_var=0.1, flags=flags | 16)]
+    ctxs = [DDH(n, S, noise_var=0.1, flags=flags | 32), DDH(n, S, noise_var=0.1, flags=flags)]
     bufs = [torch.empty((1, S, n, n), dtype=torch.complex64, device=DEV) for _ in ctxs]
     outs = [(torch.empty((1, S, n, n), device=DEV), torch.empty((1, S, n, n), device=DEV)) for _ in ctxs]
     for t in range(T):
