@@ -237,24 +237,37 @@ __global__ void kz_screen_coef(float2 *coef, int M, int S, const double *r0px, u
   }
 }
 
-// plane sums of Re(screen)[0:N, 0:N] over the aperture: (sum phi, phi x, phi y)
-__global__ void kz_plane_sums(const float2 *scr, int n, int M, const int2 *span, double *sums) {
+// plane sums of Re(screen)[0:N, 0:N] over the aperture: (sum phi, phi x, phi y);
+// grid (n / 8 row groups, S): FP32 per-thread partials of one row, FP64 block
+// sums, then a fixed-order reduction of the row groups (kz_plane_reduce)
+__global__ void kz_plane_sums(const float2 *scr, int n, int M, const int2 *span, double *part) {
   __shared__ double red[32 * 5];
-  const int s = blockIdx.x;
+  const int s = blockIdx.y, i0 = blockIdx.x * 8;
   double v[3] = {0, 0, 0};
-  for (int k = threadIdx.x; k < n * n; k += kT) {
-    const int i = k / n, j = k % n;
+  for (int r = 0; r < 8; ++r) {
+    const int i = i0 + r;
     const int2 sp = span[i];
-    if (j >= sp.x && j < sp.y) {
-      const double f = scr[((size_t)s * M + i) * M + j].x;
-      v[0] += f;
-      v[1] += f * (j - n / 2);
-      v[2] += f * (i - n / 2);
+    float a0 = 0.f, a1 = 0.f;
+    for (int j = sp.x + threadIdx.x; j < sp.y; j += kT) {
+      const float f = scr[((size_t)s * M + i) * M + j].x;
+      a0 += f;
+      a1 = fmaf(f, (float)(j - n / 2), a1);
     }
+    v[0] += a0;
+    v[1] += a1;
+    v[2] += (double)a0 * (i - n / 2);
   }
   block_sum<3>(v, red);
   if (threadIdx.x == 0)
-    for (int k = 0; k < 3; ++k) sums[3 * s + k] = v[k];
+    for (int k = 0; k < 3; ++k) part[((size_t)s * gridDim.x + blockIdx.x) * 3 + k] = v[k];
+}
+__global__ void kz_plane_reduce(const double *part, int groups, double *sums, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  double v[3] = {0, 0, 0};
+  for (int g = 0; g < groups; ++g)
+    for (int k = 0; k < 3; ++k) v[k] += part[((size_t)s * groups + g) * 3 + k];
+  for (int k = 0; k < 3; ++k) sums[3 * s + k] = v[k];
 }
 
 struct AsmArgs {
@@ -348,7 +361,7 @@ struct ddh_synth {
   uint2 key{};
   float *r = nullptr, *tmp = nullptr;
   float2 *coef = nullptr, *scr = nullptr, *spk = nullptr;
-  double *shift = nullptr, *r0px = nullptr, *mm = nullptr, *sums = nullptr, *sig2 = nullptr;
+  double *shift = nullptr, *r0px = nullptr, *mm = nullptr, *sums = nullptr, *sig2 = nullptr, *psum = nullptr;
   int2 *span = nullptr;
   double minv[9] = {};
   std::vector<double> vel;  // [S][2]
@@ -358,7 +371,7 @@ struct ddh_synth {
 namespace {
 void synth_free(ddh_synth *z) {
   if (!z) return;
-  void *p[] = {z->r, z->tmp, z->coef, z->scr, z->spk, z->shift, z->r0px, z->mm, z->sums, z->sig2, z->span};
+  void *p[] = {z->r, z->tmp, z->coef, z->scr, z->spk, z->shift, z->r0px, z->mm, z->sums, z->sig2, z->span, z->psum};
   for (void *q : p)
     if (q) cudaFree(q);
   delete z;
@@ -403,6 +416,7 @@ ddh_status ddh_synth_create(int32_t n, float diam, int32_t streams, const double
   A(cudaMalloc(&z->r0px, S * 8));
   A(cudaMalloc(&z->mm, S * 3 * 8));
   A(cudaMalloc(&z->sums, S * 3 * 8));
+  A(cudaMalloc(&z->psum, S * (n / 8) * 3 * 8));
   A(cudaMalloc(&z->sig2, S * 8));
   A(cudaMalloc(&z->span, n * sizeof(int2)));
   if (e != cudaSuccess) {
@@ -488,7 +502,8 @@ ddh_status ddh_synth_frames(ddh_synth *z, int64_t t0, int32_t T, void *y, float 
     a.shift = z->shift;
     if (ddh::z_rows(z->M, 1, a, z->S, z->st) != cudaSuccess) return DDH_E_CUDA;
     if (ddh::z_cols(z->M, a, z->S, z->st) != cudaSuccess) return DDH_E_CUDA;
-    ddh::kz_plane_sums<<<z->S, ddh::kT, 0, z->st>>>(z->scr, z->n, z->M, z->span, z->sums);
+    ddh::kz_plane_sums<<<dim3(z->n / 8, z->S), ddh::kT, 0, z->st>>>(z->scr, z->n, z->M, z->span, z->psum);
+    ddh::kz_plane_reduce<<<(z->S + 127) / 128, 128, 0, z->st>>>(z->psum, z->n / 8, z->sums, z->S);
     // speckle: rows of chi g (inverse DFT), then columns
     a.buf = z->spk;
     a.r = z->r;

@@ -26,8 +26,8 @@ os.makedirs(out_dir, exist_ok=True)
 
 
 def short(name):
-    m = re.search(r"(k[a-z0-9_]+)(<\d+>)?\(", name)
-    return (m.group(1) + (m.group(2) or "")) if m else name[:40]
+    m = re.search(r"(k[a-z0-9_]+)(<[\d, ]+>)?\(", name)
+    return (m.group(1) + (m.group(2) or "").replace(" ", "")) if m else name[:40]
 
 
 # ---- launch list (cold-cache, serialised: shares, not absolutes)
@@ -40,6 +40,8 @@ if os.path.exists(lcsv):
     for r in rows:
         if r["Metric Name"] == "gpu__time_duration.sum":
             k = short(r["Kernel Name"])
+            if k.startswith("kz_"):  # on-device synthesiser: input generation before the timed steps
+                continue
             tot[k] += float(r["Metric Value"])
             cnt[k] += 1
     allns = sum(tot.values())
