@@ -191,6 +191,40 @@ __host__ __device__ __forceinline__ float newton_root(float x, float B2, float S
   return x;
 }
 
+// Halley's method on g (cubic convergence; g'' = 12 B x - 4 S), from the same
+// start points as the monotone Newton runs: two unrolled steps, then a guarded
+// loop.  Checked against the oracle's exact minimiser on 6e5 random cases and
+// the c3 ICD inputs (tools/check_r_update.py: same roots, max relative error
+// 1e-6); 3.6 instead of 4.9 iterations for the slowest lane of a warp.
+__host__ __device__ __forceinline__ float halley_root(float x, float B2, float S2, float B6, float S4, float q) {
+  float dx = 0.f;
+  const float B12 = 2.f * B6;
+#pragma unroll
+  for (int it = 0; it < 2; ++it) {
+#if defined(DDH_ITER_HOOK) && !defined(__CUDA_ARCH__)
+    DDH_ITER_HOOK;
+#endif
+    const float G = g_of(x, B2, S2, q), D = dg_of(x, B6, S4), H = fmaf(B12, x, -S4);
+    const float den = fmaf(2.f * D, D, -G * H);
+    dx = (D > 0.f && den > 0.f) ? DDH_FDIV(2.f * G * D, den) : 0.f;
+    x -= dx;
+  }
+  if (fabsf(dx) <= 2e-7f * fabsf(x)) return x;
+#pragma unroll 1
+  for (int it = 0; it < 14; ++it) {
+#if defined(DDH_ITER_HOOK) && !defined(__CUDA_ARCH__)
+    DDH_ITER_HOOK;
+#endif
+    const float G = g_of(x, B2, S2, q), D = dg_of(x, B6, S4), H = fmaf(B12, x, -S4);
+    const float den = fmaf(2.f * D, D, -G * H);
+    if (!(D > 0.f) || !(den > 0.f)) break;
+    const float d = DDH_FDIV(2.f * G * D, den);
+    x -= d;
+    if (fabsf(d) <= 2e-7f * fabsf(x)) break;
+  }
+  return x;
+}
+
 // Three roots (both local minima present): the lower surrogate value wins.
 static __host__ __device__ __noinline__ float r_pick_two(float rc, float q, float B, float S, float r_min, float xs,
                                                   float B2, float S2, float B6, float S4) {
@@ -220,10 +254,10 @@ __host__ __device__ __forceinline__ float r_update(float rc, float q, float B, f
     has_small = xi > 0.f && g_of(xi, B2, S2, q) > 0.f;
     has_large = !has_small;
   }
-  // one Newton run per lane: the small root if it exists (from 0: first iterate
-  // q), else the large root (from max(S/B, q)); the second minimum only when
-  // both exist (rare; separate non-inlined path)
-  const float x = newton_root(has_small ? q : fmaxf(S * iB, q), B2, S2, B6, S4, q);
+  // one root search per lane: the small root if it exists (start q), else the
+  // large root (start max(S/B, q)); the second minimum only when both exist
+  // (rare; separate non-inlined path, monotone Newton)
+  const float x = halley_root(has_small ? q : fmaxf(S * iB, q), B2, S2, B6, S4, q);
   if (has_small && has_large) return r_pick_two(rc, q, B, S, r_min, x, B2, S2, B6, S4);
   return fmaxf(x, r_min);
 }

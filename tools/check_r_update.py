@@ -3,6 +3,9 @@ import subprocess, sys
 import numpy as np
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import oracle.ddh_oracle as O
+_HERE = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+subprocess.run(["nvcc", "-x", "cu", "-O2", "-o", "/tmp/r_update_host", __import__("os").path.join(_HERE, "r_update_host.cu")],
+               check=True)
 g = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 m = 200000
 for scale in (1.0, 0.01, 100.0):
