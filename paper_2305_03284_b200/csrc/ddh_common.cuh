@@ -109,24 +109,19 @@ __device__ __forceinline__ float qgg_w(float d, float inv_Tsig, float tmq) {
 }
 
 // The same weight for a pair of neighbours (rj.x, rj.y) of pixel ri on packed
-// FP32 pairs (fused path): t = (|d| / (T sig))^(2-q) = 2^(h lg2(d^2 + tiny) + g)
-// with h = (2-q)/2, g = (2-q) lg2(1/(T sig)); the 1e-37 floor keeps lg2 finite
-// at d = 0 (t ~ 2^-49 there, and t = 1 exactly at q = 2).  1/(1+t) on the FMA
-// pipe: magic-constant seed + 3 Newton steps (rel. error < 2e-7), which leaves
-// 2 MUFU per neighbour (lg2, ex2) instead of 3.  Returns (w(d.x), w(d.y)).
+// FP32 pairs (streaming and cluster paths): t = (|d| / (T sig))^(2-q) =
+// 2^(h lg2(d^2 + tiny) + g) with h = (2-q)/2, g = (2-q) lg2(1/(T sig)); the
+// 1e-37 floor keeps lg2 finite at d = 0 (t ~ 2^-49 there, and t = 1 exactly at
+// q = 2).  3 MUFU per neighbour (lg2, ex2, rcp: 64 ops/clk/SM on this part,
+// tools/micro/mufu_rate.cu) and 5 packed FP32 instructions per pair; the
+// kernels around it are issue-bound, so the reciprocal stays on MUFU.
+// Returns (w(d.x), w(d.y)).
 __device__ __forceinline__ float2 qgg_w2(float ri, float2 rj, float h, float g, float k) {
   const float2 d = p_sub(bc2(ri), rj);
   const float2 a = p_fma(d, d, bc2(1e-37f));
   const float2 e = p_fma(make_float2(lg2_approx(a.x), lg2_approx(a.y)), bc2(h), bc2(g));
   const float2 u = p_add(make_float2(ex2_approx(e.x), ex2_approx(e.y)), bc2(1.f));
-#ifdef DDH_QGG_MUFU_RCP
   const float2 y = make_float2(rcp_approx(u.x), rcp_approx(u.y));
-#else
-  float2 y = make_float2(__int_as_float(0x7EF311C3 - __float_as_int(u.x)), __int_as_float(0x7EF311C3 - __float_as_int(u.y)));
-  const float2 nu = make_float2(-u.x, -u.y);
-#pragma unroll
-  for (int it = 0; it < 3; ++it) y = p_mul(y, p_fma(nu, y, bc2(2.f)));
-#endif
   return p_mul(p_fma(y, bc2(1.f - k), bc2(k)), y);  // (k + (1-k)/u) / u
 }
 
