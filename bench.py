@@ -237,7 +237,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     t0 = time.time()
-    if args.synth == "device":  # on-device synthesiser (libddh ddh_synth_*), same recipe as synth/
+    if args.synth == "device" and n <= 512:  # on-device synthesiser (libddh ddh_synth_*, N <= 512), same recipe as synth/
         y_dev = device_frames(cfg, S, F, first, local)
         torch.cuda.synchronize()
         y_host = y_dev.cpu().numpy()
