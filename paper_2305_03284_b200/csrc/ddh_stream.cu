@@ -398,12 +398,19 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
   const float *__restrict__ qin = A.q + off;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
-  for (int idx = tid; idx < G::kReg * G::kSub; idx += kSThreads) {
-    const int li = idx / G::kSub, pj = idx - li * G::kSub;
-    const int gi = (i0 - kHalo + li) & (N - 1), gj = (j0 - kHalo + 2 * pj) & (N - 1);
-    const float2 v = *reinterpret_cast<const float2 *>(rin + (size_t)gi * N + gj);
-    rs[G::sidx(2 * (li & 1), li >> 1, pj)] = v.x;
-    rs[G::sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
+  {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
+    constexpr int RP = kSThreads / G::kSub;
+    const int pj = tid % G::kSub, r0 = tid / G::kSub;
+    if (r0 < RP) {
+      const float *src = rin + ((j0 - kHalo + 2 * pj) & (N - 1));
+#pragma unroll 4
+      for (int li = r0; li < G::kReg; li += RP) {
+        const float2 v = *reinterpret_cast<const float2 *>(src + (size_t)((i0 - kHalo + li) & (N - 1)) * N);
+        float *d = rs + G::sidx(2 * (li & 1), li >> 1, pj);
+        d[0] = v.x;                     // colour (li & 1, 0)
+        d[G::kSub * G::kSubP] = v.y;    // colour (li & 1, 1)
+      }
+    }
   }
   const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   __syncthreads();
@@ -476,17 +483,28 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
   const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
   if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
   const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
-  for (int idx = tid; idx < G::kReg * G::kSub; idx += kSThreads) {
-    const int li = idx / G::kSub, pj = idx - li * G::kSub;
-    const int gi = i0 - kHalo + li, gj = j0 - kHalo + 2 * pj;
-    float2 v = make_float2(0.f, 0.f);
-    if (gi >= 0 && gi < N && gj >= 0 && gj < N) {  // pairs are both inside or both outside
-      const float2 f = *reinterpret_cast<const float2 *>(pin + (size_t)gi * N + gj);
-      const float pl = c0 + c1 * (float)(gj - N / 2) + c2 * (float)(gi - N / 2);
-      v = make_float2(f.x - pl, f.y - (pl + c1));
+  {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
+    constexpr int RP = kSThreads / G::kSub;
+    const int pj = tid % G::kSub, r0 = tid / G::kSub;
+    if (r0 < RP) {
+      const int gj = j0 - kHalo + 2 * pj;
+      const bool jin = gj >= 0 && gj < N;  // pairs are both inside or both outside
+      const float px = fmaf(c1, (float)(gj - N / 2), c0);
+      const float *src = pin + gj;
+#pragma unroll 4
+      for (int li = r0; li < G::kReg; li += RP) {
+        const int gi = i0 - kHalo + li;
+        float2 v = make_float2(0.f, 0.f);
+        if (jin && gi >= 0 && gi < N) {
+          const float2 f = *reinterpret_cast<const float2 *>(src + (size_t)gi * N);
+          const float pl = fmaf(c2, (float)(gi - N / 2), px);
+          v = make_float2(f.x - pl, f.y - (pl + c1));
+        }
+        float *d = ps + G::sidx(2 * (li & 1), li >> 1, pj);
+        d[0] = v.x;
+        d[G::kSub * G::kSubP] = v.y;
+      }
     }
-    ps[G::sidx(2 * (li & 1), li >> 1, pj)] = v.x;
-    ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj)] = v.y;
   }
   __syncthreads();
   if (!degenerate) {
