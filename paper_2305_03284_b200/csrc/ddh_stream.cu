@@ -24,6 +24,8 @@
 // N <= 256), all arithmetic on complex pairs uses packed FP32x2 instructions.
 // The ICD kernels store the tile colour-separated (four (i mod 2, j mod 2)
 // sub-grids), so a colour phase reads and writes consecutive words.
+#include <cstdlib>
+
 #include "ddh_common.cuh"
 #include "ddh_fft_reg.cuh"
 #include "ddh_kernels.h"
@@ -238,6 +240,128 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
 #endif
 #pragma unroll
   for (int e = 0; e < E; ++e) A.cbuf[row + t + TPV * out_comb<N>(e)] = v[e];
+}
+
+// S1, persistent form: grid = 2 CTAs per SM; each CTA walks its row blocks
+// (item = (row block, stream)) through a two-stage shared-memory ring filled
+// by bulk asynchronous copies (cp.async.bulk, completion on an mbarrier): the
+// H contiguous y rows (H N 8 B) and phi rows (H N 4 B) of item k+2 stream in
+// while item k is transformed.  The stage of the item being transformed also
+// serves as its FFT exchange buffer.
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *m, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(m)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int N> struct S1P {
+  using C = SCfg<N>;
+  static constexpr int YB = C::H * N * 8, FB = C::H * N * 4;   // bytes per stage: y rows, phi rows
+  static constexpr int STAGE = YB + FB;
+  static_assert(C::H * C::RPITCH * 8 <= STAGE, "FFT exchange fits in a stage");
+  static constexpr size_t SMEM = N * sizeof(float4) + 2 * (size_t)STAGE;
+};
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
+  using C = SCfg<N>;
+  using Q = S1P<N>;
+  constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N, NR = N / H;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;                                           // [N]
+  char *stage0 = reinterpret_cast<char *>(smem4 + N);           // 2 x [y rows | phi rows]
+  __shared__ double red[32];
+  __shared__ __align__(8) uint64_t mb[2];
+  const int tid = threadIdx.x, G = gridDim.x, total = NR * A.sc;
+  const int t = tid % TPV, b = tid / TPV;
+  auto issue = [&](int item, int st, bool y_part, bool phi_part) {  // thread 0
+    const int bx = item % NR, s = item / NR;
+    char *dst = stage0 + st * Q::STAGE;
+    const size_t row0 = (size_t)s * P + (size_t)bx * H * N;
+    if (y_part) {
+      mbar_expect_tx(&mb[st], Q::YB + Q::FB);
+      bulk_g2s(dst, A.y + row0, Q::YB, &mb[st]);
+    }
+    if (phi_part) bulk_g2s(dst + Q::YB, A.phi_in + row0, Q::FB, &mb[st]);
+  };
+  if (tid == 0) {
+    mbar_init(&mb[0], 1);
+    mbar_init(&mb[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  DDH_PDL_TRIGGER();
+  // y is read-only user input: its copies may start before the wait; phi after
+  if (tid == 0) {
+    if (blockIdx.x < total) issue(blockIdx.x, 0, true, false);
+    if (blockIdx.x + G < total) issue(blockIdx.x + G, 1, true, false);
+  }
+  load_tw<N>(tw, A.tw4, tid, NT);
+  DDH_PDL_WAIT();
+  if (tid == 0) {
+    if (blockIdx.x < total) issue(blockIdx.x, 0, false, true);
+    if (blockIdx.x + G < total) issue(blockIdx.x + G, 1, false, true);
+  }
+  __syncthreads();  // twiddles
+  int k = 0;
+  for (int item = blockIdx.x; item < total; item += G, ++k) {
+    const int st = k & 1, bx = item % NR, s = item / NR;
+    const int i = bx * H + b;
+    const size_t row = (size_t)s * P + (size_t)i * N;
+    char *stg = stage0 + st * Q::STAGE;
+    const float2 *ys = reinterpret_cast<const float2 *>(stg) + b * N;
+    const float *fs = reinterpret_cast<const float *>(stg + Q::YB) + b * N;
+    double sums[5], cpl[3] = {0, 0, 0};
+    sum_part0(A.part0, A.nb0, s, sums);
+    if (A.apply_plane) plane_from_sums(sums, A.minv, cpl);
+    const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
+    const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
+    const int2 sp = __ldg(A.rowspan + i);
+    const float pyi = fmaf(c2, (float)(i - N / 2), c0);
+    mbar_wait(&mb[st], (k >> 1) & 1);
+    float2 v[E];
+    float acc = 0.f;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int j = t + TPV * e;
+      const float2 d = p_sub(ys[j], make_float2(mur, mui));
+      acc = fmaf(d.x, d.x, fmaf(d.y, d.y, acc));
+      float2 z = make_float2(0.f, 0.f);
+      if (j >= sp.x && j < sp.y) {
+        float sn, cs;
+        sincos_red(fs[j] - fmaf(c1, (float)(j - N / 2), pyi), sn, cs);
+        const float sg = ((i + j) & 1) ? -1.f : 1.f;
+        z = p_fma(bc2(d.x * sg), make_float2(cs, -sn), p_mul(bc2(d.y * sg), make_float2(sn, cs)));
+      }
+      v[e] = z;
+    }
+    double a1[1] = {(double)acc};
+    block_sum<1>(a1, red);  // also: every thread is past its reads of the stage
+    if (tid == 0) A.part1[(size_t)s * A.nb1 + bx] = a1[0];
+    fft_reg<N>(v, t, reinterpret_cast<float2 *>(stg) + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) A.cbuf[row + t + TPV * out_comb<N>(e)] = v[e];
+    __syncthreads();  // the stage (FFT exchange) is free
+    if (tid == 0 && item + 2 * G < total) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(item + 2 * G, st, true, true);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ S2
@@ -597,6 +721,7 @@ template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t
 template <int N>
 static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_fwd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
+  cudaFuncSetAttribute(ks_rows_fwd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S1P<N>::SMEM);
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
   cudaFuncSetAttribute(ks_phiicd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
@@ -632,6 +757,15 @@ cudaError_t launch_s0(const StepArgs &a, cudaStream_t st) {
   return launch_pdl(ks_stats, dim3(a.nb0, a.sc), dim3(kSThreads), 0, st, a);
 }
 cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
+  static const int persist = getenv("DDH_S1P") ? atoi(getenv("DDH_S1P")) : 1;
+  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
+  if (persist) {
+    DDH_SDISPATCH(a.n, ({
+                    const int total = N / SCfg<N>::H * a.sc;
+                    const int grid = total < 2 * sms ? total : 2 * sms;
+                    return launch_pdl(ks_rows_fwd_p<N>, dim3(grid), dim3(SCfg<N>::NTR), S1P<N>::SMEM, st, a);
+                  }));
+  }
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_fwd<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srow_smem<N>(), st, a));
 }
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
