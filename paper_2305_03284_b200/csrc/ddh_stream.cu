@@ -417,6 +417,96 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   for (int e = 0; e < E; ++e) A.cbuf[off + (size_t)(t + TPV * out_comb<N>(e)) * N + col] = w2[e];
 }
 
+// S2, persistent form (N <= 256): 2 CTAs per SM walk their column slabs
+// (item = (W-column block, stream)) through a two-stage ring filled with
+// 16-byte cp.async copies: the spectrum slab [N][W] (also the stage's FFT
+// exchange buffer) and the r_prev slab [N][W] of item k+2 stream in while
+// item k is transformed.
+template <int N> struct S2P {
+  using C = SCfg<N>;
+  static constexpr int CB = N * C::W * 8, RB = N * C::W * 4, STAGE = CB + RB;
+  static constexpr size_t SMEM = N * sizeof(float4) + 2 * (size_t)STAGE;
+};
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTC, 2) ks_cols_p(StepArgs A) {
+  using C = SCfg<N>;
+  using Q = S2P<N>;
+  constexpr int E = C::E, TPV = C::TPV, W = C::W, NT = C::NTC, P = N * N, NC = N / W;
+  static_assert(NT == 256, "256-thread column CTAs");
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;
+  char *stage0 = reinterpret_cast<char *>(smem4 + N);
+  const int tid = threadIdx.x, G = gridDim.x, total = NC * A.sc;
+  const int b = tid % W, t = tid / W;
+  auto issue = [&](int item, int st) {  // all threads: 16-byte chunks of the two slabs
+    const int bx = item % NC, s = item / NC;
+    const size_t base = (size_t)s * P + (size_t)bx * W;
+    const unsigned dc = smem_u32(stage0 + st * Q::STAGE), dr = dc + Q::CB;
+    for (int c = tid; c < N * W / 2; c += NT) {  // spectrum: W/2 chunks (2 complex) per row
+      const int row = c / (W / 2), part = c % (W / 2);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dc + 16 * c),
+                   "l"(A.cbuf + base + (size_t)row * N + 2 * part));
+    }
+    for (int c = tid; c < N * W / 4; c += NT) {  // r_prev: W/4 chunks per row
+      const int row = c / (W / 4), part = c % (W / 4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dr + 16 * c),
+                   "l"(A.r_state + base + (size_t)row * N + 4 * part));
+    }
+  };
+  DDH_PDL_TRIGGER();
+  load_tw<N>(tw, A.tw4, tid, NT);
+  DDH_PDL_WAIT();
+  if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
+  asm volatile("cp.async.commit_group;");
+  if ((int)blockIdx.x + G < total) issue(blockIdx.x + G, 1);
+  asm volatile("cp.async.commit_group;");
+  int k = 0;
+  for (int item = blockIdx.x; item < total; item += G, ++k) {
+    const int st = k & 1, bx = item % NC, s = item / NC;
+    const int col = bx * W + b;
+    const size_t off = (size_t)s * P;
+    float2 *slab = reinterpret_cast<float2 *>(stage0 + st * Q::STAGE);  // [N][W]
+    const float *rsl = reinterpret_cast<const float *>(stage0 + st * Q::STAGE + Q::CB);
+    const double d2 = sum_part1(A.part1, A.nb1, s);
+    const bool degenerate = !(d2 > 0.0);
+    if (A.status && bx == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
+    const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+    const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's group (one newer may be pending)
+    __syncthreads();  // every thread's chunks (and the twiddles) visible
+    float2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = slab[(t + TPV * e) * W + b];
+    __syncthreads();  // the slab becomes the exchange buffer
+    fft_reg<N>(v, t, slab + b, [](int p) { return p * W; }, tw);
+    const bool warm = A.warm && !degenerate;
+    float2 w2[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int ki = t + TPV * out_comb<N>(e);
+      const size_t g = off + (size_t)ki * N + col;
+      const float sg = ((ki + col) & 1) ? -scale : scale;
+      const float2 u = p_mul(v[e], bc2(sg));
+      float r0 = rsl[ki * W + b];
+      if (warm) r0 = fmaxf(fmaf(A.oml, r0, A.la * fmaf(u.x, u.x, u.y * u.y)), A.r_min);  // Eq. 3
+      const float w = r0 * rcp_approx(r0 + A.s2);                                        // E-step (R1)
+      const float2 mu = p_mul(u, bc2(w));
+      A.rinit[g] = r0;
+      A.q[g] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+      const float cs = ((ki + col) & 1) ? -1.f : 1.f;
+      w2[out_comb<N>(e)] = make_float2(cs * mu.x, -cs * mu.y);
+    }
+    __syncthreads();  // exchange buffer free
+    fft_reg<N>(w2, t, slab + b, [](int p) { return p * W; }, tw);
+#pragma unroll
+    for (int e = 0; e < E; ++e) A.cbuf[off + (size_t)(t + TPV * out_comb<N>(e)) * N + col] = w2[e];
+    __syncthreads();  // stage st free
+    if (item + 2 * G < total) issue(item + 2 * G, st);
+    asm volatile("cp.async.commit_group;");
+  }
+}
+
 // ------------------------------------------------------------------ S4
 
 template <int N>
@@ -724,6 +814,7 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_rows_fwd_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S1P<N>::SMEM);
   cudaFuncSetAttribute(ks_rows_inv<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srowi_smem<N>());
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
+  if constexpr (N <= 256) cudaFuncSetAttribute(ks_cols_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S2P<N>::SMEM);
   cudaFuncSetAttribute(ks_phiicd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_ricd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
@@ -769,6 +860,19 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_fwd<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srow_smem<N>(), st, a));
 }
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
+  static const int persist = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 1;
+  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
+  if (persist && a.n <= 256) {
+    DDH_SDISPATCH(a.n, ({
+                    if constexpr (N <= 256) {
+                      // staged form for launches of at most two slabs per SM (few streams:
+                      // c2 step 28.8 -> 25.3 us); at 64 streams the plain kernel is as fast
+                      const int total = N / SCfg<N>::W * a.sc;
+                      if (total <= 2 * sms)
+                        return launch_pdl(ks_cols_p<N>, dim3(total), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
+                    }
+                  }));
+  }
   DDH_SDISPATCH(a.n, return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a));
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
