@@ -885,8 +885,19 @@ template <int N>
 static bool small_tiles(int sc) {
   return N >= 64 && (N / 64) * (N / 64) * sc < 2 * 148;
 }
+// 16x16 tiles when even 32-tiles would leave most SMs idle (one stream at
+// N <= 256: 256 CTAs with one pass per colour phase; c2 step 26.3 -> 24.7 us
+// despite 2.25x halo work)
+template <int N>
+static bool tiny_tiles(int sc) {
+  static const int on = getenv("DDH_T16") ? atoi(getenv("DDH_T16")) : 1;
+  return on && (N / 32) * (N / 32) * sc < 148;
+}
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
+                  if (tiny_tiles<N>(a.sc))
+                    return launch_pdl(ks_ricd<N, 16>, dim3(N / 16, N / 16, a.sc), dim3(kSThreads),
+                                      Icd<16>::kIcdGrid * sizeof(float), st, a);
                   if (small_tiles<N>(a.sc)) {
                     constexpr int T = N < 32 ? N : 32;
                     return launch_pdl(ks_ricd<N, 32>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
@@ -899,6 +910,9 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
+                  if (tiny_tiles<N>(a.sc))
+                    return launch_pdl(ks_phiicd<N, 16>, dim3(N / 16, N / 16, a.sc), dim3(kSThreads),
+                                      Icd<16>::kIcdGrid * sizeof(float), st, a);
                   if (small_tiles<N>(a.sc)) {
                     constexpr int T = N < 32 ? N : 32;
                     return launch_pdl(ks_phiicd<N, 32>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
