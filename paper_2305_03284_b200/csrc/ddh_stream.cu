@@ -603,8 +603,8 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 // phases the 64x64 core equals the global colour-ordered sweep.  q is read
 // from global (L2) at the pixel's update and only r is staged (21 KB smem),
 // within 32 registers: 8 CTAs (64 warps) per SM.
-template <int N, int TILE>
-__global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
+template <int N, int TILE, int NTH = kSThreads>
+__global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   using G = Icd<TILE>;
   constexpr int T = N < TILE ? N : TILE, P = N * N;
   extern __shared__ float icd_sm[];
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
   {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
-    constexpr int RP = kSThreads / G::kSub;
+    constexpr int RP = NTH / G::kSub;
     const int pj = tid % G::kSub, r0 = tid / G::kSub;
     if (r0 < RP) {
       const float *src = rin + ((j0 - kHalo + 2 * pj) & (N - 1));
@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
       const int blo = sub_lo(c + 1, cj), bhi = sub_lo(G::kReg - c - 1, cj);
       const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
 #pragma unroll 1
-      for (int p = tid; p < cnt; p += kSThreads) {
+      for (int p = tid; p < cnt; p += NTH) {
         const int a = alo + p / nbb, bb = blo + p % nbb;
         float ri, n0, n1, n2, n3, d0, d1, d2v, d3;
 #define DDH_NB(CI, CJ)                                                                       \
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
       __syncthreads();
     }
   }
-  for (int idx = tid; idx < T * (T / 2); idx += kSThreads) {
+  for (int idx = tid; idx < T * (T / 2); idx += NTH) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
     const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kSThreads, 8) ks_ricd(StepArgs A) {
 // with a 4-pixel halo; free boundary: neighbours outside the frame are absent
 // (value 0 in the tile, excluded from sum b).  The first sweep of a time step
 // subtracts the RemoveTipTilt plane (from the S0 sums) on load.
-template <int N, int TILE>
+template <int N, int TILE, int NTH = kSThreads>
 __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, const int by, const int s,
                                             const float *phi_in, float *phi_out, float *phi_copy) {
   using G = Icd<TILE>;
@@ -702,7 +702,7 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
   if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
   const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
   {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
-    constexpr int RP = kSThreads / G::kSub;
+    constexpr int RP = NTH / G::kSub;
     const int pj = tid % G::kSub, r0 = tid / G::kSub;
     if (r0 < RP) {
       const int gj = j0 - kHalo + 2 * pj;
@@ -735,12 +735,12 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
       const int alo = sub_lo(c + 1, ci), ahi = sub_lo(G::kReg - c - 1, ci);
       const int blo = sub_lo(c + 1, cj), bhi = sub_lo(G::kReg - c - 1, cj);
       const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
-      constexpr int KMAX = (35 * 35 + kSThreads - 1) / kSThreads;
+      constexpr int KMAX = (35 * 35 + NTH - 1) / NTH;
       float Rv[KMAX];
       int ix[KMAX];
 #pragma unroll
       for (int k = 0; k < KMAX; ++k) {
-        const int p = tid + k * kSThreads;
+        const int p = tid + k * NTH;
         ix[k] = -1;
         if (p < cnt) {
           const int a = alo + p / nbb, bb = blo + p % nbb;
@@ -775,7 +775,7 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
       __syncthreads();
     }
   }
-  for (int idx = tid; idx < T * (T / 2); idx += kSThreads) {
+  for (int idx = tid; idx < T * (T / 2); idx += NTH) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
     const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
@@ -787,9 +787,9 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
   }
 }
 
-template <int N, int TILE>
-__global__ void __launch_bounds__(kSThreads) ks_phiicd(StepArgs A) {
-  phiicd_body<N, TILE>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
+template <int N, int TILE, int NTH = kSThreads>
+__global__ void __launch_bounds__(NTH) ks_phiicd(StepArgs A) {
+  phiicd_body<N, TILE, NTH>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
 }
 
 // ------------------------------------------------------------- launchers
@@ -816,7 +816,7 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
   if constexpr (N <= 256) cudaFuncSetAttribute(ks_cols_p<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S2P<N>::SMEM);
   cudaFuncSetAttribute(ks_phiicd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
-  cudaFuncSetAttribute(ks_ricd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_ricd<N, 64, 320>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_ricd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
   return cudaGetLastError();
@@ -904,7 +904,9 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
                                       Icd<32>::kIcdGrid * sizeof(float), st, a);
                   }
                   constexpr int T = N < 64 ? N : 64;
-                  return launch_pdl(ks_ricd<N, 64>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
+                  // 320 threads (10 warps): the colour phases' 1225/1156/1089/1024 pixels
+                  // take 4 passes instead of 5/5/5/4 (step 434 -> 440 k frames/s; 384: 433 k)
+                  return launch_pdl(ks_ricd<N, 64, 320>, dim3(N / T, N / T, a.sc), dim3(320),
                                     Icd<64>::kIcdGrid * sizeof(float), st, a);
                 }));
 }
