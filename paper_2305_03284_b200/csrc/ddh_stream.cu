@@ -859,21 +859,21 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   }
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_fwd<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srow_smem<N>(), st, a));
 }
-cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
-  static const int persist = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 1;
-  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
-  if (persist && a.n <= 256) {
-    DDH_SDISPATCH(a.n, ({
-                    if constexpr (N <= 256) {
-                      // staged form for launches of at most two slabs per SM (few streams:
-                      // c2 step 28.8 -> 25.3 us); at 64 streams the plain kernel is as fast
-                      const int total = N / SCfg<N>::W * a.sc;
-                      if (total <= 2 * sms)
-                        return launch_pdl(ks_cols_p<N>, dim3(total), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
-                    }
-                  }));
+// staged form for launches of at most two slabs per SM (few streams: c2 step
+// 28.8 -> 25.3 us); at 64 streams the plain kernel is as fast
+template <int N>
+static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, bool staged_ok, int sms) {
+  if constexpr (N <= 256) {
+    const int total = N / SCfg<N>::W * a.sc;
+    if (staged_ok && total <= 2 * sms)
+      return launch_pdl(ks_cols_p<N>, dim3(total), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
   }
-  DDH_SDISPATCH(a.n, return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a));
+  return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a);
+}
+cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
+  static const int staged = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 1;  // diagnostic
+  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
+  DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged != 0, sms));
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
