@@ -119,7 +119,7 @@ ddh_status ddh_destroy(ddh_ctx *c);
  * iterations run; before iteration k with k mod boot_period == 0 the
  * reflectance is reset to max(boot_alpha |A_phi^H y|^2, r_min).  The frame is
  * consumed (frame counter += 1).  k_b == 0 is a no-op (Fig. 1 cold start).
- * y0: device complex64 [S][N][N].  status: device uint8 [S] or NULL (0 ok,
+ * y0: device complex64 [S][N][N], 16-byte aligned.  status: device uint8 [S] or NULL (0 ok,
  * 1 degenerate frame: the stream stays cold).  Errors: DDH_E_INVAL (k_b < 0,
  * NULL y0), DDH_E_CUDA. */
 ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *status);
@@ -129,10 +129,11 @@ ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *statu
  * LS plane incl. piston, R17); r <- max((1-lambda) r + lambda alpha
  * |A_phi^H y|^2, r_min) (Eq. 3); then N_k EM iterations (E-step, qGGMRF r-ICD,
  * GMRF phi-ICD; R1-R12), two 2-D FFTs each (R13); WriteData.
- * y: device complex64 [T][S][N][N].  phi_out, r_out: device float32
- * [T][S][N][N] or NULL (the state always advances).  status: device uint8
- * [T][S] or NULL.  Errors: DDH_E_INVAL (T < 0 or NULL y with T > 0),
- * DDH_E_CUDA. */
+ * y: device complex64 [T][S][N][N], 16-byte aligned (bulk asynchronous copies
+ * of whole rows).  phi_out, r_out: device float32 [T][S][N][N], 8-byte
+ * aligned, or NULL (the state always advances).  status: device uint8 [T][S]
+ * or NULL.  Errors: DDH_E_INVAL (T < 0, NULL y with T > 0, misaligned
+ * pointers), DDH_E_CUDA. */
 ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float *r_out,
                     uint8_t *status);
 

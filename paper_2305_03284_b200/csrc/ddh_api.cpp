@@ -826,6 +826,7 @@ ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *statu
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (k_b < 0 || (!y0 && k_b > 0)) return fail(c, DDH_E_INVAL, "ddh_bootstrap: bad arguments");
+  if ((uintptr_t)y0 & 15) return fail(c, DDH_E_INVAL, "ddh_bootstrap: y0 must be 16-byte aligned");
   if (k_b == 0) return DDH_OK;
   DDH_CK(c, cudaSetDevice(c->p.device));
   s = run_frame(c, (const float2 *)y0, nullptr, nullptr, status, Mode::Boot, k_b);
@@ -838,6 +839,8 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (T < 0 || (!y && T > 0)) return fail(c, DDH_E_INVAL, "ddh_step: bad arguments");
+  if (((uintptr_t)y & 15) || ((uintptr_t)phi_out & 7) || ((uintptr_t)r_out & 7))
+    return fail(c, DDH_E_INVAL, "ddh_step: y must be 16-byte aligned, phi_out / r_out 8-byte aligned");
   DDH_CK(c, cudaSetDevice(c->p.device));
   const size_t fs = (size_t)c->S * c->P;
   for (int t = 0; t < T; ++t) {
@@ -854,6 +857,8 @@ ddh_status ddh_static(ddh_ctx *c, const void *y, int32_t T, int32_t iters, float
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (T < 0 || iters < 1 || (!y && T > 0)) return fail(c, DDH_E_INVAL, "ddh_static: bad arguments");
+  if (((uintptr_t)y & 15) || ((uintptr_t)phi_out & 7) || ((uintptr_t)r_out & 7))
+    return fail(c, DDH_E_INVAL, "ddh_static: y must be 16-byte aligned, phi_out / r_out 8-byte aligned");
   DDH_CK(c, cudaSetDevice(c->p.device));
   const size_t fs = (size_t)c->S * c->P;
   for (int t = 0; t < T; ++t) {

@@ -491,3 +491,21 @@ def test_graph_replay_bit_exact(flags):
     r1, p1, f1 = ctxs[1].get_state()
     assert torch.equal(r0, r1) and torch.equal(p0, p1) and f0 == f1 == T
     assert ctxs[0].kernel_launches == ctxs[1].kernel_launches
+
+
+def test_misaligned_frames_are_rejected():
+    """Whole frame rows move by bulk asynchronous copies: a y pointer that is
+    not 16-byte aligned is refused with DDH_E_INVAL (not a CUDA fault), and
+    the ctx stays usable."""
+    import ctypes
+    n, S = 64, 1
+    ctx = DDH(n, S, noise_var=0.1)
+    y = torch.zeros((2, S, n, n), dtype=torch.complex64, device=DEV)
+    rc = ctx.lib.ddh_step(ctx.h, ctypes.c_void_p(y.data_ptr() + 8), 1, None, None, None)
+    assert rc == 1 and b"aligned" in ctx.lib.ddh_last_error(ctx.h)
+    rc = ctx.lib.ddh_bootstrap(ctx.h, ctypes.c_void_p(y.data_ptr() + 8), 2, None)
+    assert rc == 1
+    y[0] = torch.from_numpy(frames(n, S, 1)[0][0]).to(DEV)
+    ctx.step(y[:1])
+    torch.cuda.synchronize()
+    assert ctx.get_state()[2] == 1
