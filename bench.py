@@ -475,9 +475,47 @@ def e2e_leg(ctx, y_host, K, ws, dev, S, n):
     dt = time.perf_counter() - t0
     dt = reduce_max(dt, ws, dev)
     P = n * n
-    return {"value": Ke * S * ws / dt, "unit": UNIT, "h2d_bytes_per_step": S * P * 8, "d2h_bytes_per_step": S * P * 4,
+    h2d_gbs, d2h_gbs = pcie_gbs(S * P * 8, S * P * 4, dev)
+    ceiling = min(h2d_gbs * 1e9 / (S * P * 8), d2h_gbs * 1e9 / (S * P * 4)) * S * ws
+    value = Ke * S * ws / dt
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": S * P * 8, "d2h_bytes_per_step": S * P * 4,
             "steps": Ke, "frames_per_call": Tc,
-            "api": "ddh_step_host (pinned host y in, phi out; copies overlapped across frames), host wall clock, max over ranks"}
+            "api": "ddh_step_host (pinned host y in, phi out; copies overlapped across frames), host wall clock, max over ranks",
+            "pcie": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "ceiling": ceiling, "frac": value / ceiling,
+                     "note": "pinned copies of one step's bytes, both directions at once on two streams, measured "
+                             "here: the e2e leg's transfer ceiling"}}
+
+
+def pcie_gbs(b_in, b_out, dev, reps=40):
+    """Concurrent pinned H2D (b_in bytes) and D2H (b_out bytes) bandwidth, GB/s."""
+    import torch
+    h_in = torch.empty(b_in, dtype=torch.uint8).pin_memory()
+    h_out = torch.empty(b_out, dtype=torch.uint8).pin_memory()
+    d_in = torch.empty(b_in, dtype=torch.uint8, device=dev)
+    d_out = torch.empty(b_out, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+    def burst(k):
+        e = torch.cuda.Event()
+        e.record(main)
+        s1.wait_event(e)
+        s2.wait_event(e)
+        for _ in range(k):
+            with torch.cuda.stream(s1):
+                d_in.copy_(h_in, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h_out.copy_(d_out, non_blocking=True)
+        main.wait_stream(s1)
+        main.wait_stream(s2)
+    burst(3)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    burst(reps)
+    e1.record(main)
+    torch.cuda.synchronize(dev)
+    t = e0.elapsed_time(e1) * 1e-3
+    return reps * b_in / t / 1e9, reps * b_out / t / 1e9
 
 
 def latency_leg(dev, local):
