@@ -16,7 +16,8 @@
 //   S3 ks_ricd      qGGMRF r-ICD on 64x64 tiles with a 4-pixel periodic halo
 //                   (one colour sweep, R6-R9), recomputing the halo ring
 //   S4 ks_rows_inv  row DFT of the conjugated spectrum -> f = F_c^{-1} mu;
-//                   c = (2/s2)|y-hat||f|, theta = arg(y-hat conj f)
+//                   c = (2/s2)|y-hat||f|, theta = arg(y-hat conj f), written
+//                   as (c, theta) pairs in place over the spectrum rows
 //   S5 ks_phiicd    GMRF phi-ICD on 64x64 tiles, 4-pixel halo, free edge
 //                   (R10-R11)
 //
@@ -559,8 +560,7 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
       c = two_s2 * sqrt_approx(fmaf(z.x, z.x, z.y * z.y) + 1e-37f);
       th = atan2_fast(z.y, z.x);
     }
-    A.cc[row + j] = c;
-    A.theta[row + j] = th;
+    A.cbuf[row + j] = make_float2(c, th);  // in place: this CTA read its spectrum rows before the FFT
   }
 }
 
@@ -757,7 +757,8 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
 #undef DDH_NB
           const int me = G::sidx(c, a, bb);
           const size_t g = off + (size_t)gi * N + gj;
-          const float cv = __ldg(A.cc + g), tv = __ldg(A.theta + g);
+          const float2 ct = __ldg(A.cbuf + g);  // (c, theta) from S4
+          const float cv = ct.x, tv = ct.y;
           const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
           float sb = 1.f;  // sum of b over the existing neighbours
           if (edge) {
