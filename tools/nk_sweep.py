@@ -1,6 +1,7 @@
 """throughput of the c3 workload (256^2, 64 streams) vs the
 number of EM iterations per time step N_k in {1, 2, 4, 8} (uninstrumented
-CUDA-event timing, inputs resident in HBM).  Writes profiles/<round>_nk_sweep.json."""
+CUDA-event timing, inputs resident in HBM).  Writes profiles/<round>_nk_sweep.json
+(gpurun_out/ on a gpurun box, whose profiles/ is not copied back)."""
 import json
 import os
 import sys
@@ -36,4 +37,4 @@ for nk in (1, 2, 4, 8):
     print(f"N_k={nk}: {ms * 1000:8.1f} us/step  {S / (ms * 1e-3):10.0f} frames/s  {S * nk / (ms * 1e-3):10.0f} EM-iter/s",
           flush=True)
 json.dump({"workload": "c3: 256x256, 64 streams, synthetic", "results": res},
-          open(os.path.join(ROOT, "profiles", f"{rnd}_nk_sweep.json"), "w"), indent=1)
+          open(os.path.join(ROOT, "gpurun_out" if os.environ.get("GRAFT_REPO_ROOT") else "profiles", f"{rnd}_nk_sweep.json"), "w"), indent=1)

@@ -44,4 +44,4 @@ for nk in (1, 2, 4, 8):
           f"first frame >= 0.8: {first}", flush=True)
 json.dump({"config": "paper (P:218-229): 256^2, D/r0 10, |v| 0.595 px/frame at 45 deg, SNR 10 dB, cold start, "
                      f"{seeds} seeds, scene {scene}", "paper_result": "Strehl >= 0.8 within 150 frames at N_k = 1 (P:266, 270)",
-           "results": res}, open(os.path.join(ROOT, "profiles", f"{rnd}_paper_convergence_{scene}.json"), "w"), indent=1)
+           "results": res}, open(os.path.join(ROOT, "gpurun_out" if os.environ.get("GRAFT_REPO_ROOT") else "profiles", f"{rnd}_paper_convergence_{scene}.json"), "w"), indent=1)
