@@ -61,4 +61,5 @@ for nk in (1, 5, 50):
 ctx = DDH(n, 1, noise_var=nv)
 run("static DH-MBIR 300 iters", lambda o, c=ctx: c.static(yd, 300, o))
 os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump(out, open(os.path.join(ROOT, "gpurun_out" if os.environ.get("GRAFT_REPO_ROOT") else "profiles", f"{rnd}_c5_compare.json"), "w"), indent=1)

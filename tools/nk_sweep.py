@@ -36,5 +36,6 @@ for nk in (1, 2, 4, 8):
     res[nk] = {"ms_per_step": ms, "frames_per_s": S / (ms * 1e-3), "em_iterations_per_s": S * nk / (ms * 1e-3)}
     print(f"N_k={nk}: {ms * 1000:8.1f} us/step  {S / (ms * 1e-3):10.0f} frames/s  {S * nk / (ms * 1e-3):10.0f} EM-iter/s",
           flush=True)
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump({"workload": "c3: 256x256, 64 streams, synthetic", "results": res},
           open(os.path.join(ROOT, "gpurun_out" if os.environ.get("GRAFT_REPO_ROOT") else "profiles", f"{rnd}_nk_sweep.json"), "w"), indent=1)

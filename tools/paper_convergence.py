@@ -42,6 +42,7 @@ for nk in (1, 2, 4, 8):
     print(f"N_k={nk}: median Strehl frames 150-300 {np.median(st[150:]):.3f}; frame 50/100/150/299 "
           f"{np.median(st[50]):.3f} {np.median(st[100]):.3f} {np.median(st[150]):.3f} {np.median(st[299]):.3f}; "
           f"first frame >= 0.8: {first}", flush=True)
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
 json.dump({"config": "paper (P:218-229): 256^2, D/r0 10, |v| 0.595 px/frame at 45 deg, SNR 10 dB, cold start, "
                      f"{seeds} seeds, scene {scene}", "paper_result": "Strehl >= 0.8 within 150 frames at N_k = 1 (P:266, 270)",
            "results": res}, open(os.path.join(ROOT, "gpurun_out" if os.environ.get("GRAFT_REPO_ROOT") else "profiles", f"{rnd}_paper_convergence_{scene}.json"), "w"), indent=1)
