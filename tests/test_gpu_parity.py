@@ -509,3 +509,23 @@ def test_misaligned_frames_are_rejected():
     ctx.step(y[:1])
     torch.cuda.synchronize()
     assert ctx.get_state()[2] == 1
+
+
+def test_kernel_variants_bit_exact():
+    """The launch-size-dependent kernel variants compute the same arithmetic:
+    at 256^2 with 20 streams, launch groups of 1, 4 and 20 streams take the
+    16x16, 32x32 and 64x64 ICD tiles (halo recomputation gives exactly the
+    global colour-ordered sweep) and the staged / plain column kernel; the
+    results agree bit for bit."""
+    n, S, T = 256, 20, 2
+    y, _, _ = frames(n, S, T)
+    yt = torch.from_numpy(y).to(DEV)
+    outs = []
+    for chunk in (1, 4, 20):
+        ctx = DDH(n, S, noise_var=0.1, chunk_streams=chunk)
+        po = torch.empty((T, S, n, n), device=DEV)
+        ro = torch.empty_like(po)
+        ctx.step(yt, po, ro)
+        outs.append((po, ro))
+    for po, ro in outs[1:]:
+        assert torch.equal(outs[0][0], po) and torch.equal(outs[0][1], ro)
