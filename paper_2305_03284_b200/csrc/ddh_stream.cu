@@ -8,13 +8,15 @@
 //
 //   S0 ks_stats     per stream: sum y (Eq. 4 mean) and the
 //                   RemoveTipTilt normal-equation sums of phi
-//   S1 ks_rows_fwd  z = chi a e^{-j phi'} (y - mu); forward row DFT;
-//                   partial ||y - mu||^2
+//   S1 ks_rows_fwd_p  z = chi a e^{-j phi'} (y - mu); forward row DFT;
+//                   partial ||y - mu||^2; persistent, rows streamed in by
+//                   bulk asynchronous copies (ks_rows_fwd: one-shot form)
 //   S2 ks_cols      column DFT -> u = A^H y-hat (R13); Eq. 3; E-step (R1)
 //                   -> r0, q to HBM; FFT of conj(chi mu) (the inverse column
-//                   DFT by conjugation)
-//   S3 ks_ricd      qGGMRF r-ICD on 64x64 tiles with a 4-pixel periodic halo
-//                   (one colour sweep, R6-R9), recomputing the halo ring
+//                   DFT by conjugation); ks_cols_p (staged) for small launches
+//   S3 ks_ricd      qGGMRF r-ICD on 64x64 (32x32, 16x16 for small launches)
+//                   tiles with a 4-pixel periodic halo (one colour sweep,
+//                   R6-R9), recomputing the halo ring
 //   S4 ks_rows_inv  row DFT of the conjugated spectrum -> f = F_c^{-1} mu;
 //                   c = (2/s2)|y-hat||f|, theta = arg(y-hat conj f), written
 //                   as (c, theta) pairs in place over the spectrum rows
@@ -602,7 +604,9 @@ __host__ __device__ constexpr int sub_lo(int lo, int p) { return (lo - p + 1) / 
 // pixels of colour c in the region shrunk by c+1 on each side, so after the 4
 // phases the 64x64 core equals the global colour-ordered sweep.  q is read
 // from global (L2) at the pixel's update and only r is staged (21 KB smem),
-// within 32 registers: 8 CTAs (64 warps) per SM.
+// within 32 registers.  The 64x64 tile runs 320 threads (6 CTAs, 60 warps
+// per SM): its colour phases (1225, 1156, 1089, 1024 pixels) take 4 passes
+// each, against 5/5/5/4 at 256 threads.
 template <int N, int TILE, int NTH = kSThreads>
 __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   using G = Icd<TILE>;
