@@ -88,7 +88,7 @@ typedef struct {
   int32_t icd_sweeps;   /* 4-colour ICD sweeps per M-step >= 1, default 1 (R8)             */
   int32_t boot_period;  /* bootstrap reset period P_b >= 1, default 200            */
   double boot_alpha;    /* bootstrap back-projection weight alpha_b > 0, default 1 (R15)   */
-  int32_t chunk_streams;/* streams per launch group (L2-resident workspace); 0 = auto       */
+  int32_t chunk_streams;/* streams per launch group; 0 = auto (all, up to 8 GiB workspace) */
   uint32_t flags;       /* DDH_F_*                                                        */
   int32_t lanes;        /* fused path: concurrent sub-groups of a launch group, each on its
                            own CUDA stream forked from / joined to the ctx stream, so the
