@@ -475,24 +475,24 @@ def e2e_leg(ctx, y_host, K, ws, dev, S, n):
     dt = time.perf_counter() - t0
     dt = reduce_max(dt, ws, dev)
     P = n * n
-    h2d_gbs, d2h_gbs = pcie_gbs(S * P * 8, S * P * 4, dev)
+    h2d_gbs, d2h_gbs = pcie_gbs(y_pin[0], phi_pin[0], dev)  # the e2e leg's own pinned buffers
     ceiling = min(h2d_gbs * 1e9 / (S * P * 8), d2h_gbs * 1e9 / (S * P * 4)) * S * ws
     value = Ke * S * ws / dt
     return {"value": value, "unit": UNIT, "h2d_bytes_per_step": S * P * 8, "d2h_bytes_per_step": S * P * 4,
             "steps": Ke, "frames_per_call": Tc,
             "api": "ddh_step_host (pinned host y in, phi out; copies overlapped across frames), host wall clock, max over ranks",
             "pcie": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "ceiling": ceiling, "frac": value / ceiling,
-                     "note": "pinned copies of one step's bytes, both directions at once on two streams, measured "
-                             "here: the e2e leg's transfer ceiling"}}
+                     "note": "copies of one step's frames in and phi out between the e2e leg's own pinned buffers "
+                             "and the device, both directions at once on two streams, measured right after the leg"}}
 
 
-def pcie_gbs(b_in, b_out, dev, reps=40):
-    """Concurrent pinned H2D (b_in bytes) and D2H (b_out bytes) bandwidth, GB/s."""
+def pcie_gbs(h_in, h_out, dev, reps=40):
+    """Concurrent pinned H2D (from h_in) and D2H (into h_out) bandwidth, GB/s:
+    one step's frames in and phi out, the same pinned buffers as the e2e leg."""
     import torch
-    h_in = torch.empty(b_in, dtype=torch.uint8).pin_memory()
-    h_out = torch.empty(b_out, dtype=torch.uint8).pin_memory()
-    d_in = torch.empty(b_in, dtype=torch.uint8, device=dev)
-    d_out = torch.empty(b_out, dtype=torch.uint8, device=dev)
+    b_in, b_out = h_in.numel() * h_in.element_size(), h_out.numel() * h_out.element_size()
+    d_in = torch.empty_like(h_in, device=dev)
+    d_out = torch.empty_like(h_out, device=dev)
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     main = torch.cuda.current_stream(dev)
     def burst(k):
