@@ -774,6 +774,38 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     c->cs = ddh::fused_cluster(n);
     A(ddh::init_fused(n));
   }
+  // Streaming path: the spectrum buffer is written by S1 and read / rewritten
+  // by S2, S4 and S5 within a step; a persisting-L2 window over it keeps it
+  // resident against the frames and state streaming through (c3: 32 MiB,
+  // 449.7 -> 455.5 k frames/s; a larger carve-out than the buffer, or a
+  // partial window over a buffer much larger than L2, does not pay).  The
+  // carve-out is a device-wide limit; DDH_L2P=0 disables it (diagnostic).
+  if (c->streaming) {
+    const char *pl = std::getenv("DDH_L2P");
+    const size_t cb = SC * P * sizeof(float2);
+    int maxp = 0;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p.device);
+    if ((!pl || std::atoi(pl) != 0) && cb <= ((size_t)48 << 20) && cb <= (size_t)maxp) {
+      size_t cur = 0;
+      cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      // best effort (not available under some sharing modes): failures are ignored
+      if (cur >= cb || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, cb) == cudaSuccess) {
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.base_ptr = c->cbuf;
+        v.accessPolicyWindow.num_bytes = cb;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        // only the library's own streams (lanes, r-ICD side streams); the
+        // caller's stream is left as it is
+        for (int l = 0; l < 8; ++l) {
+          if (c->lane_st[l]) cudaStreamSetAttribute(c->lane_st[l], cudaStreamAttributeAccessPolicyWindow, &v);
+          if (c->side_st[l]) cudaStreamSetAttribute(c->side_st[l], cudaStreamAttributeAccessPolicyWindow, &v);
+        }
+      }
+      cudaGetLastError();
+    }
+  }
   // state: n = 0, r = r_min, phi = 0 (Fig. 1; R14)
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));
   A(cudaMemsetAsync(c->phi[0], 0, S * P * sizeof(float), c->st));
