@@ -67,6 +67,7 @@ struct ddh_ctx {
   // streaming path: the r M-step (S3) of a lane runs on a side stream,
   // concurrently with the phi branch (S4, S5) it does not depend on (R12)
   bool split_r = false;
+  bool l2_window = false;  // holds the device's persisting-L2 carve-out
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
   // CUDA graphs of single-frame steps (DDH_F_GRAPHS): a key (frame, outputs,
@@ -102,6 +103,11 @@ struct ddh_ctx {
 namespace {
 
 std::mutex g_err_mu;
+// persisting-L2 carve-out (device-wide): contexts holding one per device, and
+// the limit found before the first of them raised it (restored by the last)
+std::mutex g_l2_mu;
+int g_l2_users[64] = {};
+size_t g_l2_prev[64] = {};
 std::string g_create_err;
 
 ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
@@ -545,6 +551,19 @@ double inv3(const double G[9], double out[9]) {
 
 void free_ctx(ddh_ctx *c) {
   if (!c) return;
+  if (c->l2_window) {  // the last context on the device restores the limit it found
+    std::lock_guard<std::mutex> lk(g_l2_mu);
+    const int d = c->p.device & 63;
+    if (--g_l2_users[d] == 0) {
+      int prev = -1;
+      cudaGetDevice(&prev);
+      cudaSetDevice(c->p.device);
+      cudaCtxResetPersistingL2Cache();
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, g_l2_prev[d]);
+      if (prev >= 0) cudaSetDevice(prev);
+      cudaGetLastError();
+    }
+  }
   for (auto &g : c->gcache) cudaGraphExecDestroy(g.exec);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
@@ -786,10 +805,14 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     int maxp = 0;
     cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, p.device);
     if ((!pl || std::atoi(pl) != 0) && cb <= ((size_t)48 << 20) && cb <= (size_t)maxp) {
+      std::lock_guard<std::mutex> lk(g_l2_mu);
       size_t cur = 0;
       cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+      if (g_l2_users[p.device & 63] == 0) g_l2_prev[p.device & 63] = cur;
       // best effort (not available under some sharing modes): failures are ignored
       if (cur >= cb || cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, cb) == cudaSuccess) {
+        ++g_l2_users[p.device & 63];
+        c->l2_window = true;
         cudaStreamAttrValue v = {};
         v.accessPolicyWindow.base_ptr = c->cbuf;
         v.accessPolicyWindow.num_bytes = cb;
