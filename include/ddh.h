@@ -105,8 +105,13 @@ ddh_status ddh_default_params(ddh_params *p);
 /* Create a ctx for S streams on p->device: validates p, allocates the state
  * r = r_min, phi = 0, frame counter n = 0 (Fig. 1 P:163 with R14), and the
  * workspace.  cuda_stream: a cudaStream_t (NULL = legacy default stream) on
- * which all work of this ctx is enqueued.  *out receives the ctx (caller frees
- * it with ddh_destroy).  Synchronous.
+ * which all work of this ctx is enqueued and ordered (the ctx may fork work
+ * onto streams of its own and joins them back before returning control to
+ * that stream's order).  *out receives the ctx (caller frees it with
+ * ddh_destroy).  Synchronous.  Side effect: with multiple lanes the ctx may
+ * raise the device's persisting-L2 carve-out to its spectrum buffer's size
+ * (<= 48 MiB, its own streams only); the last ctx on the device restores the
+ * previous limit in ddh_destroy.
  * Errors: DDH_E_INVAL (params out of range, unsupported N, non-interval mask),
  * DDH_E_NOMEM, DDH_E_CUDA. */
 ddh_status ddh_create(const ddh_params *p, void *cuda_stream, ddh_ctx **out);
