@@ -37,6 +37,9 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+# The CUDA runtime is linked dynamically from the toolkit (same image on the GPU box): a static
+# cudart would embed every runtime entry point's name in the shipped .so.
+CUDA_LIB = "/usr/local/cuda/lib64"
 EXTRA = os.environ.get("DDH_NVCC_EXTRA", "").split()
 
 
@@ -58,7 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.run(cmd, check=True)
         objs.append(obj)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "shared",
+           "-Xlinker", "-rpath," + CUDA_LIB, "-o", tmp, *objs]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB

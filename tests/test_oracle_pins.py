@@ -566,3 +566,250 @@ def test_icd_stencils_are_tangent_to_J_pair_sums():
         dJp = (O.cost_J_parts(r, phi + e, y, p, a)[2] - O.cost_J_parts(r, phi - e, y, p, a)[2]) / (2 * h)
         assert dJr == pytest.approx(2 * (B[k] * r[i, j] - S[k]), rel=1e-6, abs=1e-8)
         assert dJp == pytest.approx(w * (sb[k] * phi[i, j] - nb[k]), rel=1e-6, abs=1e-8)
+
+
+# ------------------------------------------- pins added after the round-1 mutation run
+
+
+def test_qggmrf_potential_shape_and_exponents():
+    """R6 fixes the qGGMRF potential with p = 2 (north_star "qGGMRF"): near zero
+    it is the Gaussian Delta^2/(2 sigma^2) (exponent p = 2), in the tail it grows
+    as |Delta|^q, and the transition sits at |Delta| = T sigma where the two
+    branches have equal weight (rho = T^2/4 there).  These follow from the
+    definition rho = |D|^p/(p sig^p) / (1 + |D/(T sig)|^(p-q)) and are checked
+    on log-log slopes measured by finite differences of log rho, so a swapped
+    exponent (q for 2-q) or a misplaced T fails."""
+    for sig, T, q in [(0.5, 1.0, 1.2), (0.2, 2.0, 1.5), (1.3, 0.5, 1.05)]:
+        # Gaussian limit at zero
+        for d in (1e-14 * T * sig, -1e-14 * T * sig):
+            rho = float(O.qggmrf_rho(np.array(d), sig, T, q))
+            assert rho * 2 * sig * sig / (d * d) == pytest.approx(1.0, abs=1e-6)
+        # local log-log slopes
+        def slope(d):
+            h = 1e-4
+            return (math.log(float(O.qggmrf_rho(np.array(d * math.exp(h)), sig, T, q)))
+                    - math.log(float(O.qggmrf_rho(np.array(d * math.exp(-h)), sig, T, q)))) / (2 * h)
+        assert slope(1e-7 * T * sig) == pytest.approx(2.0, abs=1e-3)
+        assert slope(1e9 * T * sig) == pytest.approx(q, abs=1e-3)
+        assert slope(-1e9 * T * sig) == pytest.approx(q, abs=1e-3)
+        # transition point: the two factors are equal (t = 1)
+        assert float(O.qggmrf_rho(np.array(T * sig), sig, T, q)) == pytest.approx(T * T / 4.0, rel=1e-12)
+        # the slope at the transition is the mean of the two exponents
+        assert slope(T * sig) == pytest.approx((2.0 + q) / 2.0, abs=1e-6)
+
+
+@pytest.mark.parametrize("n", [4])
+def test_phase_correlation_is_expected_complete_data_loglik(n):
+    """The phi M-step data term sum_i c_i cos(phi_i - theta_i) must equal the
+    phi-dependent part of Q(phi) = E[log p(y | g, phi)] = -E||y - A_phi g||^2/s2
+    + const (EM; y = A g + w, w ~ CN(0, s2 I)), with the
+    expectation over the posterior of g at the current (r, phi0).  Q is built
+    densely here: posterior mean and covariance by textbook Gaussian
+    conditioning, A_phi from the DFT definition, the trace term written out.
+    a = 1 (exact E-step).  Pins the factor 2/s2 in c and the sign of theta."""
+    g = rng(80)
+    P = n * n
+    a = np.ones((n, n))
+    s2 = 0.37
+    r = g.random((n, n)) * 2 + 0.05
+    phi0 = g.standard_normal((n, n))
+    y = crandn(g, n, n)
+    Fc = dense_centred_dft(n)
+
+    def A_of(phi):
+        return np.diag(np.exp(1j * phi.ravel())) @ Fc.conj().T
+
+    A0 = A_of(phi0)
+    Dr = np.diag(r.ravel())
+    Sy = A0 @ Dr @ A0.conj().T + s2 * np.eye(P)
+    K = Dr @ A0.conj().T @ np.linalg.inv(Sy)
+    mu = K @ y.ravel()
+    Sig = Dr - K @ A0 @ Dr
+    M2 = Sig + np.outer(mu, mu.conj())      # E[g g^H]
+
+    def Q(phi):
+        A = A_of(phi)
+        e = (np.vdot(y.ravel(), y.ravel()) - 2 * np.real(np.vdot(y.ravel(), A @ mu))
+             + np.real(np.trace(A.conj().T @ A @ M2)))
+        return -np.real(e) / s2
+
+    # the oracle's data term from its own E-step and second FFT
+    mu_o, _, _ = O.e_step(O.adjoint(phi0, y, a), r, s2)
+    c, theta = O.phase_correlation(y, O.ifft2c(mu_o), a, s2)
+
+    def D(phi):
+        return float(np.sum(c * np.cos(phi - theta)))
+
+    for k in range(5):
+        phi = phi0 + g.standard_normal((n, n)) * (0.3 + k)
+        lhs = Q(phi) - Q(phi0)
+        rhs = D(phi) - D(phi0)
+        assert lhs == pytest.approx(rhs, rel=1e-10, abs=1e-10 * abs(Q(phi0)))
+    # and the gradient at phi0 (finite differences of the dense Q)
+    h = 1e-6
+    for k in range(P):
+        e = np.zeros(P)
+        e[k] = h
+        e = e.reshape(n, n)
+        gq = (Q(phi0 + e) - Q(phi0 - e)) / (2 * h)
+        gd = float((-c * np.sin(phi0 - theta)).ravel()[k])
+        assert gq == pytest.approx(gd, rel=1e-6, abs=1e-8)
+
+
+def test_bootstrap_resets_every_period():
+    """the bootstrap resets r to a back-projected estimate every P_b
+    iterations ([pellizzari2017b], "every 200 iterations").  K_b = 5, P_b = 2:
+    resets happen before iterations 0, 2 and 4, written out by hand."""
+    n = 16
+    p = O.OracleParams(n=n, aperture_diam=14, boot_period=2, boot_alpha=0.7)
+    g = rng(81)
+    y = crandn(g, n, n) * 1.3
+    a = O.aperture_of(p)
+    r, phi, st = O.bootstrap(y, p, 5, a)
+    yh = O.normalize(y)
+    r2 = np.full((n, n), p.r_min)
+    phi2 = np.zeros((n, n))
+    for k in range(5):
+        u = O.adjoint(phi2, yh, a)
+        if k in (0, 2, 4):
+            r2 = np.maximum(0.7 * np.abs(u) ** 2, p.r_min)
+        r2, phi2 = O.em_update(r2, phi2, yh, u, a, p)
+    assert st == 0
+    assert np.allclose(r, r2, rtol=1e-12, atol=1e-14) and np.allclose(phi, phi2, rtol=1e-12, atol=1e-14)
+    # and it differs from the run with a single reset at k = 0 (the pin discriminates)
+    r3 = np.full((n, n), p.r_min)
+    phi3 = np.zeros((n, n))
+    for k in range(5):
+        u = O.adjoint(phi3, yh, a)
+        if k == 0:
+            r3 = np.maximum(0.7 * np.abs(u) ** 2, p.r_min)
+        r3, phi3 = O.em_update(r3, phi3, yh, u, a, p)
+    assert np.max(np.abs(r3 - r)) > 1e-3
+
+
+def test_remove_tip_tilt_removes_piston_and_plane():
+    """R17: RemoveTipTilt (Fig. 1) removes the LS plane including piston,
+    so a pure plane (any piston) maps to exactly zero at every pixel, and the
+    residual of any phase has zero mean and zero x/y moments over the aperture."""
+    n = 32
+    a = O.aperture(n, 30.0)
+    x, yy = O.plane_coords(n)
+    out = O.remove_tip_tilt(2.0 + 3.0 * x - 1.0 * yy, a)
+    assert np.max(np.abs(out)) < 1e-11
+    res = O.remove_tip_tilt(rng(82).standard_normal((n, n)), a)
+    m = a > 0
+    for basis in (np.ones((n, n)), x, yy):
+        assert abs(np.sum(res[m] * basis[m])) < 1e-9
+
+
+def _hand_r_icd(r, q, p):
+    """Pixel-by-pixel colour-ordered ICD written out with plain loops (R8):
+    colours (0,0),(0,1),(1,0),(1,1); inside a colour, raster order; each pixel
+    minimises the per-pixel surrogate (R9) given its current neighbours."""
+    r = r.copy()
+    n = r.shape[0]
+    for (ci, cj) in ((0, 0), (0, 1), (1, 0), (1, 1)):
+        for i in range(ci, n, 2):
+            for j in range(cj, n, 2):
+                B = S = 0.0
+                for (di, dj, b) in ((-1, 0, 1 / 6), (1, 0, 1 / 6), (0, -1, 1 / 6), (0, 1, 1 / 6),
+                                    (-1, -1, 1 / 12), (-1, 1, 1 / 12), (1, -1, 1 / 12), (1, 1, 1 / 12)):
+                    rj = r[(i + di) % n, (j + dj) % n]
+                    bt = b * float(O.qggmrf_weight(np.array(r[i, j] - rj), p.r_sigma, p.r_T, p.r_q))
+                    B += bt
+                    S += bt * rj
+                r[i, j] = O.r_update_pixels(np.array([r[i, j]]), np.array([q[i, j]]),
+                                            np.array([B]), np.array([S]), p.r_min)[0]
+    return r
+
+
+def _hand_phi_icd(phi, c, theta, p):
+    """Pixel-by-pixel GMRF phi-ICD (R8, R11) with plain loops: colour order as R8,
+    raster inside a colour, free boundary (neighbours off the grid dropped)."""
+    phi = phi.copy()
+    n = phi.shape[0]
+    w = 1.0 / p.phi_sigma ** 2
+    for (ci, cj) in ((0, 0), (0, 1), (1, 0), (1, 1)):
+        for i in range(ci, n, 2):
+            for j in range(cj, n, 2):
+                x0 = math.remainder(phi[i, j] - theta[i, j], 2 * math.pi)
+                if x0 == -math.pi:
+                    x0 = math.pi
+                s = 1.0 if x0 == 0 else math.sin(x0) / x0
+                nb = sb = 0.0
+                for (di, dj, b) in ((-1, 0, 1 / 6), (1, 0, 1 / 6), (0, -1, 1 / 6), (0, 1, 1 / 6),
+                                    (-1, -1, 1 / 12), (-1, 1, 1 / 12), (1, -1, 1 / 12), (1, 1, 1 / 12)):
+                    if 0 <= i + di < n and 0 <= j + dj < n:
+                        nb += b * phi[i + di, j + dj]
+                        sb += b
+                num = c[i, j] * s * (phi[i, j] - x0) + w * nb
+                den = c[i, j] * s + w * sb
+                if den != 0:
+                    phi[i, j] = num / den
+    return phi
+
+
+def test_icd_sweeps_equal_hand_written_sequential_sweeps():
+    """R8: the vectorised colour-phase ICDs equal a pixel-by-pixel sequential
+    sweep in the colour order (0,0),(0,1),(1,0),(1,1) (brute force, N = 6, with
+    values spread so the colour order changes the result)."""
+    n = 6
+    p = O.OracleParams(n=n)
+    g = rng(83)
+    r = g.random((n, n)) * 2 + 0.01
+    q = g.random((n, n)) * 3 + 0.01
+    assert np.allclose(O.r_icd(r, q, p), _hand_r_icd(r, q, p), rtol=1e-12, atol=1e-14)
+    phi = g.standard_normal((n, n)) * 2
+    c = g.random((n, n)) * 4
+    theta = g.uniform(-math.pi, math.pi, (n, n))
+    assert np.allclose(O.phi_icd(phi, c, theta, p), _hand_phi_icd(phi, c, theta, p), rtol=1e-12, atol=1e-13)
+
+
+def test_ddh_step_n_k_two_recomputes_the_back_projection():
+    """Fig. 1 P:169-171 / a9: with N_k = 2 the second EM iteration runs the
+    E-step on u = A^H_{phi_1} y, the back-projection through the phase the
+    first iteration produced (same normalised y, no second Eq. 3)."""
+    n = 16
+    p2 = O.OracleParams(n=n, aperture_diam=14, n_k=2, noise_var=0.2)
+    p1 = O.OracleParams(n=n, aperture_diam=14, n_k=1, noise_var=0.2)
+    a = O.aperture_of(p2)
+    g = rng(84)
+    y = crandn(g, n, n)
+    r = g.random((n, n)) + 0.05
+    phi = g.standard_normal((n, n))
+    r_a, phi_a, _ = O.ddh_step(r, phi, y, p2, a)
+    r_b, phi_b, _ = O.ddh_step(r, phi, y, p1, a)
+    yh = O.normalize(y)
+    r_b, phi_b = O.em_update(r_b, phi_b, yh, O.adjoint(phi_b, yh, a), a, p1)
+    assert np.allclose(r_a, r_b, rtol=1e-12, atol=1e-14) and np.allclose(phi_a, phi_b, rtol=1e-12, atol=1e-14)
+
+
+def test_r_update_exact_tie_picks_candidate_nearest_current():
+    """SURVEY 8.c.4 tie rule: two local minima x1 < x3 of the surrogate with
+    equal cost -> the one nearest the current r.  The tie is constructed in
+    closed form: the stationary points are the roots of 2B(x-x1)(x-x2)(x-x3),
+    so B = 1/(2 e2), S = B e1, q = 2B e3, and x2 is solved so f(x1) = f(x3)."""
+    x1, x3 = 0.3, 2.0
+
+    def coeffs(x2):
+        e1, e2, e3 = x1 + x2 + x3, x1 * x2 + x1 * x3 + x2 * x3, x1 * x2 * x3
+        B = 1.0 / (2.0 * e2)
+        return 2.0 * B * e3, B, B * e1
+
+    def gap(x2):
+        q, B, S = coeffs(x2)
+        f = lambda x: math.log(x) + q / x + B * x * x - 2 * S * x
+        return f(x1) - f(x3)
+
+    lo, hi = x1 + 1e-6, x3 - 1e-6
+    assert gap(lo) * gap(hi) < 0
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if gap(lo) * gap(mid) <= 0:
+            hi = mid
+        else:
+            lo = mid
+    q, B, S = coeffs(0.5 * (lo + hi))
+    qv, Bv, Sv = np.array([q, q]), np.array([B, B]), np.array([S, S])
+    out = O.r_update_pixels(np.array([0.25, 2.4]), qv, Bv, Sv, 1e-4)
+    assert out[0] == pytest.approx(x1, rel=1e-9) and out[1] == pytest.approx(x3, rel=1e-9)
