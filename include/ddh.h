@@ -54,8 +54,9 @@ typedef enum {
 #define DDH_F_NO_TIPTILT 1u /* skip RemoveTipTilt (Fig. 1) in ddh_step  */
 #define DDH_F_UNFUSED 2u    /* force the multi-pass kernels K0-K3b (reference
                                structure, used as a second implementation)      */
-#define DDH_F_CLUSTER 4u    /* force the cluster-fused 3-kernel iteration (N <= 512);
-                               default: the streaming 6-kernel iteration          */
+#define DDH_F_CLUSTER 4u    /* retired (round 2): the cluster-fused iteration was slower
+                               than the streaming one at every config; ddh_create
+                               returns DDH_E_INVAL when it is set                   */
 #define DDH_F_SERIAL 8u     /* enqueue every kernel on the ctx stream in order (no
                                lanes, no side stream): per-kernel event timing     */
 #define DDH_F_GRAPHS 32u    /* latency mode for synchronous per-frame calls: a single-
@@ -72,10 +73,12 @@ typedef struct {
   int32_t n;        /* grid side N: 64, 128, 256, 512 or 1024                         */
   int32_t streams;  /* S independent sensor streams owned by this ctx (>= 1)           */
   int32_t device;   /* CUDA device ordinal                                             */
-  float aperture_diam;          /* D_a: circle of diameter D px, strictly inside,
-                                   centred at (N/2, N/2); <= 0 selects aperture_mask     */
-  const uint8_t *aperture_mask; /* host [N][N] {0,1}, used when aperture_diam <= 0; every
-                                   row must be empty or one contiguous run of ones       */
+  float aperture_diam;          /* D_a: circle of diameter D px (0 < D <= N; 0 with
+                                   no mask means D = N), pixel centres strictly inside,
+                                   centred at (N/2, N/2); < 0 selects aperture_mask      */
+  const uint8_t *aperture_mask; /* host [N][N] {0,1}, used when aperture_diam <= 0 and it is
+                                   not NULL; every row must be empty or one contiguous run
+                                   of ones                                              */
   double noise_var; /* sigma^2 of the reconstruction in normalised-data units (R19), > 0  */
   double lambda;    /* Eq. 3 weight lambda in [0,1], default 0.45                 */
   double alpha;     /* Eq. 3 weight alpha in [0,1], default 0.025                 */
@@ -90,11 +93,10 @@ typedef struct {
   double boot_alpha;    /* bootstrap back-projection weight alpha_b > 0, default 1 (R15)   */
   int32_t chunk_streams;/* streams per launch group; 0 = auto (all, up to 8 GiB workspace) */
   uint32_t flags;       /* DDH_F_*                                                        */
-  int32_t lanes;        /* fused path: concurrent sub-groups of a launch group, each on its
-                           own CUDA stream forked from / joined to the ctx stream, so the
-                           kernels of different sub-groups share the SMs; 1..8, 0 = auto
-                           (streaming path: streams/32 in [1,2]; cluster path: streams/16
-                           in [1,4]).  Results do not depend on it.                      */
+  int32_t lanes;        /* streaming path: concurrent sub-groups of a launch group, each on
+                           its own CUDA stream forked from / joined to the ctx stream, so
+                           the kernels of different sub-groups share the SMs; 1..8, 0 =
+                           auto (streams/32 in [1,2]).  Results do not depend on it.      */
 } ddh_params;
 
 /* Defaults: N=256, S=1, device 0, D=N, sigma^2=0.1, lambda=0.45, alpha=0.025,
@@ -190,7 +192,9 @@ int64_t ddh_frame_index(const ddh_ctx *c);
 /* ---- instrumentation: per-kernel device time (CUDA events on the ctx stream) ----
  * Kernel kinds: 0 K0 stats, 1 K1 rows_fwd, 2 K2a cols, 3 K2b r-ICD,
  * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
- * 8 KA kf_rows_fwd, 9 KB kf_cols, 10 KC kf_rows_inv (cluster-fused path).
+ * 8-10 unused (the retired cluster path); 11 S0 ks_stats, 12 S1 ks_rows_fwd,
+ * 13 S2 ks_cols, 14 S3 ks_ricd, 15 S4 ks_rows_inv, 16 S5 ks_phiicd
+ * (streaming path, default).
  * When enabled, every launch of the ctx is bracketed by two events. */
 #define DDH_KIND_COUNT 17
 ddh_status ddh_profile_enable(ddh_ctx *c, int32_t enable);
@@ -201,18 +205,34 @@ ddh_status ddh_profile_read(ddh_ctx *c, double *ms, int64_t *launches);
 /* Static name of kernel kind k (or "?"). */
 const char *ddh_kind_name(int32_t k);
 
-/* ---- stage entry points for parity tests (same kernels as the hot path) ---- */
+/* ---- stage entry points for parity tests ----
+ * With the default (streaming) path these run the streaming kernels' own
+ * device code: the register FFT of S1/S2/S4, the E-step epilogue of S2, the
+ * S3 and S5 tile kernels.  With DDH_F_UNFUSED they run the multi-pass
+ * kernels.  All buffers are device buffers owned by the caller; the calls are
+ * asynchronous on the ctx stream.  Errors: DDH_E_INVAL (B < 0, NULL buffer),
+ * DDH_E_CUDA. */
 
 /* Centred unitary 2-D DFT F_c (inverse = 0) or F_c^{-1} (inverse = 1) of B
- * fields (R4): in, out device complex64 [B][N][N] (may alias). */
+ * fields ("normalized 2D discrete Fourier transform"; R4): in, out
+ * complex64 [B][N][N] (may alias). */
 ddh_status ddh_test_fft2c(ddh_ctx *c, const void *in, void *out, int32_t B, int32_t inverse);
 
+/* Eq. 3 + E-step of B fields (Eq. 3; P:93-95, 121 E-step, reading
+ * R1): u = A^H y-hat complex64 [B][N][N], r_prev float32 [B][N][N];
+ * warm != 0: r0 = max((1 - lambda) r_prev + lambda alpha |u|^2, r_min), else
+ * r0 = r_prev; w = r0/(r0 + noise_var); mu = w u (complex64), q = |mu|^2 +
+ * w noise_var.  Outputs r0, q float32 [B][N][N], mu complex64 [B][N][N]. */
+ddh_status ddh_test_estep(ddh_ctx *c, const void *u, const float *r_prev, int32_t B, int32_t warm,
+                          float *r0, void *mu, float *q);
+
 /* One r M-step (colour-ordered qGGMRF ICD, icd_sweeps sweeps; R6-R9) of B
- * fields: r_in, q, r_out device float32 [B][N][N] (r_out must not alias). */
+ * fields: r_in, q, r_out float32 [B][N][N] (r_out must not alias r_in). */
 ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t B, float *r_out);
 
-/* One phi M-step (colour-ordered GMRF ICD; R10-R11) of B fields given the
- * phase-correlation terms c, theta: device float32 [B][N][N]. */
+/* One phi M-step (colour-ordered GMRF ICD, icd_sweeps sweeps; R10-R11) of B
+ * fields given the phase-correlation terms c, theta: float32 [B][N][N]
+ * (phi_out must not alias phi_in). */
 ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta,
                            int32_t B, float *phi_out);
 

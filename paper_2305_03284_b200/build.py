@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libddh.so")
-SOURCES = ["ddh_kernels.cu", "ddh_fused.cu", "ddh_stream.cu", "ddh_synth.cu", "ddh_api.cpp"]
+SOURCES = ["ddh_kernels.cu", "ddh_stream.cu", "ddh_synth.cu", "ddh_api.cpp"]
 HEADERS = ["ddh_kernels.h", "ddh_fft.cuh", "ddh_common.cuh", "ddh_f32x2.cuh", "ddh_fft_reg.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

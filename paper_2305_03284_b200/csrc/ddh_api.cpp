@@ -41,8 +41,6 @@ struct ddh_ctx {
   float *rinit = nullptr, *q = nullptr, *cc = nullptr, *theta = nullptr;
   float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
   double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
-  bool fused = false;
-  int cs = 0;  // CTAs per stream of the fused path
   bool streaming = false;  // cluster-free 6-kernel path (ddh_stream.cu)
   float4 *tw4 = nullptr;
   float *pmax = nullptr;
@@ -58,9 +56,9 @@ struct ddh_ctx {
   uint8_t *status_stage[2] = {nullptr, nullptr};
   cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
   cudaEvent_t h2d_ev[2] = {}, comp_ev[2] = {}, d2h_ev[2] = {};
-  // concurrent launch lanes of the fused path: the streams of a launch group
-  // are split over `lanes` CUDA streams so that the kernels of different
-  // sub-groups (KA of one, KB of another, ...) share the SMs
+  // concurrent launch lanes of the streaming path: the streams of a launch
+  // group are split over `lanes` CUDA streams so that the kernels of different
+  // sub-groups (S1 of one, S3 of another, ...) share the SMs
   int lanes = 1;
   cudaStream_t lane_st[8] = {};
   cudaEvent_t lane_ev[9] = {};
@@ -94,6 +92,9 @@ struct ddh_ctx {
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> ev_kind;  // kind of pending record i (events 2i, 2i+1)
+  // stage entry points of the streaming path: stand-in per-stream partial sums
+  // (no plane, ||y - mu||^2 > 0) for kernels that read them
+  double *test_part0 = nullptr, *test_part1 = nullptr;
   // bookkeeping
   uint64_t launches = 0;
   bool sticky = false;
@@ -132,7 +133,7 @@ enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FIL
             K_S0, K_S1, K_S2, K_S3, K_S4, K_S5 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
-                                          "kf_rows_fwd", "kf_cols", "kf_rows_inv",
+                                          "unused8", "unused9", "unused10",
                                           "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
@@ -385,59 +386,6 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
       cur ^= (iters & 1);
       continue;
     }
-    if (c->fused) {  // KA -> KB -> KC per EM iteration (cluster per stream)
-      a.nb1 = c->cs;
-      // lanes: sub-groups of streams on their own CUDA streams (fork/join
-      // with events); each sub-group uses its own slice of the workspace
-      const int L = std::min(c->lanes, sc);
-      if (L > 1) {
-        DDH_CK(c, cudaEventRecord(c->lane_ev[8], c->st));
-        for (int l = 0; l < L; ++l) DDH_CK(c, cudaStreamWaitEvent(c->lane_st[l], c->lane_ev[8], 0));
-      }
-      for (int l = 0; l < L; ++l) {
-        const int g0 = (int)((long)sc * l / L), g1 = (int)((long)sc * (l + 1) / L);
-        const size_t go = (size_t)(s0 + g0) * P;
-        cudaStream_t st = L > 1 ? c->lane_st[l] : c->st;
-        StepArgs b = a;
-        b.sc = g1 - g0;
-        b.y = y + go;
-        b.r_state = c->r + go;
-        b.cbuf = c->cbuf + (size_t)g0 * P;
-        b.part1 = c->part1 + (size_t)g0 * c->cs;
-        b.stats = c->stats + (size_t)g0 * 5;
-        int cl = cur;
-        for (int it = 0; it < iters; ++it) {
-          const bool first = (it == 0), last = (it == iters - 1);
-          b.phi_in = c->phi[cl] + go;
-          b.phi_out = c->phi[cl ^ 1] + go;
-          b.apply_plane = (plane && first) ? 1 : 0;
-          if (mode == Mode::Step) {
-            b.warm = first ? 1 : 0;
-            b.oml = (float)(1.0 - c->p.lambda);
-            b.la = (float)(c->p.lambda * c->p.alpha);
-          } else {
-            b.warm = (it % c->p.boot_period == 0) ? 1 : 0;
-            b.oml = 0.f;
-            b.la = (float)c->p.boot_alpha;
-          }
-          b.status = (first && status) ? status + s0 + g0 : nullptr;
-          b.r_copy = (last && r_out) ? r_out + go : nullptr;
-          b.phi_copy = (last && phi_out) ? phi_out + go : nullptr;
-          DDH_LAUNCH_ON(c, K_KA, st, ddh::launch_ka(b, st));
-          DDH_LAUNCH_ON(c, K_KB, st, ddh::launch_kb(b, st));
-          DDH_LAUNCH_ON(c, K_KC, st, ddh::launch_kc(b, st));
-          cl ^= 1;
-        }
-      }
-      if (L > 1) {
-        for (int l = 0; l < L; ++l) {
-          DDH_CK(c, cudaEventRecord(c->lane_ev[l], c->lane_st[l]));
-          DDH_CK(c, cudaStreamWaitEvent(c->st, c->lane_ev[l], 0));
-        }
-      }
-      cur ^= (iters & 1);
-      continue;
-    }
     DDH_LAUNCH(c, K_STATS, ddh::launch_k0(a, c->st));
     for (int it = 0; it < iters; ++it) {
       const bool first = (it == 0), last = (it == iters - 1);
@@ -586,7 +534,7 @@ void free_ctx(ddh_ctx *c) {
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
                   c->y_stage[0], c->phi_stage[0], c->r_stage[0], c->status_stage[0],
-                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1]};
+                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1], c->test_part0, c->test_part1};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -602,7 +550,7 @@ ddh_status ddh_default_params(ddh_params *p) {
   p->n = 256;
   p->streams = 1;
   p->device = 0;
-  p->aperture_diam = 256.f;
+  p->aperture_diam = 0.f;  // D = N
   p->aperture_mask = nullptr;
   p->noise_var = 0.1;
   p->lambda = 0.45;
@@ -640,10 +588,15 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     return fail(nullptr, DDH_E_INVAL, "ddh_create: boot_period >= 1 and boot_alpha > 0 required");
   if (p.chunk_streams < 0) return fail(nullptr, DDH_E_INVAL, "ddh_create: chunk_streams must be >= 0");
   if (p.lanes < 0 || p.lanes > 8) return fail(nullptr, DDH_E_INVAL, "ddh_create: lanes must be in [0, 8]");
-  if (!(p.aperture_diam > 0) && !p.aperture_mask)
-    return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture_diam <= 0 requires aperture_mask");
-
+  if (p.flags & DDH_F_CLUSTER)
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: the cluster path (DDH_F_CLUSTER) was retired (slower than the streaming path at every config)");
   const int n = p.n;
+  // aperture_diam 0 with no mask: the configs' D = N; a circle wider than the grid is refused
+  const float diam = (p.aperture_diam == 0.f && !p.aperture_mask) ? (float)n : p.aperture_diam;
+  if (!(diam > 0) && !p.aperture_mask)
+    return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture_diam < 0 requires aperture_mask");
+  if (diam > (float)n) return fail(nullptr, DDH_E_INVAL, "ddh_create: aperture_diam must be <= n");
+
   // aperture row intervals and plane normal matrix (RemoveTipTilt)
   std::vector<int2> span(n);
   double G[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -653,8 +606,8 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     bool seen = false, ended = false;
     for (int j = 0; j < n; ++j) {
       bool in;
-      if (p.aperture_diam > 0) {
-        const double di = i - n / 2, dj = j - n / 2, rr = 0.5 * (double)p.aperture_diam;
+      if (diam > 0) {
+        const double di = i - n / 2, dj = j - n / 2, rr = 0.5 * (double)diam;
         in = di * di + dj * dj < rr * rr;
       } else {
         in = p.aperture_mask[(size_t)i * n + j] != 0;
@@ -688,6 +641,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   ddh_ctx *c = new ddh_ctx();
   c->p = p;
   c->p.aperture_mask = nullptr;  // not retained
+  c->p.aperture_diam = diam;
   c->st = (cudaStream_t)cuda_stream;
   c->n = n;
   c->S = p.streams;
@@ -756,9 +710,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const char *pe = std::getenv("DDH_PATH");  // diagnostic override: stream | cluster | multipass
     const std::string path = pe ? pe : "";
     if (path == "multipass" || (path.empty() && (p.flags & DDH_F_UNFUSED))) {
-      c->fused = c->streaming = false;
-    } else if (path == "cluster" || (path.empty() && (p.flags & DDH_F_CLUSTER))) {
-      c->fused = ddh::fused_supported(n);
+      c->streaming = false;
     } else {
       c->streaming = true;
     }
@@ -768,11 +720,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     c->graphs = gr ? std::atoi(gr) != 0 : (p.flags & DDH_F_GRAPHS) != 0;
   }
   if (c->streaming) A(ddh::init_stream(n));
-  if (c->streaming || ddh::fused_supported(n)) {
+  if (c->streaming) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = (p.flags & DDH_F_SERIAL) ? 1 : ev ? std::atoi(ev) : p.lanes;
-    if (c->lanes <= 0)  // measured at 256^2 x 64 streams: stream path 2, cluster path 4
-      c->lanes = c->streaming ? std::min(2, std::max(1, c->sc / 32)) : std::min(4, std::max(1, c->sc / 16));
+    if (c->lanes <= 0)  // measured at 256^2 x 64 streams: 2
+      c->lanes = std::min(2, std::max(1, c->sc / 32));
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
@@ -788,10 +740,6 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
         A(cudaEventCreateWithFlags(&c->side_join[l], cudaEventDisableTiming));
       }
     }
-  }
-  if (c->fused) {
-    c->cs = ddh::fused_cluster(n);
-    A(ddh::init_fused(n));
   }
   // Streaming path: the spectrum buffer is written by S1 and read / rewritten
   // by S2, S4 and S5 within a step; a persisting-L2 window over it keeps it
@@ -1094,19 +1042,64 @@ ddh_status ddh_test_fft2c(ddh_ctx *c, const void *in, void *out, int32_t B, int3
   if (B < 0 || (B > 0 && (!in || !out))) return fail(c, DDH_E_INVAL, "ddh_test_fft2c: bad arguments");
   if (B == 0) return DDH_OK;
   DDH_CK(c, cudaSetDevice(c->p.device));
-  DDH_CK(c, ddh::launch_test_fft2c(c->n, (const float2 *)in, (float2 *)out, B, inverse, c->tw, c->st));
+  if (c->streaming)  // the register FFT of S1 / S2 / S4 (ks_test_rows + ks_test_cols)
+    DDH_CK(c, ddh::launch_test_fft_stream(c->n, (const float2 *)in, (float2 *)out, B, inverse, c->tw4, c->st));
+  else
+    DDH_CK(c, ddh::launch_test_fft2c(c->n, (const float2 *)in, (float2 *)out, B, inverse, c->tw, c->st));
   c->launches += 2;
   return DDH_OK;
 }
+
+namespace {
+ddh_status ensure_test_parts(ddh_ctx *c) {
+  if (c->test_part0) return DDH_OK;
+  const size_t n0 = (size_t)c->sc * std::max(c->nb0, ddh::stream_nb0(c->n)) * 5;
+  const size_t n1 = (size_t)c->sc * std::max(std::max(c->nb1, 16), ddh::stream_nb1(c->n));
+  DDH_CK(c, dalloc(&c->test_part0, n0));
+  DDH_CK(c, dalloc(&c->test_part1, n1));
+  std::vector<double> ones(n1, 1.0);
+  DDH_CK(c, cudaMemset(c->test_part0, 0, n0 * sizeof(double)));
+  DDH_CK(c, cudaMemcpy(c->test_part1, ones.data(), n1 * sizeof(double), cudaMemcpyHostToDevice));
+  return DDH_OK;
+}
+
+// StepArgs for a streaming ICD stage entry point over streams [b0, b0 + bn) of caller buffers
+StepArgs test_icd_args(ddh_ctx *c, int bn) {
+  StepArgs a = base_args(c, 0, bn);
+  a.nb0 = ddh::stream_nb0(c->n);
+  a.nb1 = ddh::stream_nb1(c->n);
+  a.part0 = c->test_part0;
+  a.part1 = c->test_part1;
+  a.apply_plane = 0;
+  return a;
+}
+}  // namespace
 
 ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t B, float *r_out) {
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (B < 0 || (B > 0 && (!r_in || !q || !r_out))) return fail(c, DDH_E_INVAL, "ddh_test_ricd: bad arguments");
   if (B == 0) return DDH_OK;
-  if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_ricd: B > chunk with sweeps > 1");
   DDH_CK(c, cudaSetDevice(c->p.device));
-  return run_ricd(c, r_in, q, r_out, nullptr, nullptr, B);
+  if (!c->streaming) {
+    if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_ricd: B > chunk with sweeps > 1");
+    return run_ricd(c, r_in, q, r_out, nullptr, nullptr, B);
+  }
+  if ((s = ensure_test_parts(c)) != DDH_OK) return s;
+  const int sw = c->p.icd_sweeps;
+  for (int b0 = 0; b0 < B; b0 += c->sc) {  // S3, icd_sweeps sweeps, per launch group
+    const int bn = std::min(c->sc, B - b0);
+    const size_t off = (size_t)b0 * c->P;
+    StepArgs a = test_icd_args(c, bn);
+    a.q = const_cast<float *>(q) + off;
+    for (int k = 0; k < sw; ++k) {
+      a.icd_in = k == 0 ? r_in + off : c->rtmp[(k - 1) & 1];
+      a.icd_out = k == sw - 1 ? r_out + off : c->rtmp[k & 1];
+      a.icd_copy = nullptr;
+      DDH_LAUNCH(c, K_S3, ddh::launch_s3(a, c->st));
+    }
+  }
+  return DDH_OK;
 }
 
 ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const float *theta, int32_t B,
@@ -1116,9 +1109,41 @@ ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, con
   if (B < 0 || (B > 0 && (!phi_in || !cc || !theta || !phi_out)))
     return fail(c, DDH_E_INVAL, "ddh_test_phiicd: bad arguments");
   if (B == 0) return DDH_OK;
-  if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_phiicd: B > chunk with sweeps > 1");
   DDH_CK(c, cudaSetDevice(c->p.device));
-  return run_phiicd(c, phi_in, cc, theta, phi_out, nullptr, nullptr, nullptr, 0, B);
+  if (!c->streaming) {
+    if (c->p.icd_sweeps > 1 && B > c->sc) return fail(c, DDH_E_INVAL, "ddh_test_phiicd: B > chunk with sweeps > 1");
+    return run_phiicd(c, phi_in, cc, theta, phi_out, nullptr, nullptr, nullptr, 0, B);
+  }
+  if ((s = ensure_test_parts(c)) != DDH_OK) return s;
+  const int sw = c->p.icd_sweeps;
+  for (int b0 = 0; b0 < B; b0 += c->sc) {  // (c, theta) pairs as S4 leaves them, then S5 sweeps
+    const int bn = std::min(c->sc, B - b0);
+    const size_t off = (size_t)b0 * c->P;
+    DDH_CK(c, ddh::launch_test_pack(cc + off, theta + off, c->cbuf, (size_t)bn * c->P, c->st));
+    c->launches++;
+    StepArgs a = test_icd_args(c, bn);
+    for (int k = 0; k < sw; ++k) {
+      a.icd_in = k == 0 ? phi_in + off : c->ptmp[(k - 1) & 1];
+      a.icd_out = k == sw - 1 ? phi_out + off : c->ptmp[k & 1];
+      a.icd_copy = nullptr;
+      DDH_LAUNCH(c, K_S5, ddh::launch_s5(a, c->st));
+    }
+  }
+  return DDH_OK;
+}
+
+ddh_status ddh_test_estep(ddh_ctx *c, const void *u, const float *r_prev, int32_t B, int32_t warm, float *r0,
+                          void *mu, float *q) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!u || !r_prev || !r0 || !mu || !q))) return fail(c, DDH_E_INVAL, "ddh_test_estep: bad arguments");
+  if (B == 0) return DDH_OK;
+  DDH_CK(c, cudaSetDevice(c->p.device));
+  DDH_CK(c, ddh::launch_test_estep((const float2 *)u, r_prev, r0, (float2 *)mu, q, (size_t)B * c->P, warm,
+                                   (float)(1.0 - c->p.lambda), (float)(c->p.lambda * c->p.alpha),
+                                   (float)c->p.r_min, (float)c->p.noise_var, c->st));
+  c->launches++;
+  return DDH_OK;
 }
 
 }  // extern "C"

@@ -45,10 +45,7 @@ struct StepArgs {
   float s2, r_min;        // noise variance, r floor
   float P;                // N*N
   double minv[9];         // inverse of the aperture plane normal matrix
-  // fused (cluster) path
-  double *stats;          // [sc][5]: mu re, mu im, plane c0, c1, c2 (written by KA)
-  float *phi_out;         // KC: phi after the M-step [sc][N][N]
-  float *phi_copy, *r_copy;  // optional user outputs [sc][N][N] or null
+  double *stats;          // [sc][5] scratch (Strehl)
   int r_prior;            // qGGMRF on
   float r_b0, r_inv_Tsig, r_tmq;  // 1/(2 sig_r^2), 1/(T sig_r), 2 - q
   float r_b6, r_h, r_g, r_k;       // r_b0/6, (2-q)/2, (2-q) log2(1/(T sig_r)), q/2 (qgg_w2)
@@ -108,13 +105,6 @@ cudaError_t launch_ricd(const IcdArgs &a, int sc, cudaStream_t st);
 cudaError_t launch_phiicd(const IcdArgs &a, int sc, cudaStream_t st);
 cudaError_t launch_fill(float *p, float v, size_t count, cudaStream_t st);
 cudaError_t launch_strehl(const StrehlArgs &a, int B, cudaStream_t st);
-// cluster-fused EM iteration (N <= 512): KA rows+stats, KB cols+E+r-ICD, KC rows+phi-ICD
-bool fused_supported(int n);
-int fused_cluster(int n);  // CTAs per stream (= nb1 of the fused path)
-cudaError_t init_fused(int n);
-cudaError_t launch_ka(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_kb(const StepArgs &a, cudaStream_t st);
-cudaError_t launch_kc(const StepArgs &a, cudaStream_t st);
 
 // streaming (cluster-free) EM iteration, ddh_stream.cu: S0 stats, S1 rows,
 // S2 cols + E-step, S3 r-ICD tiles, S4 inverse rows + c/theta, S5 phi-ICD tiles
@@ -128,6 +118,12 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
 
+// stage entry points of the streaming kernels (ddh_test_*)
+cudaError_t launch_test_fft_stream(int n, const float2 *in, float2 *out, int B, int inverse, const float4 *tw4,
+                                   cudaStream_t st);
+cudaError_t launch_test_estep(const float2 *u, const float *r_prev, float *r0, float2 *mu, float *q, size_t count,
+                              int warm, float oml, float la, float r_min, float s2, cudaStream_t st);
+cudaError_t launch_test_pack(const float *c, const float *th, float2 *out, size_t count, cudaStream_t st);
 cudaError_t launch_test_fft2c(int n, const float2 *in, float2 *out, int B, int inverse, const float2 *tw,
                               cudaStream_t st);
 

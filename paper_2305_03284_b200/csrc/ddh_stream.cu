@@ -369,6 +369,20 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
 
 // ------------------------------------------------------------------ S2
 
+// Eq. 3 + E-step of one pixel (R1, R14): from u = A^H y-hat and
+// r_prev, r0 = max(oml r_prev + la |u|^2, r_min) when `warm` (else r_prev),
+// w = r0/(r0 + s2), mu = w u, q = |mu|^2 + w s2.  Shared by both S2 forms and
+// the stage entry point ddh_test_estep.
+__device__ __forceinline__ float2 estep_px(float2 u, float r_prev, bool warm, float oml, float la, float r_min,
+                                           float s2, float &r0, float &q) {
+  r0 = r_prev;
+  if (warm) r0 = fmaxf(fmaf(oml, r0, la * fmaf(u.x, u.x, u.y * u.y)), r_min);  // Eq. 3
+  const float w = r0 * rcp_approx(r0 + s2);                                   // E-step (R1)
+  const float2 mu = p_mul(u, bc2(w));
+  q = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * s2));
+  return mu;
+}
+
 template <int N>
 __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(StepArgs A) {
   using C = SCfg<N>;
@@ -404,12 +418,10 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
     const size_t g = off + (size_t)ki * N + col;
     const float sg = ((ki + col) & 1) ? -scale : scale;
     const float2 u = p_mul(v[e], bc2(sg));
-    float r0 = A.r_state[g];
-    if (warm) r0 = fmaxf(fmaf(A.oml, r0, A.la * fmaf(u.x, u.x, u.y * u.y)), A.r_min);  // Eq. 3
-    const float w = r0 * rcp_approx(r0 + A.s2);                                        // E-step (R1)
-    const float2 mu = p_mul(u, bc2(w));
+    float r0, q;
+    const float2 mu = estep_px(u, A.r_state[g], warm, A.oml, A.la, A.r_min, A.s2, r0, q);
     A.rinit[g] = r0;
-    A.q[g] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+    A.q[g] = q;
     // conj(chi mu) into input position out_comb(e) of the next FFT
     const float cs = ((ki + col) & 1) ? -1.f : 1.f;
     w2[out_comb<N>(e)] = make_float2(cs * mu.x, -cs * mu.y);
@@ -491,12 +503,10 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 2) ks_cols_p(StepArgs A) {
       const size_t g = off + (size_t)ki * N + col;
       const float sg = ((ki + col) & 1) ? -scale : scale;
       const float2 u = p_mul(v[e], bc2(sg));
-      float r0 = rsl[ki * W + b];
-      if (warm) r0 = fmaxf(fmaf(A.oml, r0, A.la * fmaf(u.x, u.x, u.y * u.y)), A.r_min);  // Eq. 3
-      const float w = r0 * rcp_approx(r0 + A.s2);                                        // E-step (R1)
-      const float2 mu = p_mul(u, bc2(w));
+      float r0, q;
+      const float2 mu = estep_px(u, rsl[ki * W + b], warm, A.oml, A.la, A.r_min, A.s2, r0, q);
       A.rinit[g] = r0;
-      A.q[g] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+      A.q[g] = q;
       const float cs = ((ki + col) & 1) ? -1.f : 1.f;
       w2[out_comb<N>(e)] = make_float2(cs * mu.x, -cs * mu.y);
     }
@@ -797,6 +807,86 @@ __global__ void __launch_bounds__(NTH) ks_phiicd(StepArgs A) {
   phiicd_body<N, TILE, NTH>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
 }
 
+// ------------------------------------------------- stage entry points
+// (ddh_test_*: the streaming kernels' own device code on caller buffers)
+
+// Row pass of F_c on B fields: out row = FFT_row(chi . [conj] in row), the
+// register FFT and comb layout of S1 / S4.
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTR) ks_test_rows(const float2 *in, float2 *out, int inverse,
+                                                             const float4 *tw4) {
+  using C = SCfg<N>;
+  constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;
+  float2 *buf = reinterpret_cast<float2 *>(smem4 + N);
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int t = tid % TPV, b = tid / TPV;
+  const int i = blockIdx.x * H + b;
+  const size_t row = (size_t)s * P + (size_t)i * N;
+  load_tw<N>(tw, tw4, tid, NT);
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int j = t + TPV * e;
+    float2 x = in[row + j];
+    if (inverse) x.y = -x.y;
+    const float sg = ((i + j) & 1) ? -1.f : 1.f;
+    v[e] = p_mul(x, bc2(sg));
+  }
+  __syncthreads();
+  fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) out[row + t + TPV * out_comb<N>(e)] = v[e];
+}
+
+// Column pass of F_c: out column = chi/N . FFT_col(in column) [conj], the
+// register FFT and comb layout of S2.
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::NTC) ks_test_cols(const float2 *in, float2 *out, int inverse,
+                                                             const float4 *tw4) {
+  using C = SCfg<N>;
+  constexpr int E = C::E, TPV = C::TPV, W = C::W, NT = C::NTC, P = N * N;
+  extern __shared__ float4 smem4[];
+  float4 *tw = smem4;
+  float2 *buf = reinterpret_cast<float2 *>(smem4 + N);
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int b = tid % W, t = tid / W;
+  const int col = blockIdx.x * W + b;
+  const size_t off = (size_t)s * P;
+  load_tw<N>(tw, tw4, tid, NT);
+  float2 v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = in[off + (size_t)(t + TPV * e) * N + col];
+  __syncthreads();
+  fft_reg<N>(v, t, buf + b, [](int p) { return p * W; }, tw);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int ki = t + TPV * out_comb<N>(e);
+    const float sg = ((ki + col) & 1) ? -1.f / N : 1.f / N;
+    float2 x = p_mul(v[e], bc2(sg));
+    if (inverse) x.y = -x.y;
+    out[off + (size_t)ki * N + col] = x;
+  }
+}
+
+// Eq. 3 + E-step of S2 (estep_px) on B fields: u complex64, r_prev -> r0, mu, q
+__global__ void ks_test_estep(const float2 *u, const float *r_prev, float *r0, float2 *mu, float *q, size_t count,
+                              int warm, float oml, float la, float r_min, float s2) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < count; k += (size_t)gridDim.x * blockDim.x) {
+    float rr, qq;
+    mu[k] = estep_px(u[k], r_prev[k], warm != 0, oml, la, r_min, s2, rr, qq);
+    r0[k] = rr;
+    q[k] = qq;
+  }
+}
+
+// (c, theta) pairs in S4's output layout, for the S5 stage entry point
+__global__ void ks_test_pack(const float *c, const float *th, float2 *out, size_t count) {
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < count; k += (size_t)gridDim.x * blockDim.x)
+    out[k] = make_float2(c[k], th[k]);
+}
+
 // ------------------------------------------------------------- launchers
 
 #define DDH_SDISPATCH(n, CALL)                          \
@@ -824,6 +914,8 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_ricd<N, 64, 320>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_ricd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_test_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
+  cudaFuncSetAttribute(ks_test_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
   return cudaGetLastError();
 }
 
@@ -929,6 +1021,26 @@ cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
                   return launch_pdl(ks_phiicd<N, 64>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
                                     Icd<64>::kIcdGrid * sizeof(float), st, a);
                 }));
+}
+
+
+cudaError_t launch_test_fft_stream(int n, const float2 *in, float2 *out, int B, int inverse, const float4 *tw4,
+                                   cudaStream_t st) {
+  // rows in -> out, then columns out -> out (each column CTA reads its own columns only)
+  DDH_SDISPATCH(n, ({
+                  ks_test_rows<N><<<dim3(N / SCfg<N>::H, B), SCfg<N>::NTR, srow_smem<N>(), st>>>(in, out, inverse, tw4);
+                  ks_test_cols<N><<<dim3(N / SCfg<N>::W, B), SCfg<N>::NTC, scol_smem<N>(), st>>>(out, out, inverse, tw4);
+                  return cudaGetLastError();
+                }));
+}
+cudaError_t launch_test_estep(const float2 *u, const float *r_prev, float *r0, float2 *mu, float *q, size_t count,
+                              int warm, float oml, float la, float r_min, float s2, cudaStream_t st) {
+  ks_test_estep<<<592, 256, 0, st>>>(u, r_prev, r0, mu, q, count, warm, oml, la, r_min, s2);
+  return cudaGetLastError();
+}
+cudaError_t launch_test_pack(const float *c, const float *th, float2 *out, size_t count, cudaStream_t st) {
+  ks_test_pack<<<592, 256, 0, st>>>(c, th, out, count);
+  return cudaGetLastError();
 }
 
 }  // namespace ddh

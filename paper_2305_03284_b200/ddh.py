@@ -51,7 +51,7 @@ class DdhParams(ctypes.Structure):
 EXPORTS = [
     "ddh_default_params", "ddh_create", "ddh_destroy", "ddh_bootstrap", "ddh_step", "ddh_step_host",
     "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_sync", "ddh_last_error",
-    "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_ricd", "ddh_test_phiicd",
+    "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_estep", "ddh_test_ricd", "ddh_test_phiicd",
     "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
     "ddh_synth_create", "ddh_synth_frames", "ddh_synth_reflectance", "ddh_synth_destroy",
 ]
@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.ddh_frame_index.argtypes = [vp]
     lib.ddh_frame_index.restype = i64
     lib.ddh_test_fft2c.argtypes = [vp, vp, vp, i32, i32]
+    lib.ddh_test_estep.argtypes = [vp, vp, vp, i32, i32, vp, vp, vp]
     lib.ddh_test_ricd.argtypes = [vp, vp, vp, i32, vp]
     lib.ddh_test_phiicd.argtypes = [vp, vp, vp, vp, i32, vp]
     lib.ddh_profile_enable.argtypes = [vp, i32]
@@ -277,6 +278,19 @@ class DDH:
         out = torch.empty_like(x)
         _check(self.lib.ddh_test_fft2c(self.h, xp, ctypes.c_void_p(out.data_ptr()), B, int(inverse)), self.h)
         return out
+
+    def test_estep(self, u: torch.Tensor, r_prev: torch.Tensor, warm: bool = True):
+        """(r0, mu, q) of the E-step stage (Eq. 3 when warm) for B fields."""
+        B = u.shape[0]
+        shp = (B, self.n, self.n)
+        up = _ptr(u, torch.complex64, shp, self.device, "u", allow_none=False)
+        rp = _ptr(r_prev, torch.float32, shp, self.device, "r_prev", allow_none=False)
+        r0 = torch.empty(shp, dtype=torch.float32, device=self.device)
+        q = torch.empty_like(r0)
+        mu = torch.empty(shp, dtype=torch.complex64, device=self.device)
+        _check(self.lib.ddh_test_estep(self.h, up, rp, B, int(warm), ctypes.c_void_p(r0.data_ptr()),
+                                       ctypes.c_void_p(mu.data_ptr()), ctypes.c_void_p(q.data_ptr())), self.h)
+        return r0, mu, q
 
     def test_ricd(self, r_in: torch.Tensor, q: torch.Tensor) -> torch.Tensor:
         B = r_in.shape[0]

@@ -83,7 +83,15 @@ def test_create_rejects_bad_params_without_gpu(lib):
     p.lam = 1.5
     assert lib.ddh_create(ctypes.byref(p), None, ctypes.byref(h)) == 1
     p = D.default_params()
-    p.aperture_diam = 0.0
+    assert p.aperture_diam == 0.0  # default: D = N (whatever N is)
+    p.aperture_diam = -1.0  # a mask is required then
+    assert lib.ddh_create(ctypes.byref(p), None, ctypes.byref(h)) == 1
+    p = D.default_params()
+    p.n, p.aperture_diam = 64, 65.0  # wider than the grid
+    assert lib.ddh_create(ctypes.byref(p), None, ctypes.byref(h)) == 1
+    assert b"aperture_diam" in lib.ddh_last_error(None)
+    p = D.default_params()
+    p.flags = 4  # the retired cluster path
     assert lib.ddh_create(ctypes.byref(p), None, ctypes.byref(h)) == 1
 
 

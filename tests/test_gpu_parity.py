@@ -3,12 +3,18 @@ the same seeded synthetic frames (-m gpu).
 
 Tolerances (north_star, DESIGN.md "Parity"):
   * per step, from identical FP32 state: max piston-removed wrapped |dphi|
-    over the aperture <= 1e-3 rad and relative L2 r error <= 1e-4, excluding
-    (and counting) pixels where the oracle's r-surrogate has two far-apart
-    candidates within 1e-6 of each other and their 5x5 neighbourhood
-    (SURVEY 8.c.9: "several results are correct");
-  * end to end: per-frame Strehl within 0.01 absolute;
-  * stages: FFT relative L2 <= 3e-6 (FP32 floor ~ eps log2 N), ICDs <= 1e-5.
+    over the WHOLE grid <= 1e-3 rad; relative L2 r error <= 1e-4 and max
+    pointwise relative r error <= 1e-3, over every pixel.  Where the r
+    surrogate has two minima within FP32 evaluation precision of each other
+    ("several results are correct") the oracle is guided to the
+    minimiser the GPU chose (oracle.r_update_pixels(guide=...)): the GPU's
+    choice must be one of the near-optimal candidates, and every later pixel
+    of the sweep is then compared against the same history;
+  * end to end: per-frame phi (piston-removed, wrapped, over the aperture)
+    <= 1e-3 rad and per-frame Strehl within 0.01 absolute, on scenes where the
+    estimate moves (a phi = 0 stand-in fails the same test);
+  * stages (the streaming kernels' own device code): FFT relative L2 <= 3e-6
+    (FP32 floor ~ eps log2 N), E-step <= 1e-6, ICDs <= 1e-5.
 """
 import math
 
@@ -48,7 +54,7 @@ def oracle_params(n, diam=None, **kw):
     return p
 
 
-PATH_FLAGS = {"stream": 0, "cluster": 4, "multipass": 2, False: 0, True: 2}
+PATH_FLAGS = {"stream": 0, "multipass": 2, False: 0, True: 2}
 
 
 def gpu_kwargs(p: O.OracleParams, unfused=False):
@@ -57,25 +63,53 @@ def gpu_kwargs(p: O.OracleParams, unfused=False):
                 boot_alpha=p.boot_alpha, flags=(0 if p.tiptilt else 1) | PATH_FLAGS[unfused])
 
 
-def tie_mask(gaps, thr=1e-6, rad=2):
-    m = gaps < thr
-    out = m.copy()
-    for di in range(-rad, rad + 1):
-        for dj in range(-rad, rad + 1):
-            out |= np.roll(np.roll(m, di, 0), dj, 1)
-    return out
-
-
-def phi_err(phi_g, phi_o, a):
+def phi_err(phi_g, phi_o, a, full=True):
+    """max |wrap(phi_g - phi_o) - piston| over the grid (full) or the aperture;
+    the piston is the circular mean of the difference over the aperture."""
     d = np.angle(np.exp(1j * (phi_g.astype(np.float64) - phi_o)))
-    d = d[a > 0]
-    d = np.angle(np.exp(1j * (d - np.angle(np.mean(np.exp(1j * d))))))
-    return float(np.max(np.abs(d)))
+    pist = np.angle(np.mean(np.exp(1j * d[a > 0])))
+    d = np.angle(np.exp(1j * (d - pist)))
+    return float(np.max(np.abs(d if full else d[a > 0])))
 
 
-def r_err(r_g, r_o, excl):
-    keep = ~excl
-    return float(np.linalg.norm((r_g - r_o)[keep]) / np.linalg.norm(r_o[keep]))
+def r_errs(r_g, r_o):
+    """(relative L2, max pointwise relative) over every pixel."""
+    r_g = r_g.astype(np.float64)
+    return (float(np.linalg.norm(r_g - r_o) / np.linalg.norm(r_o)),
+            float(np.max(np.abs(r_g - r_o) / np.abs(r_o))))
+
+
+def check_step(r_g, phi_g, r_in, phi_in, y, p, a, tol_phi=1e-3, tol_r=1e-4, tol_rmax=1e-3):
+    """One oracle step from (r_in, phi_in) on frame y against the GPU's
+    (r_g, phi_g); near-tie pixels follow the GPU's valid choice (guided
+    oracle).  Returns a dict of the errors and the tie / guided counts."""
+    n = r_in.shape[0]
+    gaps = np.full((n, n), np.inf)
+    r_def, _, _ = O.ddh_step(r_in, phi_in, y, p, a, gaps)
+    r_ref, phi_ref, st = O.ddh_step(r_in, phi_in, y, p, a, guide=r_g.astype(np.float64))
+    ep = phi_err(phi_g, phi_ref, a)
+    er, emax = r_errs(r_g, r_ref)
+    res = {"phi": ep, "r_l2": er, "r_max": emax, "ties": int((gaps < 1e-6).sum()),
+           "guided": int(np.sum(np.abs(r_ref - r_def) > 1e-6 * np.abs(r_def)))}
+    if p.n_k > 1 or p.icd_sweeps > 1:
+        # the GPU's choices at near-ties of earlier sweeps / iterations are not
+        # observable (only the final r is), so the guide is exact for the last
+        # sweep only: the pointwise bound skips the 5x5 neighbourhood of the
+        # near-tie pixels (< 1 % of the grid); the L2 bound covers every pixel
+        near = gaps < 1e-6
+        m = near.copy()
+        for di in range(-2, 3):
+            for dj in range(-2, 3):
+                m |= np.roll(np.roll(near, di, 0), dj, 1)
+        assert m.mean() < 0.01, res
+        emax = float(np.max((np.abs(r_g.astype(np.float64) - r_ref) / np.abs(r_ref))[~m]))
+        res.update(r_max=emax, r_max_skipped=int(m.sum()))
+    assert ep <= tol_phi, res
+    assert er <= tol_r and emax <= tol_rmax, res
+    # validity at near-ties is by construction: the guide may only choose among
+    # candidates within guide_tol of the minimum, so a GPU pixel in a worse
+    # minimum differs from the guided oracle and fails the r bounds above
+    return res
 
 
 def frames(n, S, T, cfg="c1", **over):
@@ -87,12 +121,13 @@ def frames(n, S, T, cfg="c1", **over):
 # ------------------------------------------------------------------ stages
 
 
+@pytest.mark.parametrize("flags", [pytest.param(0, id="stream"), pytest.param(2, id="multipass")])
 @pytest.mark.parametrize("n", [64, 128, 256, 512, 1024])
-def test_fft2c_parity(n):
+def test_fft2c_parity(n, flags):
     g = np.random.default_rng(n)
     B = 3 if n <= 256 else 2
     x = crandn(g, B, n, n)
-    ctx = DDH(n, 1)
+    ctx = DDH(n, 1, flags=flags)
     xt = torch.from_numpy(x).to(DEV)
     for inv in (False, True):
         out = ctx.test_fft2c(xt, inverse=inv).cpu().numpy()
@@ -100,6 +135,26 @@ def test_fft2c_parity(n):
             ref = O.ifft2c(x[b].astype(np.complex128)) if inv else O.fft2c(x[b].astype(np.complex128))
             err = np.linalg.norm(out[b] - ref) / np.linalg.norm(ref)
             assert err < 3e-6, (n, inv, err)
+
+
+@pytest.mark.parametrize("warm", [True, False])
+def test_estep_stage_parity(warm):
+    """S2's Eq. 3 + E-step epilogue (estep_px) against the oracle's warm_start
+    and e_step on the same u, r_prev (FP32 inputs)."""
+    n, B = 64, 3
+    g = np.random.default_rng(17)
+    u = (crandn(g, B, n, n) * 3).astype(np.complex64)
+    r = (g.random((B, n, n)) * 2 + 1e-4).astype(np.float32)
+    p = oracle_params(n, noise_var=0.287)
+    ctx = DDH(n, 1, **gpu_kwargs(p))
+    r0, mu, q = (t.cpu().numpy() for t in ctx.test_estep(torch.from_numpy(u).to(DEV), torch.from_numpy(r).to(DEV), warm))
+    for b in range(B):
+        ub, rb = u[b].astype(np.complex128), r[b].astype(np.float64)
+        r_ref = O.warm_start(rb, ub, p.lam, p.alpha, p.r_min) if warm else rb
+        mu_ref, _, q_ref = O.e_step(ub, r_ref, p.noise_var)
+        assert np.max(np.abs(r0[b] - r_ref) / r_ref) < 1e-6
+        assert np.max(np.abs(mu[b] - mu_ref)) < 1e-6 * np.max(np.abs(mu_ref))
+        assert np.max(np.abs(q[b] - q_ref) / q_ref) < 1e-6
 
 
 def _realistic_rq(n, seed):
@@ -115,8 +170,10 @@ def _realistic_rq(n, seed):
     return r.astype(np.float32), q.astype(np.float32), p
 
 
-@pytest.mark.parametrize("n,kind", [(64, "random"), (256, "random"), (128, "realistic"), (256, "realistic")])
-def test_ricd_stage_parity(n, kind):
+@pytest.mark.parametrize("flags", [pytest.param(0, id="stream"), pytest.param(2, id="multipass")])
+@pytest.mark.parametrize("n,kind,sweeps", [(64, "random", 1), (256, "random", 1), (128, "realistic", 1),
+                                           (256, "realistic", 1), (128, "random", 2)])
+def test_ricd_stage_parity(n, kind, sweeps, flags):
     g = np.random.default_rng(7 + n)
     B = 2
     if kind == "random":
@@ -128,17 +185,26 @@ def test_ricd_stage_parity(n, kind):
         r = np.stack([x[0] for x in rq])
         q = np.stack([x[1] for x in rq])
         p = rq[0][2]
-    ctx = DDH(n, B, **gpu_kwargs(p))
+    p.icd_sweeps = sweeps
+    ctx = DDH(n, B, **dict(gpu_kwargs(p), flags=flags))
     out = ctx.test_ricd(torch.from_numpy(r).to(DEV), torch.from_numpy(q).to(DEV)).cpu().numpy()
+    outs = [out]
+    if sweeps > 1:
+        # every sweep's output, from a one-sweep ctx applied sweep after sweep (the
+        # multi-sweep call runs exactly these launches: checked bit for bit)
+        c1 = DDH(n, B, **dict(gpu_kwargs(p), flags=flags, icd_sweeps=1))
+        cur, outs = torch.from_numpy(r).to(DEV), []
+        for _ in range(sweeps):
+            cur = c1.test_ricd(cur, torch.from_numpy(q).to(DEV))
+            outs.append(cur.cpu().numpy())
+        assert np.array_equal(outs[-1], out)
+    p1 = O.OracleParams(**{**p.__dict__, "icd_sweeps": 1})
     for b in range(B):
-        gaps = np.full((n, n), np.inf)
-        ref = O.r_icd(r[b].astype(np.float64), q[b].astype(np.float64), p, gaps)
-        excl = tie_mask(gaps)
-        assert excl.mean() < 0.03  # double-well pixels (two minima within 1e-6) and their 5x5 halo
-        e = r_err(out[b], ref, excl)
-        assert e < 1e-5, (b, e, int((gaps < 1e-6).sum()))
-        rel = np.abs(out[b] - ref)[~excl] / np.abs(ref[~excl])
-        assert rel.max() < 1e-3
+        ref = r[b].astype(np.float64)
+        for k in range(sweeps):  # follow the GPU at near-ties, sweep by sweep
+            ref = O.r_icd(ref, q[b].astype(np.float64), p1, guide=outs[k][b].astype(np.float64))
+        e, emax = r_errs(out[b], ref)
+        assert e < 1e-5 and emax < 1e-3, (b, e, emax)
 
 
 def test_ricd_prior_off_is_clamp():
@@ -146,21 +212,22 @@ def test_ricd_prior_off_is_clamp():
     g = np.random.default_rng(3)
     r = g.random((1, n, n)).astype(np.float32)
     q = (g.random((1, n, n)) * 1e-3).astype(np.float32)
-    ctx = DDH(n, 1, r_sigma=0.0)
+    ctx = DDH(n, 1, r_sigma=0.0)  # streaming S3 with the prior off
     out = ctx.test_ricd(torch.from_numpy(r).to(DEV), torch.from_numpy(q).to(DEV)).cpu().numpy()
     assert np.array_equal(out[0], np.maximum(q[0], np.float32(1e-4)))
 
 
-@pytest.mark.parametrize("n,prior", [(64, True), (256, True), (128, False)])
-def test_phiicd_stage_parity(n, prior):
+@pytest.mark.parametrize("flags", [pytest.param(0, id="stream"), pytest.param(2, id="multipass")])
+@pytest.mark.parametrize("n,prior,sweeps", [(64, True, 1), (256, True, 1), (128, False, 1), (128, True, 2)])
+def test_phiicd_stage_parity(n, prior, sweeps, flags):
     g = np.random.default_rng(11 + n)
     B = 2
     phi = (g.standard_normal((B, n, n)) * 2).astype(np.float32)
     c = (g.random((B, n, n)) * 5).astype(np.float32)
     c[:, :, : n // 8] = 0.0  # pixels outside an aperture: prior only
     th = g.uniform(-math.pi, math.pi, (B, n, n)).astype(np.float32)
-    p = oracle_params(n, phi_sigma=0.5 if prior else 0.0)
-    ctx = DDH(n, B, **gpu_kwargs(p))
+    p = oracle_params(n, phi_sigma=0.5 if prior else 0.0, icd_sweeps=sweeps)
+    ctx = DDH(n, B, **dict(gpu_kwargs(p), flags=flags))
     out = ctx.test_phiicd(*(torch.from_numpy(v).to(DEV) for v in (phi, c, th))).cpu().numpy()
     for b in range(B):
         ref = O.phi_icd(phi[b].astype(np.float64), c[b].astype(np.float64), th[b].astype(np.float64), p)
@@ -198,20 +265,13 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, unfused=
     assert np.array_equal(r_s.cpu().numpy(), r_g) and np.array_equal(phi_s.cpu().numpy(), phi_g)
     worst = (0.0, 0.0)
     for s in range(S):
-        gaps = np.full((n, n), np.inf)
-        r_ref, phi_ref, st = O.ddh_step(orc.r[s], orc.phi[s], y[1, s], p, a, gaps)
-        excl = tie_mask(gaps)
-        ep = phi_err(phi_g[s], phi_ref, a)
-        er = r_err(r_g[s], r_ref, excl)
-        assert ep <= 1e-3, (s, ep)
-        assert er <= 1e-4, (s, er, int((gaps < 1e-6).sum()))
-        worst = (max(worst[0], ep), max(worst[1], er))
+        res = check_step(r_g[s], phi_g[s], orc.r[s], orc.phi[s], y[1, s], p, a)
+        worst = (max(worst[0], res["phi"]), max(worst[1], res["r_l2"]))
     return worst
 
 
-# the three implementations of the EM iteration: streaming (default), cluster-fused, multi-pass
-PATHS = [pytest.param("stream", id="stream"), pytest.param("cluster", id="cluster"),
-         pytest.param("multipass", id="multipass")]
+# the two implementations of the EM iteration: streaming (default), multi-pass
+PATHS = [pytest.param("stream", id="stream"), pytest.param("multipass", id="multipass")]
 
 
 @pytest.mark.parametrize("unfused", PATHS)
@@ -258,7 +318,7 @@ def test_bootstrap_and_static_parity():
         r_ref, phi_ref, _ = O.bootstrap(y[0, s], p, 5, a)
         # 5 chained iterations from a cold start: FP32 drift stays far inside the per-step bar
         assert phi_err(phi_g[s].cpu().numpy(), phi_ref, a) < 1e-3
-        assert r_err(r_g[s].cpu().numpy(), r_ref, np.zeros((n, n), bool)) < 1e-3
+        assert r_errs(r_g[s].cpu().numpy(), r_ref)[0] < 1e-3
     phi_o = torch.empty((2, S, n, n), device=DEV)
     ctx.static(torch.from_numpy(y).to(DEV), 4, phi_out=phi_o)
     for t in range(2):
@@ -270,30 +330,78 @@ def test_bootstrap_and_static_parity():
 # ---------------------------------------------------------- end to end
 
 
-def test_end_to_end_c1_strehl_parity():
-    """BASELINE config 1: 64x64, bootstrap then 1 EM iteration per frame,
-    16 frames; both sides run free from their own state."""
-    cfg = synth.CONFIGS["c1"]
-    n, T = cfg["n"], cfg["frames"]
-    y, ph, _ = frames(n, 1, T)
-    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, cfg["snr_db"]))
+def _e2e(cfg, T, n_k=1, k_b=0, streams=1):
+    """Both sides run free from their own state over T frames of config `cfg`
+    (bootstrap on frame 0 when k_b > 0, else cold start at frame 0).  Returns
+    per-frame errors and Strehl series (GPU phi, oracle phi, phi = 0)."""
+    n = cfg["n"]
+    y, ph = synth.make_batch(cfg, streams=streams, frames=T, workers=1)
+    p = oracle_params(n, diam=cfg["diam"], noise_var=synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"]), n_k=n_k)
     a = O.aperture_of(p)
-    kb = cfg["k_b"]
-    ctx = DDH(n, 1, **gpu_kwargs(p))
-    ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), kb)
-    phi_o = torch.empty((T - 1, 1, n, n), device=DEV)
-    ctx.step(torch.from_numpy(np.ascontiguousarray(y[1:])).to(DEV), phi_o)
-    strehl_gpu_api = ctx.strehl(phi_o[:, 0].contiguous(), torch.from_numpy(ph[1:, 0]).to(DEV))
-    phi_g = phi_o.cpu().numpy()[:, 0]
-    r, phi, _ = O.bootstrap(y[0, 0], p, kb, a)
-    worst = 0.0
-    for t in range(1, T):
-        r, phi, _ = O.ddh_step(r, phi, y[t, 0], p, a)
-        s_ref = O.strehl(phi, ph[t, 0], a)
-        s_gpu = O.strehl(phi_g[t - 1], ph[t, 0], a)
-        worst = max(worst, abs(s_ref - s_gpu))
-        assert abs(s_gpu - strehl_gpu_api[t - 1]) < 1e-5
-    assert worst <= 0.01, worst
+    ctx = DDH(n, streams, **gpu_kwargs(p))
+    t0 = 0
+    if k_b > 0:
+        ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), k_b)
+        t0 = 1
+    phi_o = torch.empty((T - t0, streams, n, n), device=DEV)
+    r_o = torch.empty_like(phi_o)
+    ctx.step(torch.from_numpy(np.ascontiguousarray(y[t0:])).to(DEV), phi_o, r_o)
+    s_api = [ctx.strehl(phi_o[:, s].contiguous(), torch.from_numpy(np.ascontiguousarray(ph[t0:, s])).to(DEV))
+             for s in range(streams)]
+    phi_g, r_g = phi_o.cpu().numpy(), r_o.cpu().numpy()
+    out = []
+    for s in range(streams):
+        if k_b > 0:
+            r, phi, _ = O.bootstrap(y[0, s], p, k_b, a)
+        else:
+            r, phi = np.full((n, n), p.r_min), np.zeros((n, n))
+        for t in range(t0, T):
+            r, phi, _ = O.ddh_step(r, phi, y[t, s], p, a)
+            k = t - t0
+            out.append(dict(t=t, s=s, phi=phi_err(phi_g[k, s], phi, a, full=False),
+                            phi_zero=phi_err(np.zeros((n, n), np.float32), phi, a, full=False),
+                            r=r_errs(r_g[k, s], r)[0],
+                            S_ref=O.strehl(phi, ph[t, s], a), S_gpu=O.strehl(phi_g[k, s], ph[t, s], a),
+                            S_zero=O.strehl(np.zeros((n, n)), ph[t, s], a), S_api=s_api[s][k]))
+    return out
+
+
+def _assert_e2e(rows, tol_phi=1e-3, tol_r=1e-3, discriminate_strehl=True):
+    worst = {k: max(abs(r_[k]) for r_ in rows) for k in ("phi", "r")}
+    dS = max(abs(r_["S_gpu"] - r_["S_ref"]) for r_ in rows)
+    dS0 = max(abs(r_["S_zero"] - r_["S_ref"]) for r_ in rows)
+    dapi = max(abs(r_["S_gpu"] - r_["S_api"]) for r_ in rows)
+    info = dict(worst, dS=dS, dS_zero=dS0, d_api=dapi)
+    assert worst["phi"] <= tol_phi and worst["r"] <= tol_r and dS <= 0.01, info
+    assert dapi < 1e-5, info  # ddh_strehl vs the oracle's Strehl on the same phi-hat
+    # the test discriminates: a phi-hat = 0 stand-in fails the phi bound (and,
+    # where the estimate moves the Strehl, the Strehl bound too)
+    assert max(r_["phi_zero"] for r_ in rows) > 10 * tol_phi, info
+    if discriminate_strehl:
+        assert dS0 > 0.01, info
+    return info
+
+
+def test_end_to_end_c1():
+    """BASELINE config 1: 64x64, bootstrap (K_b = 50) then 1 EM iteration per
+    frame, 16 frames; phi-hat and r-hat compared on every frame."""
+    cfg = synth.CONFIGS["c1"]
+    _assert_e2e(_e2e(cfg, cfg["frames"], k_b=cfg["k_b"]), discriminate_strehl=False)
+
+
+def test_end_to_end_bar_scene_paper_conditions():
+    """The paper's conditions (256^2, D/r0 = 10, |v| = 0.595 px per
+    frame, SNR 10 dB) on a scene with support (synth bar target), cold start,
+    N_k = 1, 60 frames: the estimate moves the Strehl from ~0.055 to ~0.12, so
+    phi-hat = 0 misses the oracle's Strehl by > 0.01 and the test can fail."""
+    _assert_e2e(_e2e(synth.CONFIGS["paper"], 60))
+
+
+def test_end_to_end_c2():
+    """BASELINE config 2: 256^2, 1 stream, 200 frames, SNR 5 dB, cold start,
+    N_k = 1: phi-hat and r-hat on every frame."""
+    cfg = synth.CONFIGS["c2"]
+    _assert_e2e(_e2e(cfg, cfg["frames"]), discriminate_strehl=False)
 
 
 def test_strehl_parity():
@@ -328,10 +436,8 @@ def test_c3_full_size_sampled_streams():
     r_o = torch.empty_like(phi_o)
     ctx.step(torch.from_numpy(y).to(DEV), phi_o, r_o)
     for s in (0, S - 1):
-        gaps = np.full((n, n), np.inf)
-        r_ref, phi_ref, _ = O.ddh_step(np.full((n, n), p.r_min), np.zeros((n, n)), y[0, s], p, a, gaps)
-        assert phi_err(phi_o[0, s].cpu().numpy(), phi_ref, a) <= 1e-3
-        assert r_err(r_o[0, s].cpu().numpy(), r_ref, tie_mask(gaps)) <= 1e-4
+        check_step(r_o[0, s].cpu().numpy(), phi_o[0, s].cpu().numpy(), np.full((n, n), p.r_min),
+                   np.zeros((n, n)), y[0, s], p, a)
 
 
 @pytest.mark.parametrize("cfgname,S", [("c4", 6), ("c5", 1)])
@@ -346,10 +452,8 @@ def test_large_grid_sampled(cfgname, S):
     r_o = torch.empty_like(phi_o)
     ctx.step(torch.from_numpy(y).to(DEV), phi_o, r_o)
     s = S - 1
-    gaps = np.full((n, n), np.inf)
-    r_ref, phi_ref, _ = O.ddh_step(np.full((n, n), p.r_min), np.zeros((n, n)), y[0, s], p, a, gaps)
-    assert phi_err(phi_o[0, s].cpu().numpy(), phi_ref, a) <= 1e-3
-    assert r_err(r_o[0, s].cpu().numpy(), r_ref, tie_mask(gaps)) <= 1e-4
+    check_step(r_o[0, s].cpu().numpy(), phi_o[0, s].cpu().numpy(), np.full((n, n), p.r_min),
+               np.zeros((n, n)), y[0, s], p, a)
 
 
 # ------------------------------------------------ edge cases / invariants
@@ -437,10 +541,8 @@ def test_kernel_launch_count_and_empty_call():
     y, _, _ = frames(n, S, 1)
     ctx.step(torch.from_numpy(y).to(DEV))
     assert ctx.kernel_launches - l0 == 6  # streaming: S0 S1 S2 S3 S4 S5
-    f = DDH(n, S, noise_var=0.1, flags=4)
-    l0 = f.kernel_launches
-    f.step(torch.from_numpy(y).to(DEV))
-    assert f.kernel_launches - l0 == 3  # cluster-fused: KA KB KC
+    with pytest.raises(Exception, match="retired"):
+        DDH(n, S, noise_var=0.1, flags=4)  # the cluster path is gone
     u = DDH(n, S, noise_var=0.1, flags=2)
     l0 = u.kernel_launches
     u.step(torch.from_numpy(y).to(DEV))
@@ -448,13 +550,13 @@ def test_kernel_launch_count_and_empty_call():
 
 
 def test_fused_and_unfused_paths_agree():
-    """The streaming, cluster-fused and multi-pass kernels compute the same step
+    """The streaming and multi-pass kernels compute the same step
     (FP32 rounding order differs: compare at the parity tolerance, 3 frames)."""
     n, S = 256, 2
     y, _, _ = frames(n, S, 3)
     yt = torch.from_numpy(y).to(DEV)
     outs = []
-    for flags in (2, 0, 4):
+    for flags in (2, 0):
         ctx = DDH(n, S, noise_var=0.2, flags=flags)
         po = torch.empty((3, S, n, n), device=DEV)
         ro = torch.empty_like(po)
@@ -468,7 +570,7 @@ def test_fused_and_unfused_paths_agree():
                 assert np.linalg.norm(o[1][t, s] - outs[0][1][t, s]) / np.linalg.norm(outs[0][1][t, s]) < 1e-3
 
 
-@pytest.mark.parametrize("flags", [0, 4])
+@pytest.mark.parametrize("flags", [0, 1])
 def test_graph_replay_bit_exact(flags):
     """A recurring single-frame call (fixed frame and output buffers) is
     captured into a CUDA graph on its second occurrence and replayed; results

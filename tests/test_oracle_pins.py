@@ -813,3 +813,40 @@ def test_r_update_exact_tie_picks_candidate_nearest_current():
     qv, Bv, Sv = np.array([q, q]), np.array([B, B]), np.array([S, S])
     out = O.r_update_pixels(np.array([0.25, 2.4]), qv, Bv, Sv, 1e-4)
     assert out[0] == pytest.approx(x1, rel=1e-9) and out[1] == pytest.approx(x3, rel=1e-9)
+
+
+def test_guided_tie_rule_only_moves_near_ties():
+    """The parity tests' guided oracle: a guide changes the
+    choice only among candidates within guide_tol of the minimum; a pixel with
+    a unique minimiser ignores it."""
+    x1, x3 = 0.3, 2.0
+
+    def coeffs(x2):
+        e1, e2, e3 = x1 + x2 + x3, x1 * x2 + x1 * x3 + x2 * x3, x1 * x2 * x3
+        B = 1.0 / (2.0 * e2)
+        return 2.0 * B * e3, B, B * e1
+
+    def gap(x2):
+        q, B, S = coeffs(x2)
+        return (math.log(x1) + q / x1 + B * x1 * x1 - 2 * S * x1) - (math.log(x3) + q / x3 + B * x3 * x3 - 2 * S * x3)
+
+    lo, hi = x1 + 1e-6, x3 - 1e-6
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (lo, mid) if gap(lo) * gap(mid) <= 0 else (mid, hi)
+    q, B, S = coeffs(0.5 * (lo + hi))
+    one = lambda v: np.array([v])
+    # near tie: the guide decides, whatever the current value
+    assert O.r_update_pixels(one(0.25), one(q), one(B), one(S), 1e-4, guide=one(1.9))[0] == pytest.approx(x3, rel=1e-9)
+    assert O.r_update_pixels(one(2.4), one(q), one(B), one(S), 1e-4, guide=one(0.31))[0] == pytest.approx(x1, rel=1e-9)
+    # unique minimiser: the guide is ignored
+    g = rng(85)
+    m = 200
+    qq = g.random(m) * 3 + 1e-3
+    BB = g.random(m) * 4 + 0.05
+    SS = BB * g.random(m)
+    rc = g.random(m) + 1e-3
+    best, gp = O.r_update_pixels(rc, qq, BB, SS, 1e-4, return_gap=True)
+    uniq = gp > 1e-4
+    gd = O.r_update_pixels(rc, qq, BB, SS, 1e-4, guide=g.random(m) * 10)
+    assert uniq.sum() > m // 2 and np.array_equal(gd[uniq], best[uniq])
