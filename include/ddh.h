@@ -66,6 +66,12 @@ typedef enum {
                                without it (graph boundaries stop the overlap of
                                consecutive steps)                                 */
 
+#define DDH_F_L2_PERSIST 64u /* opt-in (device-wide side effect): raise the device's
+                               persisting-L2 carve-out to the ctx's spectrum buffer
+                               (<= 48 MiB) and give the ctx's own lane streams an
+                               access-policy window over it (c3: +1.3 %); the last
+                               such ctx on the device restores the previous limit  */
+
 typedef struct ddh_ctx ddh_ctx; /* opaque */
 
 /* Algorithm and layout parameters.  Fill with ddh_default_params() first. */
@@ -110,10 +116,8 @@ ddh_status ddh_default_params(ddh_params *p);
  * which all work of this ctx is enqueued and ordered (the ctx may fork work
  * onto streams of its own and joins them back before returning control to
  * that stream's order).  *out receives the ctx (caller frees it with
- * ddh_destroy).  Synchronous.  Side effect: with multiple lanes the ctx may
- * raise the device's persisting-L2 carve-out to its spectrum buffer's size
- * (<= 48 MiB, its own streams only); the last ctx on the device restores the
- * previous limit in ddh_destroy.
+ * ddh_destroy).  Synchronous.  No device-wide side effect unless
+ * DDH_F_L2_PERSIST is set (see there).
  * Errors: DDH_E_INVAL (params out of range, unsupported N, non-interval mask),
  * DDH_E_NOMEM, DDH_E_CUDA. */
 ddh_status ddh_create(const ddh_params *p, void *cuda_stream, ddh_ctx **out);
@@ -151,9 +155,17 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
  * the download of frame t-1 overlap the step of frame t.  y_host: host
  * complex64 [T][S][N][N] (pinned memory needed for the overlap);
  * phi_out/r_out/status: host [T][S][N][N] / [T][S] or NULL.  Synchronous.
- * Errors as ddh_step, plus DDH_E_NOMEM. */
+ * Errors as ddh_step, plus DDH_E_NOMEM; on an error the copies already
+ * enqueued are waited for before returning. */
 ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out,
                          float *r_out, uint8_t *status);
+
+/* Asynchronous form of ddh_step_host: returns once the T frames are enqueued;
+ * consecutive calls continue one copy/compute pipeline (no drain between
+ * calls).  The caller keeps y_host and the output buffers alive and unread
+ * until ddh_sync(c) returns.  Errors as ddh_step_host. */
+ddh_status ddh_step_host_async(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out,
+                               float *r_out, uint8_t *status);
 
 /* Conventional single-shot DH-MBIR on each of T frame
  * batches independently: cold start, `iters` EM iterations with bootstrap
@@ -176,7 +188,8 @@ ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t f
 ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B,
                       double *strehl_out);
 
-/* Wait for all work enqueued by this ctx. */
+/* Wait for all work enqueued by this ctx (including the downloads of
+ * ddh_step_host_async). */
 ddh_status ddh_sync(ddh_ctx *c);
 
 /* Human-readable description of the last error of c (or of the last failed

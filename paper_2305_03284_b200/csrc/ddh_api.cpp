@@ -56,6 +56,8 @@ struct ddh_ctx {
   uint8_t *status_stage[2] = {nullptr, nullptr};
   cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
   cudaEvent_t h2d_ev[2] = {}, comp_ev[2] = {}, d2h_ev[2] = {};
+  bool host_pending = false;  // an asynchronous host-buffer call is in flight
+  uint64_t host_t = 0;        // frames through the host pipeline since it was last drained
   // concurrent launch lanes of the streaming path: the streams of a launch
   // group are split over `lanes` CUDA streams so that the kernels of different
   // sub-groups (S1 of one, S3 of another, ...) share the SMs
@@ -747,7 +749,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   // 449.7 -> 455.5 k frames/s; a larger carve-out than the buffer, or a
   // partial window over a buffer much larger than L2, does not pay).  The
   // carve-out is a device-wide limit; DDH_L2P=0 disables it (diagnostic).
-  if (c->streaming) {
+  if (c->streaming && (p.flags & DDH_F_L2_PERSIST)) {
     const char *pl = std::getenv("DDH_L2P");
     const size_t cb = SC * P * sizeof(float2);
     int maxp = 0;
@@ -821,6 +823,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
 ddh_status ddh_destroy(ddh_ctx *c) {
   if (!c) return DDH_E_INVAL;
   cudaSetDevice(c->p.device);
+  if (c->d2h_st) cudaStreamSynchronize(c->d2h_st);
   cudaStreamSynchronize(c->st);
   free_ctx(c);
   return DDH_OK;
@@ -875,8 +878,14 @@ ddh_status ddh_static(ddh_ctx *c, const void *y, int32_t T, int32_t iters, float
   return DDH_OK;
 }
 
-ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
-                         uint8_t *status) {
+namespace {
+// Host-buffer path: frame t of the pipeline uses stage k = t & 1.  H2D(t)
+// waits for the step of t-2 (reader of y_stage[k]); the step of t waits for
+// H2D(t) and for D2H(t-2) (reader of the output stages); D2H(t) waits for the
+// step of t.  `host_t` continues across asynchronous calls, so consecutive
+// calls keep the copy pipeline full; a synchronous call (or ddh_sync) drains it.
+ddh_status step_host_impl(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
+                          uint8_t *status, bool sync) {
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (T < 0 || (!y_host && T > 0)) return fail(c, DDH_E_INVAL, "ddh_step_host: bad arguments");
@@ -897,38 +906,69 @@ ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_o
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->d2h_st, cudaStreamNonBlocking);
     if (e != cudaSuccess) return fail(c, DDH_E_NOMEM, "ddh_step_host: staging allocation failed");
   }
-  // frame t uses stage k = t & 1: H2D(t) waits for the step of t-2 (reader of
-  // y_stage[k]); the step of t waits for H2D(t) and for D2H(t-2) (reader of
-  // the output stages); D2H(t) waits for the step of t.
-  DDH_CK(c, cudaEventRecord(c->comp_ev[0], c->st));  // order after prior work on the ctx stream
-  DDH_CK(c, cudaEventRecord(c->comp_ev[1], c->st));
-  DDH_CK(c, cudaEventRecord(c->d2h_ev[0], c->st));
-  DDH_CK(c, cudaEventRecord(c->d2h_ev[1], c->st));
+  // on any error after copies were enqueued: wait for them (best effort) so that
+  // no copy into or out of the caller's host buffers is in flight on return
+  auto drain = [c](ddh_status st) {
+    cudaStreamSynchronize(c->h2d_st);
+    cudaStreamSynchronize(c->d2h_st);
+    cudaGetLastError();
+    c->host_pending = false;
+    return st;
+  };
+#define DDH_HCK(call)                                                                           \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess)                                                                      \
+      return drain(fail(c, DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)));   \
+  } while (0)
+  if (!c->host_pending) {  // order after prior work on the ctx stream (fresh pipeline)
+    DDH_HCK(cudaEventRecord(c->comp_ev[0], c->st));
+    DDH_HCK(cudaEventRecord(c->comp_ev[1], c->st));
+    DDH_HCK(cudaEventRecord(c->d2h_ev[0], c->st));
+    DDH_HCK(cudaEventRecord(c->d2h_ev[1], c->st));
+    c->host_t = 0;
+  }
+  c->host_pending = true;
   for (int t = 0; t < T; ++t) {
-    const int k = t & 1;
-    DDH_CK(c, cudaStreamWaitEvent(c->h2d_st, c->comp_ev[k], 0));
-    DDH_CK(c, cudaMemcpyAsync(c->y_stage[k], (const float2 *)y_host + t * fs, fs * sizeof(float2),
-                              cudaMemcpyHostToDevice, c->h2d_st));
-    DDH_CK(c, cudaEventRecord(c->h2d_ev[k], c->h2d_st));
-    DDH_CK(c, cudaStreamWaitEvent(c->st, c->h2d_ev[k], 0));
-    DDH_CK(c, cudaStreamWaitEvent(c->st, c->d2h_ev[k], 0));
+    const int k = (int)((c->host_t++) & 1);
+    DDH_HCK(cudaStreamWaitEvent(c->h2d_st, c->comp_ev[k], 0));
+    DDH_HCK(cudaMemcpyAsync(c->y_stage[k], (const float2 *)y_host + t * fs, fs * sizeof(float2),
+                            cudaMemcpyHostToDevice, c->h2d_st));
+    DDH_HCK(cudaEventRecord(c->h2d_ev[k], c->h2d_st));
+    DDH_HCK(cudaStreamWaitEvent(c->st, c->h2d_ev[k], 0));
+    DDH_HCK(cudaStreamWaitEvent(c->st, c->d2h_ev[k], 0));
     s = run_frame(c, c->y_stage[k], phi_out ? c->phi_stage[k] : nullptr, r_out ? c->r_stage[k] : nullptr,
                   status ? c->status_stage[k] : nullptr, Mode::Step, c->p.n_k);
-    if (s != DDH_OK) return s;
+    if (s != DDH_OK) return drain(s);
     c->frame += 1;
-    DDH_CK(c, cudaEventRecord(c->comp_ev[k], c->st));
-    DDH_CK(c, cudaStreamWaitEvent(c->d2h_st, c->comp_ev[k], 0));
+    DDH_HCK(cudaEventRecord(c->comp_ev[k], c->st));
+    DDH_HCK(cudaStreamWaitEvent(c->d2h_st, c->comp_ev[k], 0));
     if (phi_out)
-      DDH_CK(c, cudaMemcpyAsync(phi_out + t * fs, c->phi_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
+      DDH_HCK(cudaMemcpyAsync(phi_out + t * fs, c->phi_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
     if (r_out)
-      DDH_CK(c, cudaMemcpyAsync(r_out + t * fs, c->r_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
+      DDH_HCK(cudaMemcpyAsync(r_out + t * fs, c->r_stage[k], fs * sizeof(float), cudaMemcpyDeviceToHost, c->d2h_st));
     if (status)
-      DDH_CK(c, cudaMemcpyAsync(status + (size_t)t * c->S, c->status_stage[k], c->S, cudaMemcpyDeviceToHost, c->d2h_st));
-    DDH_CK(c, cudaEventRecord(c->d2h_ev[k], c->d2h_st));
+      DDH_HCK(cudaMemcpyAsync(status + (size_t)t * c->S, c->status_stage[k], c->S, cudaMemcpyDeviceToHost, c->d2h_st));
+    DDH_HCK(cudaEventRecord(c->d2h_ev[k], c->d2h_st));
   }
-  DDH_CK(c, cudaStreamSynchronize(c->d2h_st));
-  DDH_CK(c, cudaStreamSynchronize(c->st));
+#undef DDH_HCK
+  if (sync) {
+    c->host_pending = false;
+    DDH_CK(c, cudaStreamSynchronize(c->d2h_st));
+    DDH_CK(c, cudaStreamSynchronize(c->st));
+  }
   return DDH_OK;
+}
+}  // namespace
+
+ddh_status ddh_step_host(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
+                         uint8_t *status) {
+  return step_host_impl(c, y_host, T, phi_out, r_out, status, true);
+}
+
+ddh_status ddh_step_host_async(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
+                               uint8_t *status) {
+  return step_host_impl(c, y_host, T, phi_out, r_out, status, false);
 }
 
 ddh_status ddh_get_state(ddh_ctx *c, float *r, float *phi, int64_t *frame_index) {
@@ -997,6 +1037,10 @@ ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, i
 ddh_status ddh_sync(ddh_ctx *c) {
   if (!c) return DDH_E_INVAL;
   DDH_CK(c, cudaSetDevice(c->p.device));
+  if (c->d2h_st) {  // the host-buffer pipeline's downloads (ddh_step_host_async)
+    c->host_pending = false;
+    DDH_CK(c, cudaStreamSynchronize(c->d2h_st));
+  }
   DDH_CK(c, cudaStreamSynchronize(c->st));
   return c->sticky ? DDH_E_STATE : DDH_OK;
 }

@@ -899,6 +899,14 @@ __global__ void ks_test_pack(const float *c, const float *th, float2 *out, size_
     default: return cudaErrorInvalidValue;              \
   }
 
+// SM count of the current device (queried once per device)
+static int device_sms() {
+  static int cache[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  if (!cache[d & 63]) cudaDeviceGetAttribute(&cache[d & 63], cudaDevAttrMultiProcessorCount, d);
+  return cache[d & 63] > 0 ? cache[d & 63] : 1;
+}
 template <int N> static size_t srow_smem() { return N * sizeof(float4) + (size_t)SCfg<N>::H * SCfg<N>::RPITCH * sizeof(float2); }
 template <int N> static size_t srowi_smem() { return srow_smem<N>() + (size_t)SCfg<N>::H * N * sizeof(float2); }
 template <int N> static size_t scol_smem() { return N * sizeof(float4) + (size_t)N * SCfg<N>::W * sizeof(float2); }
@@ -946,7 +954,7 @@ cudaError_t launch_s0(const StepArgs &a, cudaStream_t st) {
 }
 cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   static const int persist = getenv("DDH_S1P") ? atoi(getenv("DDH_S1P")) : 1;
-  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
+  const int sms = device_sms();
   if (persist) {
     DDH_SDISPATCH(a.n, ({
                     const int total = N / SCfg<N>::H * a.sc;
@@ -969,8 +977,7 @@ static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, bool staged_o
 }
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
   static const int staged = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 1;  // diagnostic
-  static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
-  DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged != 0, sms));
+  DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged != 0, device_sms()));
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
@@ -980,7 +987,7 @@ cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
 // single-stream latency, +20 % halo recomputation)
 template <int N>
 static bool small_tiles(int sc) {
-  return N >= 64 && (N / 64) * (N / 64) * sc < 2 * 148;
+  return N >= 64 && (N / 64) * (N / 64) * sc < 2 * device_sms();
 }
 // 16x16 tiles when even 32-tiles would leave most SMs idle (one stream at
 // N <= 256: 256 CTAs with one pass per colour phase; c2 step 26.3 -> 24.7 us
@@ -988,7 +995,7 @@ static bool small_tiles(int sc) {
 template <int N>
 static bool tiny_tiles(int sc) {
   static const int on = getenv("DDH_T16") ? atoi(getenv("DDH_T16")) : 1;
-  return on && (N / 32) * (N / 32) * sc < 148;
+  return on && (N / 32) * (N / 32) * sc < device_sms();
 }
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({

@@ -49,7 +49,7 @@ class DdhParams(ctypes.Structure):
 
 
 EXPORTS = [
-    "ddh_default_params", "ddh_create", "ddh_destroy", "ddh_bootstrap", "ddh_step", "ddh_step_host",
+    "ddh_default_params", "ddh_create", "ddh_destroy", "ddh_bootstrap", "ddh_step", "ddh_step_host", "ddh_step_host_async",
     "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_sync", "ddh_last_error",
     "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_estep", "ddh_test_ricd", "ddh_test_phiicd",
     "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
@@ -76,6 +76,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.ddh_bootstrap.argtypes = [vp, vp, i32, vp]
     lib.ddh_step.argtypes = [vp, vp, i32, vp, vp, vp]
     lib.ddh_step_host.argtypes = [vp, vp, i32, vp, vp, vp]
+    lib.ddh_step_host_async.argtypes = [vp, vp, i32, vp, vp, vp]
     lib.ddh_static.argtypes = [vp, vp, i32, i32, vp, vp, vp]
     lib.ddh_get_state.argtypes = [vp, vp, vp, ctypes.POINTER(i64)]
     lib.ddh_set_state.argtypes = [vp, vp, vp, i64]
@@ -209,13 +210,16 @@ class DDH:
         sp = _ptr(status, torch.uint8, (T, self.S), self.device, "status")
         _check(self.lib.ddh_step(self.h, yp, T, pp, rp, sp), self.h)
 
-    def step_host(self, y: torch.Tensor, phi_out=None, r_out=None, status=None):
+    def step_host(self, y: torch.Tensor, phi_out=None, r_out=None, status=None, asynchronous=False):
+        """ddh_step_host (synchronous) or ddh_step_host_async (then call sync()
+        before reading the outputs or releasing any of the host buffers)."""
         T = y.shape[0]
         yp = _ptr(y, torch.complex64, self._frames(T), None, "y", allow_none=False, host=True)
         pp = _ptr(phi_out, torch.float32, self._frames(T), None, "phi_out", host=True)
         rp = _ptr(r_out, torch.float32, self._frames(T), None, "r_out", host=True)
         sp = _ptr(status, torch.uint8, (T, self.S), None, "status", host=True)
-        _check(self.lib.ddh_step_host(self.h, yp, T, pp, rp, sp), self.h)
+        fn = self.lib.ddh_step_host_async if asynchronous else self.lib.ddh_step_host
+        _check(fn(self.h, yp, T, pp, rp, sp), self.h)
 
     def static(self, y: torch.Tensor, iters: int, phi_out=None, r_out=None, status=None):
         T = y.shape[0]

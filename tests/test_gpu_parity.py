@@ -532,6 +532,28 @@ def test_step_host_matches_device_path():
     assert sb.sum().item() == 0
 
 
+def test_step_host_async_pipeline_matches_device_path():
+    """ddh_step_host_async: consecutive calls continue one copy/compute
+    pipeline; after ddh_sync the host outputs (phi-hat, r-hat, status) equal
+    the device path's, frame for frame."""
+    n, S, T = 64, 2, 5
+    y, _, _ = frames(n, S, T)
+    a = DDH(n, S, noise_var=0.1)
+    b = DDH(n, S, noise_var=0.1)
+    pa = torch.empty((T, S, n, n), device=DEV)
+    ra = torch.empty_like(pa)
+    a.step(torch.from_numpy(y).to(DEV), pa, ra)
+    yh = torch.from_numpy(y).pin_memory()
+    pb = torch.empty((T, S, n, n)).pin_memory()
+    rb = torch.empty((T, S, n, n)).pin_memory()
+    sb = torch.full((T, S), 7, dtype=torch.uint8).pin_memory()
+    for t0, t1 in ((0, 2), (2, 3), (3, 5)):  # calls of 2, 1, 2 frames, one pipeline
+        b.step_host(yh[t0:t1], pb[t0:t1], rb[t0:t1], sb[t0:t1], asynchronous=True)
+    b.sync()
+    assert torch.equal(pa.cpu(), pb) and torch.equal(ra.cpu(), rb)
+    assert sb.sum().item() == 0 and b.get_state()[2] == T
+
+
 def test_kernel_launch_count_and_empty_call():
     n, S = 64, 1
     ctx = DDH(n, S, noise_var=0.1)
