@@ -36,11 +36,21 @@ struct ddh_ctx {
   float *phi[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t frame = 0;
+  // streaming path: RemoveTipTilt sums of the phase state in 2^-24 fixed point,
+  // [2][S][3]; psum[pcur] holds the sums of phi[cur] when psum_valid (written
+  // by the last S5 of the previous frame), so S0 reads only y
+  long long *psum[2] = {nullptr, nullptr};
+  int pcur = 0;
+  bool psum_valid = false;
+  // the S0 y sums of frame t+1 of one call run on the r-ICD side stream of
+  // frame t: the frame batch whose sums are already in part0, or null
+  const void *y_prefetched = nullptr;
   // launch-group workspace
   float2 *cbuf = nullptr;
   float *rinit = nullptr, *q = nullptr, *cc = nullptr, *theta = nullptr;
   float *rtmp[2] = {nullptr, nullptr}, *ptmp[2] = {nullptr, nullptr};
   double *part0 = nullptr, *part1 = nullptr, *stats = nullptr;
+  float *sstat = nullptr;  // streaming path: per-stream scalars of a step [SC][8]
   bool streaming = false;  // cluster-free 6-kernel path (ddh_stream.cu)
   float4 *tw4 = nullptr;
   float *pmax = nullptr;
@@ -77,8 +87,11 @@ struct ddh_ctx {
   struct GraphKey {
     const void *y;
     const void *phi, *r, *st;
-    int cur;
-    bool operator==(const GraphKey &o) const { return y == o.y && phi == o.phi && r == o.r && st == o.st && cur == o.cur; }
+    int cur, pcur;
+    bool pvalid;
+    bool operator==(const GraphKey &o) const {
+      return y == o.y && phi == o.phi && r == o.r && st == o.st && cur == o.cur && pcur == o.pcur && pvalid == o.pvalid;
+    }
   };
   struct GraphEntry {
     GraphKey key;
@@ -97,6 +110,7 @@ struct ddh_ctx {
   // stage entry points of the streaming path: stand-in per-stream partial sums
   // (no plane, ||y - mu||^2 > 0) for kernels that read them
   double *test_part0 = nullptr, *test_part1 = nullptr;
+  float *test_sstat = nullptr;
   // bookkeeping
   uint64_t launches = 0;
   bool sticky = false;
@@ -196,6 +210,7 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
   a.P = (float)c->P;
   std::memcpy(a.minv, c->minv, sizeof(a.minv));
   a.stats = c->stats;
+  a.sstat = c->sstat;
   a.r_prior = c->p.r_sigma > 0 ? 1 : 0;
   if (a.r_prior) {
     a.r_b0 = (float)(1.0 / (2.0 * c->p.r_sigma * c->p.r_sigma));
@@ -287,8 +302,12 @@ enum class Mode { Step, Boot };
 // [S][N][N] of this time step.  Outputs (may be null) are [S][N][N] / [S].
 // Mode::Step: DDH step (Fig. 1).  Mode::Boot: cold start + `iters` iterations
 // with resets every boot_period (bootstrap / static DH-MBIR).
+// y_next: the next frame batch of the same call (streaming path, Step mode:
+// its S0 y sums are computed during this frame, on the r-ICD side stream), or null.
 ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status, Mode mode,
-                     int iters) {
+                     int iters, const float2 *y_next = nullptr) {
+  // (one launch group only: the S0 partials are launch-group workspace)
+  if (mode != Mode::Step || !c->streaming || c->sc < c->S) y_next = nullptr;
   const size_t P = c->P;
   const int cur0 = c->cur;
   const bool plane = (mode == Mode::Step) && !(c->p.flags & DDH_F_NO_TIPTILT);
@@ -330,10 +349,25 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
         b.theta = c->theta + wo;
         b.part0 = c->part0 + (size_t)g0 * nb0 * 5;
         b.part1 = c->part1 + (size_t)g0 * nb1;
+        b.sstat = c->sstat + (size_t)g0 * 8;
         b.want_y = 1;
         b.apply_plane = plane ? 1 : 0;
         b.phi_in = c->phi[cur] + go;
-        DDH_LAUNCH_ON(c, K_S0, st, ddh::launch_s0(b, st));
+        const bool stepm = mode == Mode::Step;
+        b.psum_in = c->psum[c->pcur] + (size_t)(s0 + g0) * 3;
+        long long *psum_next = stepm ? c->psum[c->pcur ^ 1] + (size_t)(s0 + g0) * 3 : nullptr;
+        // S0: the y sums (unless frame t-1 of this call prefetched them) and, when the
+        // fixed-point plane sums of phi are not already there, those too
+        const bool need_plane = plane && !c->psum_valid;
+        const bool y_ready = c->y_prefetched == (const void *)y;
+        if (need_plane)
+          DDH_CK(c, cudaMemsetAsync(b.psum_in, 0, (size_t)b.sc * 3 * sizeof(long long), st));
+        if (!y_ready || need_plane) {
+          b.want_y = y_ready ? 0 : 1;
+          b.apply_plane = need_plane ? 1 : 0;
+          DDH_LAUNCH_ON(c, K_S0, st, ddh::launch_s0(b, st));
+          b.want_y = 1;
+        }
         int cl = cur;
         for (int it = 0; it < iters; ++it) {
           const bool first = (it == 0), last = (it == iters - 1);
@@ -349,6 +383,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.la = (float)c->p.boot_alpha;
           }
           b.status = (first && status) ? status + s0 + g0 : nullptr;
+          b.psum_out = first ? psum_next : nullptr;  // S1 zeroes the next frame's sums
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
           cudaStream_t rst = st;
@@ -363,6 +398,13 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
             DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
           }
+          if (last && y_next) {  // y sums of the next frame of this call, beside S4 / S5
+            StepArgs yb = b;
+            yb.y = y_next + go;
+            yb.want_y = 1;
+            yb.apply_plane = 0;
+            DDH_LAUNCH_ON(c, K_S0, rst, ddh::launch_s0(yb, rst));
+          }
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
           const int plane_it = b.apply_plane;
           for (int k = 0; k < sw; ++k) {  // phi M-step sweeps (plane removed in the first)
@@ -370,7 +412,9 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_out = k == sw - 1 ? c->phi[cl ^ 1] + go : c->ptmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
             b.apply_plane = k == 0 ? plane_it : 0;
+            b.psum_out = (k == sw - 1 && last) ? psum_next : nullptr;  // sums of the frame's phase
             DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+            b.psum_out = nullptr;
           }
           if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
             DDH_CK(c, cudaEventRecord(c->side_join[l], rst));
@@ -415,6 +459,15 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
     }
   }
   c->cur = cur0 ^ (iters & 1);
+  c->y_prefetched = y_next;
+  if (c->streaming) {
+    if (mode == Mode::Step) {
+      c->pcur ^= 1;  // the last S5 left the sums of the new phase in psum[pcur ^ 1]
+      c->psum_valid = true;
+    } else {
+      c->psum_valid = false;  // bootstrap / static: no epilogue sums
+    }
+  }
   return DDH_OK;
 }
 
@@ -422,13 +475,16 @@ constexpr size_t kGraphCache = 16, kKeyWindow = 64;
 
 // One DDH step of one frame batch, replayed from a CUDA graph when this exact
 // call (same frame and output pointers, same phi parity) recurs.
-ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status) {
+ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status,
+                      const float2 *y_next) {
   // Opt-in (DDH_F_GRAPHS) for synchronous per-frame use, where a graph removes
   // the host launch gaps from the frame's latency.  Back-to-back calls are
   // better served by direct launches, whose programmatic dependent launches
   // overlap one step's tail with the next step's head (graph boundaries do not).
-  if (!c->graphs || c->profiling) return run_frame(c, y, phi_out, r_out, status, Mode::Step, c->p.n_k);
-  const ddh_ctx::GraphKey key{y, phi_out, r_out, status, c->cur};
+  if (!c->graphs || c->profiling) return run_frame(c, y, phi_out, r_out, status, Mode::Step, c->p.n_k, y_next);
+  if (c->y_prefetched) return run_frame(c, y, phi_out, r_out, status, Mode::Step, c->p.n_k, y_next);
+  if (y_next) return run_frame(c, y, phi_out, r_out, status, Mode::Step, c->p.n_k, y_next);
+  const ddh_ctx::GraphKey key{y, phi_out, r_out, status, c->cur, c->pcur, c->psum_valid};
   ++c->gclock;
   for (auto &g : c->gcache) {
     if (g.key == key) {
@@ -436,6 +492,7 @@ ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out,
       DDH_CK(c, cudaGraphLaunch(g.exec, c->st));
       c->launches += g.launches;
       c->cur ^= (c->p.n_k & 1);
+      if (c->streaming) c->pcur ^= 1, c->psum_valid = true;
       return DDH_OK;
     }
   }
@@ -448,7 +505,8 @@ ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out,
   // capture the sequence on a private stream standing in for the ctx stream
   // (lane and side streams join through their events); replays go to the ctx stream
   if (!c->cap_st) DDH_CK(c, cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
-  const int cur0 = c->cur;
+  const int cur0 = c->cur, pcur0 = c->pcur;
+  const bool pvalid0 = c->psum_valid;
   const uint64_t l0 = c->launches;
   cudaStream_t user_st = c->st;
   DDH_CK(c, cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
@@ -458,6 +516,8 @@ ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out,
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(c->cap_st, &graph);
   c->cur = cur0;
+  c->pcur = pcur0;
+  c->psum_valid = pvalid0;
   const uint64_t nl = c->launches - l0;
   c->launches = l0;
   if (s != DDH_OK) {
@@ -479,6 +539,7 @@ ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out,
   DDH_CK(c, cudaGraphLaunch(exec, c->st));
   c->launches += nl;
   c->cur ^= (c->p.n_k & 1);
+  if (c->streaming) c->pcur ^= 1, c->psum_valid = true;
   return DDH_OK;
 }
 
@@ -536,7 +597,7 @@ void free_ctx(ddh_ctx *c) {
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
                   c->y_stage[0], c->phi_stage[0], c->r_stage[0], c->status_stage[0],
-                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1], c->test_part0, c->test_part1};
+                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1], c->test_part0, c->test_part1, c->sstat, c->test_sstat, c->psum[0], c->psum[1]};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -686,6 +747,9 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   A(dalloc(&c->part0, SC * std::max(c->nb0, ddh::stream_nb0(n)) * 5));
   A(dalloc(&c->part1, SC * std::max(std::max(c->nb1, 16), ddh::stream_nb1(n))));
   A(dalloc(&c->stats, SC * 5));
+  A(dalloc(&c->sstat, SC * 8));
+  A(dalloc(&c->psum[0], S * 3));
+  A(dalloc(&c->psum[1], S * 3));
   A(dalloc(&c->pmax, SC * c->strehl_nb));
   A(dalloc(&c->rowspan, (size_t)n));
   A(dalloc(&c->tw, (size_t)n));
@@ -783,6 +847,8 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));
   A(cudaMemsetAsync(c->phi[0], 0, S * P * sizeof(float), c->st));
   A(cudaMemsetAsync(c->phi[1], 0, S * P * sizeof(float), c->st));
+  A(cudaMemsetAsync(c->psum[0], 0, S * 3 * sizeof(long long), c->st));  // the sums of phi = 0
+  c->psum_valid = true;
   A(cudaStreamSynchronize(c->st));
   if (e != cudaSuccess) {
     free_ctx(c);
@@ -852,7 +918,8 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
   const size_t fs = (size_t)c->S * c->P;
   for (int t = 0; t < T; ++t) {
     s = step_frame(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
-                   r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr);
+                   r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr,
+                   t + 1 < T ? (const float2 *)y + (t + 1) * fs : nullptr);
     if (s != DDH_OK) return s;
     c->frame += 1;
   }
@@ -988,7 +1055,10 @@ ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t f
   DDH_CK(c, cudaSetDevice(c->p.device));
   const size_t bytes = (size_t)c->S * c->P * sizeof(float);
   if (r) DDH_CK(c, cudaMemcpyAsync(c->r, r, bytes, cudaMemcpyDeviceToDevice, c->st));
-  if (phi) DDH_CK(c, cudaMemcpyAsync(c->phi[c->cur], phi, bytes, cudaMemcpyDeviceToDevice, c->st));
+  if (phi) {
+    DDH_CK(c, cudaMemcpyAsync(c->phi[c->cur], phi, bytes, cudaMemcpyDeviceToDevice, c->st));
+    c->psum_valid = false;  // the next S0 recomputes the RemoveTipTilt sums
+  }
   c->frame = frame_index;
   return DDH_OK;
 }
@@ -1101,6 +1171,8 @@ ddh_status ensure_test_parts(ddh_ctx *c) {
   const size_t n1 = (size_t)c->sc * std::max(std::max(c->nb1, 16), ddh::stream_nb1(c->n));
   DDH_CK(c, dalloc(&c->test_part0, n0));
   DDH_CK(c, dalloc(&c->test_part1, n1));
+  DDH_CK(c, dalloc(&c->test_sstat, (size_t)c->sc * 8));
+  DDH_CK(c, cudaMemset(c->test_sstat, 0, (size_t)c->sc * 8 * sizeof(float)));  // no plane, not degenerate
   std::vector<double> ones(n1, 1.0);
   DDH_CK(c, cudaMemset(c->test_part0, 0, n0 * sizeof(double)));
   DDH_CK(c, cudaMemcpy(c->test_part1, ones.data(), n1 * sizeof(double), cudaMemcpyHostToDevice));
@@ -1114,6 +1186,7 @@ StepArgs test_icd_args(ddh_ctx *c, int bn) {
   a.nb1 = ddh::stream_nb1(c->n);
   a.part0 = c->test_part0;
   a.part1 = c->test_part1;
+  a.sstat = c->test_sstat;
   a.apply_plane = 0;
   return a;
 }

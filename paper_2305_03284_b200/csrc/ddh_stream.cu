@@ -47,6 +47,12 @@ namespace ddh {
 
 namespace {
 
+// Per-stream scalars of a step, written once by the kernel that first has
+// them (S1: mu, plane; S2: kappa, degenerate flag) and read by the later
+// kernels instead of re-reducing the partial sums in every CTA.
+//   [0] Re mu  [1] Im mu  [2..4] plane c0, c1, c2  [5] kappa  [6] degenerate (0 / 1)
+constexpr int kStatW = 8;
+
 constexpr int kSThreads = 256;
 #ifndef DDH_ROW_THREADS
 #define DDH_ROW_THREADS 256
@@ -107,6 +113,42 @@ __device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int 
 #pragma unroll
   for (int k = 0; k < 5; ++k) out[k] = warp_sum(v[k]);  // xor tree: every lane holds the totals
 }
+// RemoveTipTilt normal-equation sums (R17) in 2^-24 fixed point: the
+// sums are exact integers, so any partition and order of the pixels (S0 over
+// row blocks, S5's epilogue over ICD tiles, atomics) gives the same bits.
+// Quantisation 6e-8 rad per pixel; |phi| up to 2^14 rad on 1024^2 stays in range.
+constexpr float kFix = 16777216.f;  // 2^24
+__device__ __forceinline__ long long fix24(float f) { return __float2ll_rn(f * kFix); }
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// Block sum of (s0, sx, sy) and one 64-bit atomic add each into out[0..2]
+__device__ __forceinline__ void plane_sums_add(long long s0, long long sx, long long sy, long long *red,
+                                               long long *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  s0 = warp_sum_ll(s0);
+  sx = warp_sum_ll(sx);
+  sy = warp_sum_ll(sy);
+  if (lane == 0) red[warp * 3] = s0, red[warp * 3 + 1] = sx, red[warp * 3 + 2] = sy;
+  __syncthreads();
+  if (warp == 0) {
+    long long v[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) v[k] = warp_sum_ll(lane < nw ? red[lane * 3 + k] : 0ll);
+    if (lane == 0)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (v[k]) atomicAdd(reinterpret_cast<unsigned long long *>(out + k), (unsigned long long)v[k]);
+  }
+}
+// plane coefficients from the fixed-point sums
+__device__ __forceinline__ void plane_from_fix(const long long *__restrict__ ps, const double *minv, double *c) {
+  const double sums[5] = {0.0, 0.0, (double)ps[0] / kFix, (double)ps[1] / kFix, (double)ps[2] / kFix};
+  plane_from_sums(sums, minv, c);
+}
+
 __device__ __forceinline__ double sum_part1(const double *__restrict__ part1, int nb1, int s) {
   const int lane = threadIdx.x & 31;
   double v = 0.0;
@@ -133,14 +175,15 @@ __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g
 // ||y - mu|| = 0 of R31 stays exact) and accumulated in FP64; phi plane sums:
 // FP32 per-thread partials; FP64 block sums.
 __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
-  __shared__ double red[32 * 5];
+  __shared__ double red[32 * 2];
+  __shared__ long long redl[32 * 3];
   const int n = A.n, lg = 31 - __clz(n);
   const size_t P = (size_t)n * n;
   const int s = blockIdx.y;
   const size_t per = P / A.nb0;
   const size_t base = blockIdx.x * per;
   const size_t off = (size_t)s * P;
-  float v[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+  long long l0 = 0, lx = 0, ly = 0;
   double yr = 0.0, yi = 0.0;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
@@ -160,26 +203,29 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
         const float4 *f4 = reinterpret_cast<const float4 *>(A.phi_in + off + p0);
         const float4 f0 = __ldg(f4), f1 = __ldg(f4 + 1);
         const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-        float s0 = 0.f, sx = 0.f;
+        long long s0 = 0, sx = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int j = j0 + k;
-          const float fk = (j >= sp.x && j < sp.y) ? f[k] : 0.f;
-          s0 += fk;
-          sx = fmaf(fk, (float)(j - n / 2), sx);
+          const long long q = (j >= sp.x && j < sp.y) ? fix24(f[k]) : 0ll;
+          s0 += q;
+          sx += q * (j - n / 2);
         }
-        v[2] += s0;
-        v[3] += sx;
-        v[4] = fmaf(s0, (float)(i - n / 2), v[4]);
+        l0 += s0;
+        lx += sx;
+        ly += s0 * (i - n / 2);
       }
     }
   }
-  double d[5] = {yr, yi, (double)v[2], (double)v[3], (double)v[4]};
-  block_sum<5>(d, red);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + k] = d[k];
+  if (A.want_y) {
+    double d[2] = {yr, yi};
+    block_sum<2>(d, red);
+    if (threadIdx.x == 0) {
+      A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + 0] = d[0];
+      A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + 1] = d[1];
+    }
   }
+  if (A.apply_plane) plane_sums_add(l0, lx, ly, redl, A.psum_in + (size_t)s * 3);
 }
 
 // ------------------------------------------------------------------ S1
@@ -210,9 +256,16 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
   }
   double sums[5], cpl[3] = {0, 0, 0};
   sum_part0(A.part0, A.nb0, s, sums);
-  if (A.apply_plane) plane_from_sums(sums, A.minv, cpl);
+  if (A.apply_plane) plane_from_fix(A.psum_in + (size_t)s * 3, A.minv, cpl);
   const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
   const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
+  if (blockIdx.x == 0 && tid == 0) {  // per-stream scalars for S4 / S5
+    float *st = A.sstat + (size_t)s * kStatW;
+    st[0] = mur;
+    st[1] = mui;
+    if (A.apply_plane) st[2] = c0, st[3] = c1, st[4] = c2;
+    if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0;
+  }
   const int2 sp = __ldg(A.rowspan + i);
   const float pyi = fmaf(c2, (float)(i - N / 2), c0);
   float acc = 0.f;
@@ -331,9 +384,16 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
     const float *fs = reinterpret_cast<const float *>(stg + Q::YB) + b * N;
     double sums[5], cpl[3] = {0, 0, 0};
     sum_part0(A.part0, A.nb0, s, sums);
-    if (A.apply_plane) plane_from_sums(sums, A.minv, cpl);
+    if (A.apply_plane) plane_from_fix(A.psum_in + (size_t)s * 3, A.minv, cpl);
     const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
     const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
+    if (bx == 0 && tid == 0) {  // per-stream scalars for S4 / S5
+      float *ss = A.sstat + (size_t)s * kStatW;
+      ss[0] = mur;
+      ss[1] = mui;
+      if (A.apply_plane) ss[2] = c0, ss[3] = c1, ss[4] = c2;
+      if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0;
+    }
     const int2 sp = __ldg(A.rowspan + i);
     const float pyi = fmaf(c2, (float)(i - N / 2), c0);
     mbar_wait(&mb[st], (k >> 1) & 1);
@@ -406,8 +466,12 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   }
   const double d2 = sum_part1(A.part1, A.nb1, s);
   const bool degenerate = !(d2 > 0.0);
-  if (A.status && blockIdx.x == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+  if (blockIdx.x == 0 && tid == 0) {
+    if (A.status) A.status[s] = degenerate ? 1 : 0;
+    A.sstat[(size_t)s * kStatW + 5] = kappa;
+    A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
+  }
   const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
   fft_reg<N>(v, t, buf + b, [](int p) { return p * W; }, tw);
   const bool warm = A.warm && !degenerate;
@@ -485,8 +549,12 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 2) ks_cols_p(StepArgs A) {
     const float *rsl = reinterpret_cast<const float *>(stage0 + st * Q::STAGE + Q::CB);
     const double d2 = sum_part1(A.part1, A.nb1, s);
     const bool degenerate = !(d2 > 0.0);
-    if (A.status && bx == 0 && tid == 0) A.status[s] = degenerate ? 1 : 0;
     const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+    if (bx == 0 && tid == 0) {
+      if (A.status) A.status[s] = degenerate ? 1 : 0;
+      A.sstat[(size_t)s * kStatW + 5] = kappa;
+      A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
+    }
     const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's group (one newer may be pending)
     __syncthreads();  // every thread's chunks (and the twiddles) visible
@@ -547,11 +615,8 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.cbuf[row + t + TPV * e];
-  double sums[5];
-  sum_part0(A.part0, A.nb0, s, sums);
-  const double d2 = sum_part1(A.part1, A.nb1, s);
-  const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
-  const float kappa = d2 > 0.0 ? (float)sqrt((double)P / d2) : 0.f;
+  const float *stt = A.sstat + (size_t)s * kStatW;  // from S1 (mu) and S2 (kappa)
+  const float mur = stt[0], mui = stt[1], kappa = stt[5];
   __syncthreads();  // twiddles
   fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
   asm volatile("cp.async.wait_group 0;");
@@ -644,7 +709,7 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
       }
     }
   }
-  const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
+  const bool degenerate = A.sstat[(size_t)s * kStatW + 6] != 0.f;
   __syncthreads();
   if (A.r_prior && !degenerate) {
     const float h = A.r_h, g = A.r_g, kq = A.r_k, b6 = A.r_b6, rmin = A.r_min;
@@ -693,28 +758,100 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   }
 }
 
-// phi M-step: one 4-colour sweep of the GMRF ICD (R10-R11) on a 64x64 tile
-// with a 4-pixel halo; free boundary: neighbours outside the frame are absent
-// (value 0 in the tile, excluded from sum b).  The first sweep of a time step
-// subtracts the RemoveTipTilt plane (from the S0 sums) on load.
-template <int N, int TILE, int NTH = kSThreads>
-__device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, const int by, const int s,
-                                            const float *phi_in, float *phi_out, float *phi_copy) {
+// Fixed-column thread map of the ICD tiles: thread t owns sub-column
+// bcol = t mod kSub and the sub-rows arow0 + R k (arow0 = t / kSub), the same
+// slots in every colour phase, so all shared-memory addresses of a phase are
+// one per-thread base plus compile-time offsets and the per-pixel operands
+// from global memory (q, or the (c, theta) pairs) of a whole phase are issued
+// before its first update.  NTH = R kSub threads, KP passes per phase (the
+// last one partial): 64-tiles 8 x 36 = 288 threads (7 CTAs per SM), 32-tiles
+// 10 x 20 = 200, 16-tiles 12 x 12 = 144.
+
+template <int TILE> struct IcdMap;
+template <> struct IcdMap<64> { static constexpr int R = 8; };
+template <> struct IcdMap<32> { static constexpr int R = 10; };
+template <> struct IcdMap<16> { static constexpr int R = 12; };
+template <int TILE> struct IcdT {
   using G = Icd<TILE>;
-  constexpr int T = N < TILE ? N : TILE, P = N * N;
+  static constexpr int R = IcdMap<TILE>::R, NTH = R * G::kSub, KP = (G::kSub + R - 1) / R;
+  static constexpr int MINB = 2048 / NTH < 8 ? 2048 / NTH : 8;
+};
+
+// One colour phase C of the phi-ICD over this thread's slots (free edge: in
+// EDGE tiles, slots outside the frame are absent and the frame-boundary
+// pixels drop their missing neighbours from sum b).
+template <int N, int TILE, int C, bool EDGE>
+__device__ __forceinline__ void phiicd_phase(float *ps, const float2 *cts, int b0, int arow0, int bcol,
+                                             int I0, int J0, float w, bool prior) {
+  using G = Icd<TILE>;
+  using M = IcdT<TILE>;
+  constexpr int R = M::R, KP = M::KP, CI = C >> 1, CJ = C & 1;
+  constexpr int alo = sub_lo(C + 1, CI), ahi = sub_lo(G::kReg - C - 1, CI);
+  constexpr int blo = sub_lo(C + 1, CJ), bhi = sub_lo(G::kReg - C - 1, CJ);
+  const int gj = J0 + CJ;
+  if (bcol < blo || bcol >= bhi || (EDGE && (unsigned)gj >= (unsigned)N)) return;
+  auto okk = [&](int a, int gi) { return a >= alo && a < ahi && (!EDGE || (unsigned)gi < (unsigned)N); };
+  float2 cn = okk(arow0, I0 + CI) ? __ldg(cts + (size_t)(I0 + CI) * N + gj) : make_float2(0.f, 0.f);
+#pragma unroll 1
+  for (int k = 0; k < KP; ++k) {
+    const int a = arow0 + R * k, gi = I0 + 2 * R * k + CI;
+    const float2 ctk = cn;
+    if (k + 1 < KP && okk(a + R, gi + 2 * R)) cn = __ldg(cts + (size_t)(gi + 2 * R) * N + gj);
+    if (!okk(a, gi)) continue;
+    const int o = b0 + R * k * G::kSubP;
+    const float pi_ = ps[o + G::sidx(C, 0, 0)];
+    const float n4 = (ps[o + G::template nidx<CI, CJ, -1, 0>(0, 0)] + ps[o + G::template nidx<CI, CJ, 1, 0>(0, 0)]) +
+                     (ps[o + G::template nidx<CI, CJ, 0, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, 0, 1>(0, 0)]);
+    const float nd = (ps[o + G::template nidx<CI, CJ, -1, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, -1, 1>(0, 0)]) +
+                     (ps[o + G::template nidx<CI, CJ, 1, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, 1, 1>(0, 0)]);
+    const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
+    float sb = 1.f;  // sum of b over the existing neighbours
+    if (EDGE) {
+      const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
+      sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+           (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
+    }
+    ps[o + G::sidx(C, 0, 0)] = phi_update(pi_, ctk.x, ctk.y, nb, sb, w, prior);
+  }
+}
+
+template <int N, int TILE, bool EDGE>
+__device__ __forceinline__ void phiicd_sweep(float *ps, const float2 *cts, int tid, int i0, int j0, float w, bool prior) {
+  using G = Icd<TILE>;
+  const int bcol = tid % G::kSub, arow0 = tid / G::kSub;
+  const int b0 = arow0 * G::kSubP + bcol;
+  const int I0 = i0 - kHalo + 2 * arow0, J0 = j0 - kHalo + 2 * bcol;
+  phiicd_phase<N, TILE, 0, EDGE>(ps, cts, b0, arow0, bcol, I0, J0, w, prior);
+  __syncthreads();
+  phiicd_phase<N, TILE, 1, EDGE>(ps, cts, b0, arow0, bcol, I0, J0, w, prior);
+  __syncthreads();
+  phiicd_phase<N, TILE, 2, EDGE>(ps, cts, b0, arow0, bcol, I0, J0, w, prior);
+  __syncthreads();
+  phiicd_phase<N, TILE, 3, EDGE>(ps, cts, b0, arow0, bcol, I0, J0, w, prior);
+  __syncthreads();
+}
+
+// phi M-step: one 4-colour sweep of the GMRF ICD (R10-R11) on a TILE x TILE
+// tile with a 4-pixel halo; free boundary: neighbours outside the frame are
+// absent (value 0 in the tile, excluded from sum b).  The first sweep of a
+// time step subtracts the RemoveTipTilt plane (S1's per-stream scalars) on load.
+template <int N, int TILE>
+__global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(StepArgs A) {
+  using G = Icd<TILE>;
+  constexpr int NTH = IcdT<TILE>::NTH, T = N < TILE ? N : TILE, P = N * N;
   extern __shared__ float icd_sm[];
   float *ps = icd_sm;
-  const int tid = threadIdx.x;
-  const int i0 = by * T, j0 = bx * T;
+  const int tid = threadIdx.x, s = blockIdx.z;
+  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
   const size_t off = (size_t)s * P;
-  const float *__restrict__ pin = phi_in + off;
+  const float *__restrict__ pin = A.icd_in + off;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
-  double sums[5], cpl[3] = {0, 0, 0};
-  sum_part0(A.part0, A.nb0, s, sums);
-  const bool degenerate = !(sum_part1(A.part1, A.nb1, s) > 0.0);
-  if (A.apply_plane && !degenerate) plane_from_sums(sums, A.minv, cpl);
-  const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
+
+  const float *st = A.sstat + (size_t)s * kStatW;
+  const bool degenerate = st[6] != 0.f;
+  const bool plane = A.apply_plane && !degenerate;
+  const float c0 = plane ? st[2] : 0.f, c1 = plane ? st[3] : 0.f, c2 = plane ? st[4] : 0.f;
   {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
     constexpr int RP = NTH / G::kSub;
     const int pj = tid % G::kSub, r0 = tid / G::kSub;
@@ -738,58 +875,17 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
       }
     }
   }
+  const float2 *cts = A.cbuf + off;  // (c, theta) pairs from S4
   __syncthreads();
   if (!degenerate) {
     const bool prior = A.phi_prior != 0;
     const float w = A.phi_w;
-    const bool edge = i0 == 0 || j0 == 0 || i0 + T == N || j0 + T == N;  // tile touches the frame edge
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int ci = c >> 1, cj = c & 1;
-      const int alo = sub_lo(c + 1, ci), ahi = sub_lo(G::kReg - c - 1, ci);
-      const int blo = sub_lo(c + 1, cj), bhi = sub_lo(G::kReg - c - 1, cj);
-      const int nbb = bhi - blo, cnt = (ahi - alo) * nbb;
-      constexpr int KMAX = (35 * 35 + NTH - 1) / NTH;
-      float Rv[KMAX];
-      int ix[KMAX];
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        const int p = tid + k * NTH;
-        ix[k] = -1;
-        if (p < cnt) {
-          const int a = alo + p / nbb, bb = blo + p % nbb;
-          const int gi = i0 - kHalo + 2 * a + ci, gj = j0 - kHalo + 2 * bb + cj;
-          if (gi < 0 || gi >= N || gj < 0 || gj >= N) continue;  // outside the frame: absent
-          float pi_, n4, nd;
-#define DDH_NB(CI, CJ)                                                                           \
-  pi_ = ps[G::sidx(2 * CI + CJ, a, bb)];                                                             \
-  n4 = (ps[G::template nidx<CI, CJ, -1, 0>(a, bb)] + ps[G::template nidx<CI, CJ, 1, 0>(a, bb)]) +                         \
-       (ps[G::template nidx<CI, CJ, 0, -1>(a, bb)] + ps[G::template nidx<CI, CJ, 0, 1>(a, bb)]);                          \
-  nd = (ps[G::template nidx<CI, CJ, -1, -1>(a, bb)] + ps[G::template nidx<CI, CJ, -1, 1>(a, bb)]) +                       \
-       (ps[G::template nidx<CI, CJ, 1, -1>(a, bb)] + ps[G::template nidx<CI, CJ, 1, 1>(a, bb)]);
-          if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
-#undef DDH_NB
-          const int me = G::sidx(c, a, bb);
-          const size_t g = off + (size_t)gi * N + gj;
-          const float2 ct = __ldg(A.cbuf + g);  // (c, theta) from S4
-          const float cv = ct.x, tv = ct.y;
-          const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
-          float sb = 1.f;  // sum of b over the existing neighbours
-          if (edge) {
-            const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
-            sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
-                 (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
-          }
-          Rv[k] = phi_update(pi_, cv, tv, nb, sb, w, prior);
-          ix[k] = me;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (ix[k] >= 0) ps[ix[k]] = Rv[k];
-      __syncthreads();
-    }
+    if (i0 == 0 || j0 == 0 || i0 + T == N || j0 + T == N)  // tile touches the frame edge
+      phiicd_sweep<N, TILE, true>(ps, cts, tid, i0, j0, w, prior);
+    else
+      phiicd_sweep<N, TILE, false>(ps, cts, tid, i0, j0, w, prior);
   }
+  long long e0 = 0, ex = 0, ey = 0;
   for (int idx = tid; idx < T * (T / 2); idx += NTH) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
@@ -797,14 +893,22 @@ __device__ __forceinline__ void phiicd_body(const StepArgs &A, const int bx, con
     const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
                                 : make_float2(ps[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
                                               ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
-    *reinterpret_cast<float2 *>(phi_out + g) = v;
-    if (phi_copy) *reinterpret_cast<float2 *>(phi_copy + g) = v;
+    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
+    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+    if (A.psum_out) {  // RemoveTipTilt sums of the output phase, for the next frame's S1
+      const int gi = i0 + oi, gj = j0 + 2 * pj;
+      const int2 sp = __ldg(A.rowspan + gi);
+      const long long q0 = (gj >= sp.x && gj < sp.y) ? fix24(v.x) : 0ll;
+      const long long q1 = (gj + 1 >= sp.x && gj + 1 < sp.y) ? fix24(v.y) : 0ll;
+      e0 += q0 + q1;
+      ex += q0 * (gj - N / 2) + q1 * (gj + 1 - N / 2);
+      ey += (q0 + q1) * (gi - N / 2);
+    }
   }
-}
-
-template <int N, int TILE, int NTH = kSThreads>
-__global__ void __launch_bounds__(NTH) ks_phiicd(StepArgs A) {
-  phiicd_body<N, TILE, NTH>(A, blockIdx.x, blockIdx.y, blockIdx.z, A.icd_in, A.icd_out, A.icd_copy);
+  if (A.psum_out) {
+    __shared__ long long redl[32 * 3];
+    plane_sums_add(e0, ex, ey, redl, A.psum_out + (size_t)s * 3);
+  }
 }
 
 // ------------------------------------------------- stage entry points
@@ -921,6 +1025,7 @@ static cudaError_t init_stream_n() {
   cudaFuncSetAttribute(ks_phiicd<N, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_ricd<N, 64, 320>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<64>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_phiicd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
+  cudaFuncSetAttribute(ks_phiicd<N, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<16>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_ricd<N, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(Icd<32>::kIcdGrid * sizeof(float)));
   cudaFuncSetAttribute(ks_test_rows<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)srow_smem<N>());
   cudaFuncSetAttribute(ks_test_cols<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scol_smem<N>());
@@ -997,6 +1102,11 @@ static bool tiny_tiles(int sc) {
   static const int on = getenv("DDH_T16") ? atoi(getenv("DDH_T16")) : 1;
   return on && (N / 32) * (N / 32) * sc < device_sms();
 }
+template <int N, int TILE>
+static cudaError_t launch_icd(void (*k)(StepArgs), const StepArgs &a, cudaStream_t st, size_t smem) {
+  constexpr int T = N < TILE ? N : TILE;
+  return launch_pdl(k, dim3(N / T, N / T, a.sc), dim3(IcdT<TILE>::NTH), smem, st, a);
+}
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
                   if (tiny_tiles<N>(a.sc))
@@ -1016,20 +1126,11 @@ cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
 }
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
-                  if (tiny_tiles<N>(a.sc))
-                    return launch_pdl(ks_phiicd<N, 16>, dim3(N / 16, N / 16, a.sc), dim3(kSThreads),
-                                      Icd<16>::kIcdGrid * sizeof(float), st, a);
-                  if (small_tiles<N>(a.sc)) {
-                    constexpr int T = N < 32 ? N : 32;
-                    return launch_pdl(ks_phiicd<N, 32>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
-                                      Icd<32>::kIcdGrid * sizeof(float), st, a);
-                  }
-                  constexpr int T = N < 64 ? N : 64;
-                  return launch_pdl(ks_phiicd<N, 64>, dim3(N / T, N / T, a.sc), dim3(kSThreads),
-                                    Icd<64>::kIcdGrid * sizeof(float), st, a);
+                  if (tiny_tiles<N>(a.sc)) return launch_icd<N, 16>(ks_phiicd<N, 16>, a, st, Icd<16>::kIcdGrid * sizeof(float));
+                  if (small_tiles<N>(a.sc)) return launch_icd<N, 32>(ks_phiicd<N, 32>, a, st, Icd<32>::kIcdGrid * sizeof(float));
+                  return launch_icd<N, 64>(ks_phiicd<N, 64>, a, st, Icd<64>::kIcdGrid * sizeof(float));
                 }));
 }
-
 
 cudaError_t launch_test_fft_stream(int n, const float2 *in, float2 *out, int B, int inverse, const float4 *tw4,
                                    cudaStream_t st) {
