@@ -221,27 +221,18 @@ def run_ours(args):
     import synth
     from paper_2305_03284_b200 import DDH
     from paper_2305_03284_b200 import sched
-    ws, rank, _ = sched.env_rank()
     cfg = synth.CONFIGS[args.config]
     n, F = cfg["n"], min(args.frames, cfg["frames"])
     nv = synth.recon_noise_var(n, cfg["diam"], cfg["snr_db"])
     P = n * n
-    # ---- weak scaling: cfg["streams"] streams per GPU; rank r owns global
-    # streams [first, first + S) (sched.shard of S * ws streams), seeds per stream
-    first, S = sched.shard(cfg["streams"] * ws, ws, rank)
+    # ---- the scheduler's per-GPU unit (sched.StreamRank): weak scaling, cfg["streams"]
+    # streams per GPU; rank r owns global streams [first, first + S) (sched.shard of
+    # S * ws streams), seeds per global stream, frames staged in this GPU's HBM
     ws, rank, local = dist_setup("nccl")
+    first, S = sched.shard(cfg["streams"] * ws, ws, rank)
+    local = sched.device_of(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    t0 = time.time()
-    if args.synth == "device" and n <= 512:  # on-device synthesiser (libddh ddh_synth_*, N <= 512), same recipe as synth/
-        y_dev = device_frames(cfg, S, F, first, local)
-        torch.cuda.synchronize()
-        y_host = y_dev.cpu().numpy()
-    else:
-        y_host, _ = synth.make_batch(cfg, streams=S, frames=F, first_stream=first, want_phi=False)
-        y_dev = torch.from_numpy(y_host).to(dev)
-    gen_s = time.time() - t0
-    stream = torch.cuda.current_stream(dev)
     extra = {}
     if args.priors_off:  # diagnostic only (isolates the ICD cost); never the reported configuration
         extra = dict(r_sigma=0.0, phi_sigma=0.0)
@@ -249,14 +240,17 @@ def run_ours(args):
         args.path = "multipass"
     # DDH_F_L2_PERSIST (64): the opt-in persisting-L2 window over the spectrum buffer
     extra["flags"] = {"stream": 0, "multipass": 2}[args.path] | (8 if args.serial else 0) | (64 if args.l2_persist else 0)
-    ctx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk, **extra)
+    t0 = time.time()
+    unit = sched.StreamRank(cfg, first, S, local, F, source=args.synth, want_host=True, chunk_streams=args.chunk, **extra)
+    gen_s = time.time() - t0
+    ctx, y_dev, y_host, stream = unit.ctx, unit.y_dev, unit.y_host, unit.stream
     K, W = args.steps, args.warmup
-    for w in range(W):
-        ctx.step(y_dev[w % F:w % F + 1])
+    unit.steps(W)
     # parity sample (rank 0): one GPU step vs the oracle from the same FP32 state
     parity = None
     if rank == 0 and not args.no_parity:
-        parity = quick_parity(ctx, y_dev, y_host, W % F, n, nv, dev)
+        parity = quick_parity(ctx, y_dev, y_host, unit.pos, n, nv, dev)
+        unit.pos = (unit.pos + 1) % F
     torch.cuda.synchronize()
     # ---- timed region: K steps, uninstrumented (the reported value)
     l0 = ctx.kernel_launches
@@ -266,7 +260,7 @@ def run_ours(args):
     clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    run_steps(ctx, y_dev, W, K, F)
+    unit.steps(K)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -284,14 +278,13 @@ def run_ours(args):
     lanes = ctx_lanes(ctx)
     aextra = dict(extra, flags=extra.get("flags", 0) | 8)  # DDH_F_SERIAL
     actx = DDH(n, S, device=local, noise_var=nv, chunk_streams=args.chunk, lanes=1, **aextra)
-    for w in range(W):
-        actx.step(y_dev[w % F:w % F + 1])
+    sched.run_steps(actx, y_dev, 0, W, F)
     actx.profile(True)
     actx.profile_read()
     barrier(ws)
     torch.cuda.synchronize()
     e0.record(stream)
-    run_steps(actx, y_dev, W, K, F)
+    sched.run_steps(actx, y_dev, W, K, F)
     e1.record(stream)
     torch.cuda.synchronize()
     ms_attr = reduce_max(e0.elapsed_time(e1), ws, dev)
@@ -379,43 +372,6 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     del ctx
     return 0
-
-
-def run_steps(ctx, y_dev, start, K, F):
-    """K time steps over the F staged frame batches, cycling from batch `start`:
-    one ddh_step call per run of contiguous batches (the library overlaps the
-    S0 sums of frame t+1 with frame t inside a call)."""
-    done = 0
-    while done < K:
-        t = (start + done) % F
-        T = min(F - t, K - done)
-        ctx.step(y_dev[t:t + T])
-        done += T
-
-
-def device_frames(cfg, S, F, first, local):
-    """Frames of config `cfg` for global streams [first, first+S) from the
-    on-device synthesiser: per-stream D/r0 and flow direction drawn like
-    synth/ (uniform D/r0 range, uniform direction for "random")."""
-    import math
-
-    from paper_2305_03284_b200 import DDHSynth
-    d_r0, vel = [], []
-    for k in range(first, first + S):
-        g = np.random.default_rng([20230504, k])
-        lo_hi = cfg.get("d_r0_range")
-        d_r0.append(lo_hi[0] + (lo_hi[1] - lo_hi[0]) * g.random() if lo_hi else cfg["d_r0"])
-        if cfg["direction"] == "random":
-            th = 2 * math.pi * g.random()
-        elif cfg["direction"] == "angle":
-            th = cfg["angle"]
-        else:
-            th = math.pi / 2  # along +columns
-        vel.append((cfg["flow"] * math.sin(th), cfg["flow"] * math.cos(th)))
-    z = DDHSynth(cfg["n"], S, d_r0=d_r0, velocity=vel, sigma_b=cfg["sigma_b"], snr_db=cfg["snr_db"],
-                 diam=cfg["diam"], seed=20230504 + first, device=local)
-    y, _ = z.frames(0, F, want_phi=False)
-    return y
 
 
 def ctx_lanes(ctx):

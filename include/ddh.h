@@ -188,6 +188,17 @@ ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t f
 ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B,
                       double *strehl_out);
 
+/* Residual phase and residual PSF ("residual phase error"; Fig. 5
+ * caption P:320, tip and tilt removed) of B estimates, with their Strehl
+ * ratios: psi_b = phi_hat_b - phi_true_b minus its LS plane over the aperture
+ * (R26); resid_b = angle(e^{-j psi_b}) in (-pi, pi] on the aperture, 0 off it;
+ * psf_b = |F_c^{-1}(a e^{j psi_b})|^2 / max |F_c^{-1}(a)|^2 (centred; its
+ * maximum is the peak Strehl ratio).  phi_hat, phi_true: device float32
+ * [B][N][N]; resid, psf: device float32 [B][N][N] or NULL; strehl_out: HOST
+ * double [B].  Synchronous.  Errors as ddh_strehl. */
+ddh_status ddh_residual(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, float *resid,
+                        float *psf, double *strehl_out);
+
 /* Wait for all work enqueued by this ctx (including the downloads of
  * ddh_step_host_async). */
 ddh_status ddh_sync(ddh_ctx *c);
@@ -260,7 +271,7 @@ ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, con
  * the batching of frames.  Not the estimator: no part of the DDH-MBIR update. */
 typedef struct ddh_synth ddh_synth; /* opaque */
 
-/* n in {64,128,256,512}; aperture: circle of diameter `diam` px strictly inside,
+/* n in {64,128,256,512,1024}; aperture: circle of diameter `diam` px strictly inside,
  * centre (n/2, n/2); d_r0: host [streams] turbulence strengths D/r0 (0: no
  * turbulence); velocity: host [streams][2] frozen-flow velocity (rows, cols) in
  * px/frame; sigma_b: reflectance blur (px, > 0); snr_db: per-pixel SNR in dB.

@@ -455,6 +455,26 @@ def strehl(phi_hat, phi_true, a, remove_plane: bool = True) -> float:
     return float(num / den)
 
 
+def residual_phase(phi_hat, phi_true, a) -> np.ndarray:
+    """Residual phase error angle(e^{j(phi - phi_hat)}) (Fig. 5 caption
+    P:320: tip and tilt removed): the LS plane of phi_hat - phi over the
+    aperture is removed first (R26), values on the aperture in (-pi, pi],
+    0 elsewhere."""
+    psi = remove_tip_tilt(np.asarray(phi_hat, np.float64) - np.asarray(phi_true, np.float64), a)
+    return np.where(a > 0, np.angle(np.exp(-1j * psi)), 0.0)
+
+
+def residual_psf(phi_hat, phi_true, a) -> np.ndarray:
+    """Residual point-spread function (Fig. 5 caption P:320): the image-plane
+    intensity |F_c^{-1}(a e^{j psi})|^2 of the corrected pupil, normalised by
+    the diffraction-limited peak max|F_c^{-1}(a)|^2, so that its
+    maximum is the peak Strehl ratio of :func:`strehl`."""
+    psi = remove_tip_tilt(np.asarray(phi_hat, np.float64) - np.asarray(phi_true, np.float64), a)
+    num = np.abs(ifft2c(a * np.exp(1j * psi))) ** 2
+    den = np.max(np.abs(ifft2c(a.astype(np.complex128))) ** 2)
+    return num / den
+
+
 def cost_J(r, phi, yhat, p: OracleParams, a=None) -> float:
     """MAP cost of Eq. 2 for a full aperture (a = 1), where A_phi
     is unitary and y ~ CN(0, A(D(r) + s2 I)A^H):

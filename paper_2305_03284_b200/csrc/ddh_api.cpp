@@ -1063,10 +1063,31 @@ ddh_status ddh_set_state(ddh_ctx *c, const float *r, const float *phi, int64_t f
   return DDH_OK;
 }
 
+namespace {
+ddh_status strehl_impl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, double *out, float *resid,
+                       float *psf);
+}
+
 ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, double *out) {
   ddh_status s = check_usable(c);
   if (s != DDH_OK) return s;
   if (B < 0 || (B > 0 && (!phi_hat || !phi_true || !out))) return fail(c, DDH_E_INVAL, "ddh_strehl: bad arguments");
+  return strehl_impl(c, phi_hat, phi_true, B, out, nullptr, nullptr);
+}
+
+ddh_status ddh_residual(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, float *resid,
+                        float *psf, double *strehl_out) {
+  ddh_status s = check_usable(c);
+  if (s != DDH_OK) return s;
+  if (B < 0 || (B > 0 && (!phi_hat || !phi_true || !strehl_out)))
+    return fail(c, DDH_E_INVAL, "ddh_residual: bad arguments");
+  return strehl_impl(c, phi_hat, phi_true, B, strehl_out, resid, psf);
+}
+
+namespace {
+ddh_status strehl_impl(ddh_ctx *c, const float *phi_hat, const float *phi_true, int32_t B, double *out, float *resid,
+                       float *psf) {
+  ddh_status s = DDH_OK;
   DDH_CK(c, cudaSetDevice(c->p.device));
   std::vector<float> pm((size_t)c->sc * c->strehl_nb);
   for (int b0 = 0; b0 < B; b0 += c->sc) {
@@ -1090,6 +1111,9 @@ ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, i
     sa.tw = c->tw;
     sa.cbuf = c->cbuf;
     sa.pmax = c->pmax;
+    sa.resid = resid ? resid + off : nullptr;
+    sa.psf = psf ? psf + off : nullptr;
+    sa.inv_den = (float)(1.0 / c->strehl_den);
     DDH_CK(c, ddh::launch_strehl(sa, bn, c->st));
     c->launches += 2;
     DDH_CK(c, cudaMemcpyAsync(pm.data(), c->pmax, (size_t)bn * c->strehl_nb * sizeof(float),
@@ -1101,8 +1125,10 @@ ddh_status ddh_strehl(ddh_ctx *c, const float *phi_hat, const float *phi_true, i
       out[b0 + b] = m / c->strehl_den;
     }
   }
+  (void)s;
   return DDH_OK;
 }
+}  // namespace
 
 ddh_status ddh_sync(ddh_ctx *c) {
   if (!c) return DDH_E_INVAL;

@@ -28,6 +28,8 @@ template <> struct RPlan<128>  { static constexpr int E = 16, NP = 2, R0 = 16, R
 template <> struct RPlan<256>  { static constexpr int E = 16, NP = 2, R0 = 16, R1 = 16, R2 = 1; };
 template <> struct RPlan<512>  { static constexpr int E = 16, NP = 3, R0 = 16, R1 = 16, R2 = 2; };
 template <> struct RPlan<1024> { static constexpr int E = 16, NP = 3, R0 = 16, R1 = 16, R2 = 4; };
+// (2048: the on-device synthesiser's 2N x 2N screen grid at N = 1024 only)
+template <> struct RPlan<2048> { static constexpr int E = 16, NP = 3, R0 = 16, R1 = 16, R2 = 8; };
 
 // ---- forward DFT butterflies on packed pairs -------------------------------
 

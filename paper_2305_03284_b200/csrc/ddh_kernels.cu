@@ -490,6 +490,10 @@ __global__ void __launch_bounds__(RowCfg<N>::H *(N / FftPlan<N>::E)) ks1_rows(St
       float sn, cs;
       sincosf(psi, &sn, &cs);
       z = ((i + j) & 1) ? make_float2(-cs, -sn) : make_float2(cs, sn);
+      // residual phase angle(e^{j(phi - phi_hat)}) with tip/tilt removed: -psi wrapped
+      if (A.resid) A.resid[off + (size_t)i * N + j] = atan2f(-sn, cs);
+    } else if (A.resid) {
+      A.resid[off + (size_t)i * N + j] = 0.f;
     }
     tile[r * PITCH + j] = z;
   }
@@ -525,7 +529,9 @@ __global__ void __launch_bounds__(ColCfg<N>::W *(N / FftPlan<N>::E)) ks2_cols(St
   float m = 0.f;
   for (int idx = threadIdx.x; idx < N * W; idx += NT) {
     const float2 X = tile[idx];
-    m = fmaxf(m, X.x * X.x + X.y * X.y);
+    const float I = X.x * X.x + X.y * X.y;
+    m = fmaxf(m, I);
+    if (A.psf) A.psf[off + (size_t)(idx / W) * N + c0 + idx % W] = I / ((float)N * (float)N) * A.inv_den;
   }
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;

@@ -91,6 +91,9 @@ struct StrehlArgs {
   const float2 *tw;
   float2 *cbuf;          // [B][N][N]
   float *pmax;           // [B][nb]
+  float *resid;          // optional [B][N][N]: wrapped residual phase (phi_true - phi_hat) - plane, 0 off the aperture
+  float *psf;            // optional [B][N][N]: residual PSF |F_c^{-1}(a e^{j psi})|^2 / max |F_c^{-1} a|^2
+  float inv_den;         // 1 / max |F_c^{-1} a|^2 (psf normalisation)
 };
 
 // Returns the first launch error (cudaGetLastError) of the sequence.

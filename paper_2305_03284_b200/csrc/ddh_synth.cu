@@ -14,7 +14,7 @@
 //   y      a e^{j phi} F_c^{-1}(g) + w, complex64 (Eq. 1)
 // Random numbers: Philox-4x32-10, counter (pixel, frame, stream, purpose),
 // key = seed; Box-Muller in FP32.  Input generation only: none of the
-// estimator's arithmetic.  Supported N: 64 .. 512 (the screen grid 2N <= 1024).
+// estimator's arithmetic.  Supported N: 64 .. 1024 (screen grid 2N <= 2048).
 #include "../../include/ddh.h"
 #include "ddh_common.cuh"
 #include "ddh_fft_reg.cuh"
@@ -64,7 +64,8 @@ template <int M> struct ZCfg {
   static constexpr int E = RPlan<M>::E, TPV = M / E;
   static constexpr int H = (kT / TPV) < 1 ? 1 : kT / TPV;
   static constexpr int NTR = H * TPV;
-  static constexpr int W = (kT / TPV) < 16 ? 16 : kT / TPV;
+  static constexpr int W0 = (kT / TPV) < 16 ? 16 : kT / TPV;
+  static constexpr int W = W0 * TPV > 1024 ? 1024 / TPV : W0;  // <= 1024 threads per column CTA
   static constexpr int NTC = W * TPV;
 };
 
@@ -320,6 +321,7 @@ __global__ void kz_assemble(AsmArgs A) {
     case 256: { constexpr int M = 256; CALL; } break;   \
     case 512: { constexpr int M = 512; CALL; } break;   \
     case 1024: { constexpr int M = 1024; CALL; } break; \
+    case 2048: { constexpr int M = 2048; CALL; } break; \
     default: return cudaErrorInvalidValue;              \
   }
 
@@ -393,7 +395,7 @@ ddh_status ddh_synth_create(int32_t n, float diam, int32_t streams, const double
                             double sigma_b, double snr_db, uint64_t seed, void *cuda_stream, ddh_synth **out) {
   if (!out || !d_r0 || !velocity) return DDH_E_INVAL;
   *out = nullptr;
-  if (!(n == 64 || n == 128 || n == 256 || n == 512) || streams < 1 || !(diam > 0) || !(sigma_b > 0))
+  if (!(n == 64 || n == 128 || n == 256 || n == 512 || n == 1024) || streams < 1 || !(diam > 0) || !(sigma_b > 0))
     return DDH_E_INVAL;
   ddh_synth *z = new ddh_synth();
   z->n = n;

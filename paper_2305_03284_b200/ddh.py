@@ -50,7 +50,7 @@ class DdhParams(ctypes.Structure):
 
 EXPORTS = [
     "ddh_default_params", "ddh_create", "ddh_destroy", "ddh_bootstrap", "ddh_step", "ddh_step_host", "ddh_step_host_async",
-    "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_sync", "ddh_last_error",
+    "ddh_static", "ddh_get_state", "ddh_set_state", "ddh_strehl", "ddh_residual", "ddh_sync", "ddh_last_error",
     "ddh_kernel_launches", "ddh_frame_index", "ddh_test_fft2c", "ddh_test_estep", "ddh_test_ricd", "ddh_test_phiicd",
     "ddh_profile_enable", "ddh_profile_read", "ddh_kind_name",
     "ddh_synth_create", "ddh_synth_frames", "ddh_synth_reflectance", "ddh_synth_destroy",
@@ -81,6 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.ddh_get_state.argtypes = [vp, vp, vp, ctypes.POINTER(i64)]
     lib.ddh_set_state.argtypes = [vp, vp, vp, i64]
     lib.ddh_strehl.argtypes = [vp, vp, vp, i32, ctypes.POINTER(ctypes.c_double)]
+    lib.ddh_residual.argtypes = [vp, vp, vp, i32, vp, vp, ctypes.POINTER(ctypes.c_double)]
     lib.ddh_sync.argtypes = [vp]
     lib.ddh_last_error.argtypes = [vp]
     lib.ddh_last_error.restype = ctypes.c_char_p
@@ -252,6 +253,20 @@ class DDH:
         out = (ctypes.c_double * max(B, 1))()
         _check(self.lib.ddh_strehl(self.h, a, b, B, out), self.h)
         return [out[i] for i in range(B)]
+
+    def residual(self, phi_hat: torch.Tensor, phi_true: torch.Tensor, want_psf: bool = True):
+        """(residual phase, residual PSF or None, Strehl list) of B estimates
+        (ddh_residual: P:273, 320; tip/tilt removed)."""
+        B = phi_hat.shape[0]
+        shp = (B, self.n, self.n)
+        a = _ptr(phi_hat, torch.float32, shp, self.device, "phi_hat", allow_none=False)
+        b = _ptr(phi_true, torch.float32, shp, self.device, "phi_true", allow_none=False)
+        resid = torch.empty(shp, dtype=torch.float32, device=self.device)
+        psf = torch.empty(shp, dtype=torch.float32, device=self.device) if want_psf else None
+        out = (ctypes.c_double * max(B, 1))()
+        _check(self.lib.ddh_residual(self.h, a, b, B, ctypes.c_void_p(resid.data_ptr()),
+                                     ctypes.c_void_p(psf.data_ptr()) if psf is not None else None, out), self.h)
+        return resid, psf, [out[i] for i in range(B)]
 
     def sync(self):
         _check(self.lib.ddh_sync(self.h), self.h)

@@ -660,3 +660,85 @@ def test_kernel_variants_bit_exact():
         outs.append((po, ro))
     for po, ro in outs[1:]:
         assert torch.equal(outs[0][0], po) and torch.equal(outs[0][1], ro)
+
+
+def test_residual_phase_and_psf_parity():
+    """ddh_residual against the oracle: residual phase (wrapped,
+    tip/tilt removed) and the normalised residual PSF, plus its Strehl."""
+    n, B = 256, 2
+    a = O.aperture(n, n)
+    g = np.random.default_rng(9)
+    tru = np.stack([synth.screen_from_coeffs(synth.screen_coeffs(n, n, n / 10.0, g)) for _ in range(B)]).astype(np.float32)
+    hat = (tru + g.standard_normal((B, n, n)) * 0.3).astype(np.float32)
+    ctx = DDH(n, 1)
+    resid, psf, st = ctx.residual(torch.from_numpy(hat).to(DEV), torch.from_numpy(tru).to(DEV))
+    for b in range(B):
+        r_ref = O.residual_phase(hat[b], tru[b], a)
+        d = np.angle(np.exp(1j * (resid[b].cpu().numpy() - r_ref)))
+        assert np.max(np.abs(d)) < 1e-4
+        p_ref = O.residual_psf(hat[b], tru[b], a)
+        assert np.max(np.abs(psf[b].cpu().numpy() - p_ref)) < 1e-5 * p_ref.max() + 1e-7
+        assert abs(st[b] - O.strehl(hat[b], tru[b], a)) < 1e-5
+        assert abs(st[b] - float(psf[b].max())) < 1e-6
+
+
+def test_strehl_sequence_metrics():
+    """metrics.strehl_sequence: per-frame Strehl of several simulations from
+    the on-device synthesiser through ddh_step / ddh_strehl equals the
+    oracle's Strehl of the same phi-hat; box statistics are those of the series."""
+    from paper_2305_03284_b200 import metrics
+    cfg = dict(synth.CONFIGS["c1"])
+    out = metrics.strehl_sequence(cfg, sims=3, frames=6, k_b=10, residual_at=5)
+    S = out["strehl"]
+    a = O.aperture(cfg["n"], cfg["diam"])
+    ph, pt = out["phi_hat"].cpu().numpy(), out["phi_true"].cpu().numpy()
+    for s in range(3):
+        for t in range(6):
+            assert abs(S[s, t] - O.strehl(ph[t, s], pt[t, s], a)) < 1e-5
+    assert np.allclose(out["box"]["median"], np.median(S, axis=0))
+    assert out["residual_psf"].shape == (3, cfg["n"], cfg["n"])
+    assert np.allclose(out["residual_strehl"], S[:, 5], atol=1e-6)
+
+
+def test_run_streams_threads_match_one_context():
+    """sched.run_streams in host-thread mode (two GPU units emulated on one
+    device): each unit runs its contiguous block of streams with its own ctx;
+    the final per-stream states equal one ctx over all streams, bit for bit."""
+    from paper_2305_03284_b200 import sched
+    cfg = dict(synth.CONFIGS["c1"], streams=3)
+    res = sched.run_streams(cfg, steps=5, warmup=2, frames=8, scaling="weak", source="host", devices=[0, 0],
+                            return_state=True)
+    assert res["gpus"] == 2 and res["streams_total"] == 6 and res["frames_per_s"] > 0
+    one = sched.StreamRank(cfg, 0, 6, 0, 8, source="host")
+    one.steps(2 + 5)
+    r1, p1, f1 = one.ctx.get_state()
+    for row in res["per_gpu"]:
+        r, p, f = row["state"]
+        k0, k1 = row["first"], row["first"] + row["streams"]
+        assert f == f1 == 7
+        assert np.array_equal(r, r1[k0:k1].cpu().numpy()) and np.array_equal(p, p1[k0:k1].cpu().numpy())
+
+
+def test_bench_under_torchrun_two_ranks_one_gpu():
+    """bench.py's GPU arm under torchrun with 2 ranks (both on this GPU: the
+    scheduler falls back to gloo for its host-side collectives): one JSON
+    line, n_gpus 2, weak scaling over 2 x 64 streams."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "6", "--warmup", "3",
+           "--frames", "8", "--no-e2e", "--no-latency", "--no-cpu-baseline", "--no-parity"]
+    pr = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert pr.returncode == 0, pr.stderr[-3000:]
+    lines = [l for l in pr.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, pr.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0

@@ -98,3 +98,25 @@ def test_zero_turbulence_high_snr_gives_strehl_one():
     ctx.step(y[1:].contiguous(), po)
     st = ctx.strehl(po[-1], phi[-1])
     assert min(st) > 0.98, st
+
+
+def test_synth_1024_structure_function_and_flow():
+    """N = 1024 (c5; the 2N = 2048 screen grid): the discrete Kolmogorov
+    structure function and a 2 px/frame frozen flow along the columns."""
+    n, S = 1024, 2
+    z = DDHSynth(n, S, d_r0=30.0, velocity=(0.0, 2.0), sigma_b=4.0, snr_db=2.0)
+    y, phi = z.frames(0, 2)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y).all()
+    ph = phi.double().cpu().numpy()
+    a = synth.sim.aperture_mask(n, n) > 0
+    r0 = n / 30.0
+    for d in ((0, 1), (1, 0), (0, 4)):
+        sh = np.roll(np.roll(ph[0], -d[0], 1), -d[1], 2)
+        m = a & np.roll(np.roll(a, -d[0], 0), -d[1], 1)
+        emp = float(np.mean(((sh - ph[0]) ** 2)[:, m]))
+        exp = synth.sim.structure_function_expected(2 * n, 2 * n, r0, d)
+        assert 0.85 * exp < emp < 1.15 * exp, (d, emp, exp)
+    d2 = lambda f: f[..., 1:-1, 2:] - 2 * f[..., 1:-1, 1:-1] + f[..., 1:-1, :-2]
+    a2, b2 = d2(ph[0])[..., :-2], d2(ph[1])[..., 2:]
+    assert np.max(np.abs(a2 - b2)) < 2e-3

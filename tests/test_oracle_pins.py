@@ -850,3 +850,31 @@ def test_guided_tie_rule_only_moves_near_ties():
     uniq = gp > 1e-4
     gd = O.r_update_pixels(rc, qq, BB, SS, 1e-4, guide=g.random(m) * 10)
     assert uniq.sum() > m // 2 and np.array_equal(gd[uniq], best[uniq])
+
+
+def test_residual_phase_and_psf_closed_forms():
+    """Residual phase / PSF: a perfect estimate (up to piston and
+    tilt) leaves zero residual and the diffraction-limited PSF whose peak is 1
+    at the centre; the PSF of any residual carries the aperture's energy
+    (Parseval: sum_k psf_k = N^2 / sum a, since max|F_c^{-1} a|^2 = (sum a)^2 / N^2)
+    and its maximum is the Strehl ratio; the residual is -psi wrapped."""
+    n = 32
+    a = O.aperture(n, 30.0)
+    x, yy = O.plane_coords(n)
+    g = rng(90)
+    phi = g.standard_normal((n, n)) * 2
+    hat = phi + 0.7 + 0.1 * x - 0.05 * yy
+    assert np.max(np.abs(O.residual_phase(hat, phi, a))) < 1e-12
+    psf0 = O.residual_psf(hat, phi, a)
+    assert psf0.max() == pytest.approx(1.0, abs=1e-12) and psf0[n // 2, n // 2] == pytest.approx(1.0, abs=1e-12)
+    dense = np.abs(dense_centred_dft(n).conj().T @ a.ravel()) ** 2  # F_c^{-1} a from the definition
+    assert np.allclose(psf0.ravel(), dense / dense.max(), atol=1e-12)
+    err = g.standard_normal((n, n)) * 0.6
+    psf = O.residual_psf(phi + err, phi, a)
+    assert psf.sum() == pytest.approx(n * n / a.sum(), rel=1e-12)
+    assert psf.max() == pytest.approx(O.strehl(phi + err, phi, a), rel=1e-12)
+    res = O.residual_phase(phi + err, phi, a)
+    ref = -O.remove_tip_tilt(err, a)
+    d = np.angle(np.exp(1j * (res - ref)))
+    assert np.max(np.abs(d[a > 0])) < 1e-12 and np.all(res[a == 0] == 0)
+    assert np.all(np.abs(res) <= math.pi)

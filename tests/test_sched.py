@@ -2,6 +2,7 @@
 timing and per-stream gathers with world_size 2 over gloo.  The per-stream
 inputs a rank synthesises for its shard must equal the single-process ones
 (streams are independent; seeds are per global stream id)."""
+import math
 import os
 import socket
 
@@ -70,3 +71,29 @@ def test_two_rank_gloo_sharding_matches_single_process():
         assert allsums == ref  # both ranks see every stream, identical to one process
         assert tmax == 2.5     # max over ranks
     assert sorted((f, c) for _, f, c, _, _ in res) == [(0, 3), (3, 2)]  # stream s -> rank floor(s G / S)
+
+
+def test_backend_choice_without_enough_gpus(monkeypatch):
+    """NCCL refuses two ranks on one device: with fewer GPUs than local ranks
+    the scheduler's host-side collectives use gloo."""
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "2")
+    import torch
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 1)
+    assert sched.pick_backend("nccl") == "gloo"
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 8)
+    assert sched.pick_backend("nccl") == "nccl"
+    assert sched.pick_backend("gloo") == "gloo"
+
+
+def test_stream_draws_follow_global_stream_ids():
+    """Per-stream turbulence strength and flow direction depend on the global
+    stream id only, so a shard draws exactly the single-process values."""
+    import synth
+    cfg = dict(synth.CONFIGS["c3"])
+    d_all, v_all = sched.stream_draws(cfg, 0, 8)
+    for first, count in (sched.shard(8, 3, r) for r in range(3)):
+        d, v = sched.stream_draws(cfg, first, count)
+        assert d == d_all[first:first + count] and v == v_all[first:first + count]
+    lo, hi = cfg["d_r0_range"]
+    assert all(lo <= x <= hi for x in d_all)
+    assert all(abs(math.hypot(*vv) - cfg["flow"]) < 1e-12 for vv in v_all)
