@@ -10,6 +10,9 @@
 // constant tables (row intervals, 3x3 normal-matrix inverse, twiddles).
 #include "../../include/ddh.h"
 #include "ddh_kernels.h"
+#ifndef DDH_DEBUG_BOUNDS
+#define DDH_DEBUG_BOUNDS 0
+#endif
 
 #include <cuda_runtime.h>
 
@@ -222,6 +225,10 @@ StepArgs base_args(ddh_ctx *c, int s0, int sc) {
     a.r_k = (float)(0.5 * c->p.r_q);
   }
   a.sweeps = c->p.icd_sweeps;
+#if DDH_DEBUG_BOUNDS
+  static const int fault = std::getenv("DDH_DEBUG_FAULT") ? std::atoi(std::getenv("DDH_DEBUG_FAULT")) : 0;
+  a.dbg_fault = fault;
+#endif
   a.phi_prior = c->p.phi_sigma > 0 ? 1 : 0;
   if (a.phi_prior) a.phi_w = (float)(1.0 / (c->p.phi_sigma * c->p.phi_sigma));
   return a;

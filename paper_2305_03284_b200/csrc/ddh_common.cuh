@@ -8,6 +8,29 @@
 
 #include "ddh_f32x2.cuh"
 
+// Bounds-checked debug build (the sanitizer substitute; compute-sanitizer is
+// not available on the GPU pool): -DDDH_DEBUG_BOUNDS=1 turns DDH_DBG checks of
+// shared-memory tile indices, colour-phase ownership and global indices into
+// device traps with a message.  Compiled out otherwise.
+#ifndef DDH_DEBUG_BOUNDS
+#define DDH_DEBUG_BOUNDS 0
+#endif
+#if DDH_DEBUG_BOUNDS
+#include <cstdio>
+#define DDH_DBG(cond)                                                                                   \
+  do {                                                                                                  \
+    if (!(cond)) {                                                                                      \
+      printf("DDH_DEBUG_BOUNDS %s:%d block (%d,%d,%d) thread %d: %s\n", __FILE__, __LINE__, blockIdx.x, \
+             blockIdx.y, blockIdx.z, threadIdx.x, #cond);                                               \
+      __trap();                                                                                         \
+    }                                                                                                   \
+  } while (0)
+#else
+#define DDH_DBG(cond) \
+  do {                \
+  } while (0)
+#endif
+
 namespace ddh {
 
 __device__ __forceinline__ double warp_sum(double v) {

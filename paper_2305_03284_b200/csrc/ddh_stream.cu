@@ -657,6 +657,13 @@ template <int TILE> struct Icd {
   static constexpr int kReg = TILE + 2 * kHalo, kSub = kReg / 2, kSubP = kSub + 1;
   static constexpr int kIcdGrid = 4 * kSub * kSubP;  // floats per colour-separated tile
   static __device__ __forceinline__ int sidx(int c, int a, int b) { return (c * kSub + a) * kSubP + b; }
+  // debug build: index inside the tile, in colour sub-grid `col` (or any other than `not_col`)
+  static __device__ __forceinline__ void chk(int idx, int col, int not_col) {
+    DDH_DBG(idx >= 0 && idx < kIcdGrid);
+    DDH_DBG(idx % kSubP < kSub);                 // never the padding column
+    DDH_DBG(col < 0 || idx / (kSub * kSubP) == col);
+    DDH_DBG(not_col < 0 || idx / (kSub * kSubP) != not_col);
+  }
   // neighbour (di, dj) of a pixel of colour (ci, cj) at sub coords (a, b):
   // colour ((ci+di)&1, (cj+dj)&1), sub coords (a + floor((ci+di)/2), b + floor((cj+dj)/2))
   template <int CI, int CJ, int DI, int DJ>
@@ -703,6 +710,8 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
 #pragma unroll 4
       for (int li = r0; li < G::kReg; li += RP) {
         const float2 v = *reinterpret_cast<const float2 *>(src + (size_t)((i0 - kHalo + li) & (N - 1)) * N);
+        DDH_DBG(li < G::kReg && pj < G::kSub && 2 * pj + 1 < G::kReg);
+        G::chk(G::sidx(2 * (li & 1), li >> 1, pj) + G::kSub * G::kSubP, 2 * (li & 1) + 1, -1);
         float *d = rs + G::sidx(2 * (li & 1), li >> 1, pj);
         d[0] = v.x;                     // colour (li & 1, 0)
         d[G::kSub * G::kSubP] = v.y;    // colour (li & 1, 1)
@@ -731,7 +740,21 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   d2v = rs[G::template nidx<CI, CJ, 1, -1>(a, bb)]; d3 = rs[G::template nidx<CI, CJ, 1, 1>(a, bb)];
         if (c == 0) { DDH_NB(0, 0) } else if (c == 1) { DDH_NB(0, 1) } else if (c == 2) { DDH_NB(1, 0) } else { DDH_NB(1, 1) }
 #undef DDH_NB
+#if DDH_DEBUG_BOUNDS
+        {  // own pixel in sub-grid c; the 8 neighbours in the other sub-grids (no read of a pixel this phase writes)
+          G::chk(G::sidx(c, a, bb), c, -1);
+          if (A.dbg_fault) G::chk(G::sidx(c, a, bb), -1, c);  // injected: "own pixel not of colour c" fails
+          const int ci_ = c >> 1, cj_ = c & 1;
+          for (int di = -1; di <= 1; ++di)
+            for (int dj = -1; dj <= 1; ++dj) {
+              if (!di && !dj) continue;
+              const int ti = ci_ + di, tj = cj_ + dj, pi = ti & 1, pj2 = tj & 1;
+              G::chk(G::sidx(2 * pi + pj2, a + (ti - pi) / 2, bb + (tj - pj2) / 2), -1, c);
+            }
+        }
+#endif
         const int gi = (i0 - kHalo + 2 * a + ci) & (N - 1), gj = (j0 - kHalo + 2 * bb + cj) & (N - 1);
+        DDH_DBG(gi >= 0 && gi < N && gj >= 0 && gj < N);
         const float q = __ldg(qin + (size_t)gi * N + gj);
         const float2 nA = make_float2(n0, n1), nB = make_float2(n2, n3);
         const float2 dA = make_float2(d0, d1), dB = make_float2(d2v, d3);
@@ -748,6 +771,8 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
     const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
     const int li = oi + kHalo;
     const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
+    DDH_DBG(i0 + oi < N && j0 + 2 * pj + 1 < N && gidx + 1 < (size_t)A.sc * P);
+    G::chk(G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2), 2 * (li & 1) + 1, -1);
     float2 v = make_float2(rs[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)], rs[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
     if (!A.r_prior && !degenerate) {
       const float2 qv = *reinterpret_cast<const float2 *>(A.q + gidx);
@@ -799,6 +824,15 @@ __device__ __forceinline__ void phiicd_phase(float *ps, const float2 *cts, int b
     if (k + 1 < KP && okk(a + R, gi + 2 * R)) cn = __ldg(cts + (size_t)(gi + 2 * R) * N + gj);
     if (!okk(a, gi)) continue;
     const int o = b0 + R * k * G::kSubP;
+#if DDH_DEBUG_BOUNDS
+    DDH_DBG(o == G::sidx(0, a, bcol));
+    G::chk(o + G::sidx(C, 0, 0), C, -1);
+    G::chk(o + G::template nidx<CI, CJ, -1, 0>(0, 0), -1, C); G::chk(o + G::template nidx<CI, CJ, 1, 0>(0, 0), -1, C);
+    G::chk(o + G::template nidx<CI, CJ, 0, -1>(0, 0), -1, C); G::chk(o + G::template nidx<CI, CJ, 0, 1>(0, 0), -1, C);
+    G::chk(o + G::template nidx<CI, CJ, -1, -1>(0, 0), -1, C); G::chk(o + G::template nidx<CI, CJ, -1, 1>(0, 0), -1, C);
+    G::chk(o + G::template nidx<CI, CJ, 1, -1>(0, 0), -1, C); G::chk(o + G::template nidx<CI, CJ, 1, 1>(0, 0), -1, C);
+    DDH_DBG(!EDGE || ((unsigned)gi < (unsigned)N && (unsigned)gj < (unsigned)N));
+#endif
     const float pi_ = ps[o + G::sidx(C, 0, 0)];
     const float n4 = (ps[o + G::template nidx<CI, CJ, -1, 0>(0, 0)] + ps[o + G::template nidx<CI, CJ, 1, 0>(0, 0)]) +
                      (ps[o + G::template nidx<CI, CJ, 0, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, 0, 1>(0, 0)]);
