@@ -151,7 +151,7 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
 /* Same as ddh_step with HOST buffers (the end-to-end path): for each t the
  * frame batch y_t is copied host->device, stepped, and phi/r/status of that
  * step copied device->host.  The copies run on their own CUDA streams with
- * double-buffered device staging, so for T > 1 the upload of frame t+1 and
+ * triple-buffered device staging, so for T > 1 the upload of frame t+1 and
  * the download of frame t-1 overlap the step of frame t.  y_host: host
  * complex64 [T][S][N][N] (pinned memory needed for the overlap);
  * phi_out/r_out/status: host [T][S][N][N] / [T][S] or NULL.  Synchronous.

@@ -62,13 +62,14 @@ struct ddh_ctx {
   float2 *tw = nullptr;
   double minv[9] = {};
   double strehl_den = 1.0;
-  // host-buffer path: double-buffered staging, H2D / compute / D2H on three
+  // host-buffer path: triple-buffered staging, H2D / compute / D2H on three
   // streams so the copies of frames t+1 and t-1 overlap the step of frame t
-  float2 *y_stage[2] = {nullptr, nullptr};
-  float *phi_stage[2] = {nullptr, nullptr}, *r_stage[2] = {nullptr, nullptr};
-  uint8_t *status_stage[2] = {nullptr, nullptr};
+  static constexpr int kStages = 3;  // host pipeline depth (frames in flight)
+  float2 *y_stage[kStages] = {};
+  float *phi_stage[kStages] = {}, *r_stage[kStages] = {};
+  uint8_t *status_stage[kStages] = {};
   cudaStream_t h2d_st = nullptr, d2h_st = nullptr;
-  cudaEvent_t h2d_ev[2] = {}, comp_ev[2] = {}, d2h_ev[2] = {};
+  cudaEvent_t h2d_ev[kStages] = {}, comp_ev[kStages] = {}, d2h_ev[kStages] = {};
   bool host_pending = false;  // an asynchronous host-buffer call is in flight
   uint64_t host_t = 0;        // frames through the host pipeline since it was last drained
   // concurrent launch lanes of the streaming path: the streams of a launch
@@ -589,7 +590,7 @@ void free_ctx(ddh_ctx *c) {
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : c->lane_st)
     if (s) cudaStreamDestroy(s);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < ddh_ctx::kStages; ++k) {
     if (c->h2d_ev[k]) cudaEventDestroy(c->h2d_ev[k]);
     if (c->comp_ev[k]) cudaEventDestroy(c->comp_ev[k]);
     if (c->d2h_ev[k]) cudaEventDestroy(c->d2h_ev[k]);
@@ -604,7 +605,8 @@ void free_ctx(ddh_ctx *c) {
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
                   c->y_stage[0], c->phi_stage[0], c->r_stage[0], c->status_stage[0],
-                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1], c->test_part0, c->test_part1, c->sstat, c->test_sstat, c->psum[0], c->psum[1]};
+                  c->y_stage[1], c->phi_stage[1], c->r_stage[1], c->status_stage[1],
+                  c->y_stage[2], c->phi_stage[2], c->r_stage[2], c->status_stage[2], c->test_part0, c->test_part1, c->sstat, c->test_sstat, c->psum[0], c->psum[1]};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -953,9 +955,9 @@ ddh_status ddh_static(ddh_ctx *c, const void *y, int32_t T, int32_t iters, float
 }
 
 namespace {
-// Host-buffer path: frame t of the pipeline uses stage k = t & 1.  H2D(t)
-// waits for the step of t-2 (reader of y_stage[k]); the step of t waits for
-// H2D(t) and for D2H(t-2) (reader of the output stages); D2H(t) waits for the
+// Host-buffer path: frame t of the pipeline uses stage k = t mod 3.  H2D(t)
+// waits for the step of t-3 (reader of y_stage[k]); the step of t waits for
+// H2D(t) and for D2H(t-3) (reader of the output stages); D2H(t) waits for the
 // step of t.  `host_t` continues across asynchronous calls, so consecutive
 // calls keep the copy pipeline full; a synchronous call (or ddh_sync) drains it.
 ddh_status step_host_impl(ddh_ctx *c, const void *y_host, int32_t T, float *phi_out, float *r_out,
@@ -967,7 +969,7 @@ ddh_status step_host_impl(ddh_ctx *c, const void *y_host, int32_t T, float *phi_
   const size_t fs = (size_t)c->S * c->P;
   if (!c->y_stage[0]) {
     cudaError_t e = cudaSuccess;
-    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    for (int k = 0; k < ddh_ctx::kStages && e == cudaSuccess; ++k) {
       e = dalloc(&c->y_stage[k], fs);
       if (e == cudaSuccess) e = dalloc(&c->phi_stage[k], fs);
       if (e == cudaSuccess) e = dalloc(&c->r_stage[k], fs);
@@ -996,15 +998,15 @@ ddh_status step_host_impl(ddh_ctx *c, const void *y_host, int32_t T, float *phi_
       return drain(fail(c, DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)));   \
   } while (0)
   if (!c->host_pending) {  // order after prior work on the ctx stream (fresh pipeline)
-    DDH_HCK(cudaEventRecord(c->comp_ev[0], c->st));
-    DDH_HCK(cudaEventRecord(c->comp_ev[1], c->st));
-    DDH_HCK(cudaEventRecord(c->d2h_ev[0], c->st));
-    DDH_HCK(cudaEventRecord(c->d2h_ev[1], c->st));
+    for (int k = 0; k < ddh_ctx::kStages; ++k) {
+      DDH_HCK(cudaEventRecord(c->comp_ev[k], c->st));
+      DDH_HCK(cudaEventRecord(c->d2h_ev[k], c->st));
+    }
     c->host_t = 0;
   }
   c->host_pending = true;
   for (int t = 0; t < T; ++t) {
-    const int k = (int)((c->host_t++) & 1);
+    const int k = (int)((c->host_t++) % ddh_ctx::kStages);
     DDH_HCK(cudaStreamWaitEvent(c->h2d_st, c->comp_ev[k], 0));
     DDH_HCK(cudaMemcpyAsync(c->y_stage[k], (const float2 *)y_host + t * fs, fs * sizeof(float2),
                             cudaMemcpyHostToDevice, c->h2d_st));

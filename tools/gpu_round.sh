@@ -23,7 +23,7 @@ PY
       ;;
     ncu)
       CMD="python bench.py --steps 5 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity --serial ${BENCH_EXTRA:-}"
-      $CMD > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ks_|kf_" -s 12 -c 6 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
+      $CMD > gpurun_out/ncu_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ks_" -s 18 -c 13 -o gpurun_out/prof $CMD > gpurun_out/ncu_full.log 2>&1
       echo "ncu rc=$?"; tail -2 gpurun_out/ncu_full.log ;;
     launches)
       CMD="python bench.py --steps 20 --warmup 3 --frames 8 --no-e2e --no-latency --no-cpu-baseline --no-parity --serial"

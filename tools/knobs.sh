@@ -1,6 +1,7 @@
+# c3 throughput under diagnostic overrides (run under gpurun): tools/knobs.sh "ENV=.. ENV2=.." ...
 mkdir -p gpurun_out
-for cfg in "base" "DDH_SPLIT_R=0" "DDH_LANES=1" "DDH_LANES=3" "DDH_LANES=4" "DDH_LANES=4 DDH_SPLIT_R=0"; do
+for cfg in base "$@"; do
   if [ "$cfg" = base ]; then e=""; else e="$cfg"; fi
-  env $e timeout 300 python bench.py --steps 300 --warmup 5 --frames 40 --no-e2e --no-latency --no-cpu-baseline --no-parity > gpurun_out/k.log 2>/dev/null
-  python -c "import json;d=json.loads(open('gpurun_out/k.log').read().strip().splitlines()[-1]);print('$cfg', round(d['value']), round(d['ms_per_step']*1000,1))"
+  env $e timeout 300 python bench.py --steps 300 --warmup 5 --frames 40 --no-e2e --no-latency --no-cpu-baseline --no-parity > gpurun_out/k.log 2>gpurun_out/k.err
+  python -c "import json;d=json.loads(open('gpurun_out/k.log').read().strip().splitlines()[-1]);print('$cfg', round(d['value']), round(d['ms_per_step']*1000,1))" || tail -3 gpurun_out/k.err
 done

@@ -87,9 +87,10 @@ if os.path.exists(rep):
         summary["dram_bytes_per_launch"][base] = rb + wb
         lines.append(f"{name}\n" + "\n".join(f"  {k}: {v}" for k, v in d.items()))
     with open(os.path.join(out_dir, f"{rnd}_ncu_full.txt"), "w") as f:
-        f.write("# ncu --set full --clock-control none --import-source on -k regex:'ks_|kf_' -s 12 -c 6\n"
-                "# (bench.py --steps 5 --warmup 3 --frames 8 --serial: one launch of each kernel, 64 streams of c3,\n"
-                "#  the launch configuration of bench.py's attribution pass)\n"
+        f.write("# ncu --set full --clock-control none --import-source on -k regex:'ks_' -s 18 -c 13\n"
+                "# (bench.py --steps 5 --warmup 3 --frames 8 --serial: the kernels of two time steps in the middle of a\n"
+                "#  multi-frame call, 64 streams of c3, the launch configuration of bench.py's attribution pass; the\n"
+                "#  last launch of each kernel is listed; ks_stats there is the y-only S0 of the next frame)\n"
                 "# bytes in bytes; other units in brackets\n\n")
         f.write("\n\n".join(lines) + "\n")
     json.dump(summary, open(os.path.join(out_dir, "ncu_summary.json"), "w"), indent=1)

@@ -11,7 +11,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import synth  # noqa: E402
-from paper_2305_03284_b200 import DDH  # noqa: E402
+from paper_2305_03284_b200 import DDH, sched  # noqa: E402
 
 rnd = sys.argv[1] if len(sys.argv) > 1 else "r01"
 cfg = dict(synth.CONFIGS["c3"])
@@ -21,15 +21,13 @@ yd = torch.from_numpy(y).cuda()
 nv = synth.recon_noise_var(256, 256, cfg["snr_db"])
 res = {}
 for nk in (1, 2, 4, 8):
-    ctx = DDH(256, S, noise_var=nv, n_k=nk)
-    for k in range(3):
-        ctx.step(yd[k:k + 1])
+    ctx = DDH(256, S, noise_var=nv, n_k=nk, flags=64)
+    sched.run_steps(ctx, yd, 0, 3, F)
     torch.cuda.synchronize()
     K = 100 // nk
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for k in range(K):
-        ctx.step(yd[k % F:k % F + 1])
+    sched.run_steps(ctx, yd, 3, K, F)  # multi-frame calls, as bench.py
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
