@@ -39,10 +39,10 @@ struct ddh_ctx {
   float *phi[2] = {nullptr, nullptr};
   int cur = 0;
   int64_t frame = 0;
-  // streaming path: RemoveTipTilt sums of the phase state in 2^-24 fixed point,
-  // [2][S][3]; psum[pcur] holds the sums of phi[cur] when psum_valid (written
+  // streaming path: RemoveTipTilt sums of the phase state in 2^-16 fixed point
+  // (integer-valued doubles), [2][S][3]; psum[pcur] holds the sums of phi[cur] when psum_valid (written
   // by the last S5 of the previous frame), so S0 reads only y
-  long long *psum[2] = {nullptr, nullptr};
+  double *psum[2] = {nullptr, nullptr};
   int pcur = 0;
   bool psum_valid = false;
   // the S0 y sums of frame t+1 of one call run on the r-ICD side stream of
@@ -363,13 +363,13 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
         b.phi_in = c->phi[cur] + go;
         const bool stepm = mode == Mode::Step;
         b.psum_in = c->psum[c->pcur] + (size_t)(s0 + g0) * 3;
-        long long *psum_next = stepm ? c->psum[c->pcur ^ 1] + (size_t)(s0 + g0) * 3 : nullptr;
+        double *psum_next = stepm ? c->psum[c->pcur ^ 1] + (size_t)(s0 + g0) * 3 : nullptr;
         // S0: the y sums (unless frame t-1 of this call prefetched them) and, when the
         // fixed-point plane sums of phi are not already there, those too
         const bool need_plane = plane && !c->psum_valid;
         const bool y_ready = c->y_prefetched == (const void *)y;
         if (need_plane)
-          DDH_CK(c, cudaMemsetAsync(b.psum_in, 0, (size_t)b.sc * 3 * sizeof(long long), st));
+          DDH_CK(c, cudaMemsetAsync(b.psum_in, 0, (size_t)b.sc * 3 * sizeof(double), st));
         if (!y_ready || need_plane) {
           b.want_y = y_ready ? 0 : 1;
           b.apply_plane = need_plane ? 1 : 0;
@@ -856,7 +856,7 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   A(ddh::launch_fill(c->r, (float)p.r_min, S * P, c->st));
   A(cudaMemsetAsync(c->phi[0], 0, S * P * sizeof(float), c->st));
   A(cudaMemsetAsync(c->phi[1], 0, S * P * sizeof(float), c->st));
-  A(cudaMemsetAsync(c->psum[0], 0, S * 3 * sizeof(long long), c->st));  // the sums of phi = 0
+  A(cudaMemsetAsync(c->psum[0], 0, S * 3 * sizeof(double), c->st));  // the sums of phi = 0
   c->psum_valid = true;
   A(cudaStreamSynchronize(c->st));
   if (e != cudaSuccess) {

@@ -58,8 +58,8 @@ struct StepArgs {
   float *icd_out;         // S3 / S5 output [sc][N][N]
   float *icd_copy;        // optional user copy of the output or null
   float *sstat;           // [sc][8] per-stream scalars of the step (ddh_stream.cu kStatW)
-  long long *psum_in;     // [sc][3] RemoveTipTilt sums of phi_in, 2^-24 fixed point (S0 adds / S1 reads)
-  long long *psum_out;    // [sc][3] the same sums of the output phase (S1 zeroes, last S5 adds) or null
+  double *psum_in;        // [sc][3] RemoveTipTilt sums of phi_in, 2^-16 fixed point (integer-valued; S0 adds / S1 reads)
+  double *psum_out;       // [sc][3] the same sums of the output phase (S1 zeroes, last S5 adds) or null
   int dbg_fault;          // debug build only (DDH_DEBUG_FAULT): a deliberately failing check, to show the checks run
 };
 

@@ -113,39 +113,37 @@ __device__ __forceinline__ void sum_part0(const double *__restrict__ part0, int 
 #pragma unroll
   for (int k = 0; k < 5; ++k) out[k] = warp_sum(v[k]);  // xor tree: every lane holds the totals
 }
-// RemoveTipTilt normal-equation sums (R17) in 2^-24 fixed point: the
-// sums are exact integers, so any partition and order of the pixels (S0 over
-// row blocks, S5's epilogue over ICD tiles, atomics) gives the same bits.
-// Quantisation 6e-8 rad per pixel; |phi| up to 2^14 rad on 1024^2 stays in range.
-constexpr float kFix = 16777216.f;  // 2^24
-__device__ __forceinline__ long long fix24(float f) { return __float2ll_rn(f * kFix); }
-__device__ __forceinline__ long long warp_sum_ll(long long v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-// Block sum of (s0, sx, sy) and one 64-bit atomic add each into out[0..2]
-__device__ __forceinline__ void plane_sums_add(long long s0, long long sx, long long sy, long long *red,
-                                               long long *out) {
+// RemoveTipTilt normal-equation sums (R17) in 2^-16 fixed point: every
+// phase value is rounded to an integer multiple of 2^-16 (FP32 rint of f 2^16)
+// and the sums of those integers (and of their integer x / y moments) are
+// accumulated in FP64, where they are exact while below 2^53 (|phi| < 256 rad
+// at N = 1024, < 16384 rad at 256^2).  So any partition and order of the
+// pixels (S0 over row blocks, S5's epilogue over ICD tiles, double atomics)
+// gives the same bits.  Quantisation 1.5e-5 rad per pixel, random: the plane
+// coefficients move by ~1e-9 rad per pixel.
+constexpr float kFix = 65536.f;  // 2^16
+__device__ __forceinline__ float fixq(float f) { return rintf(f * kFix); }
+// Block sum of (s0, sx, sy) (exact: integer-valued doubles) and one atomic add each into out[0..2]
+__device__ __forceinline__ void plane_sums_add(double s0, double sx, double sy, double *red, double *out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-  s0 = warp_sum_ll(s0);
-  sx = warp_sum_ll(sx);
-  sy = warp_sum_ll(sy);
+  s0 = warp_sum(s0);
+  sx = warp_sum(sx);
+  sy = warp_sum(sy);
   if (lane == 0) red[warp * 3] = s0, red[warp * 3 + 1] = sx, red[warp * 3 + 2] = sy;
   __syncthreads();
   if (warp == 0) {
-    long long v[3];
+    double v[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) v[k] = warp_sum_ll(lane < nw ? red[lane * 3 + k] : 0ll);
+    for (int k = 0; k < 3; ++k) v[k] = warp_sum(lane < nw ? red[lane * 3 + k] : 0.0);
     if (lane == 0)
 #pragma unroll
       for (int k = 0; k < 3; ++k)
-        if (v[k]) atomicAdd(reinterpret_cast<unsigned long long *>(out + k), (unsigned long long)v[k]);
+        if (v[k] != 0.0) atomicAdd(out + k, v[k]);
   }
 }
 // plane coefficients from the fixed-point sums
-__device__ __forceinline__ void plane_from_fix(const long long *__restrict__ ps, const double *minv, double *c) {
-  const double sums[5] = {0.0, 0.0, (double)ps[0] / kFix, (double)ps[1] / kFix, (double)ps[2] / kFix};
+__device__ __forceinline__ void plane_from_fix(const double *__restrict__ ps, const double *minv, double *c) {
+  const double sums[5] = {0.0, 0.0, ps[0] / kFix, ps[1] / kFix, ps[2] / kFix};
   plane_from_sums(sums, minv, c);
 }
 
@@ -175,15 +173,14 @@ __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g
 // ||y - mu|| = 0 of R31 stays exact) and accumulated in FP64; phi plane sums:
 // FP32 per-thread partials; FP64 block sums.
 __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
-  __shared__ double red[32 * 2];
-  __shared__ long long redl[32 * 3];
+  __shared__ double red[32 * 3];
   const int n = A.n, lg = 31 - __clz(n);
   const size_t P = (size_t)n * n;
   const int s = blockIdx.y;
   const size_t per = P / A.nb0;
   const size_t base = blockIdx.x * per;
   const size_t off = (size_t)s * P;
-  long long l0 = 0, lx = 0, ly = 0;
+  double l0 = 0.0, lx = 0.0, ly = 0.0;
   double yr = 0.0, yi = 0.0;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
@@ -203,17 +200,17 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
         const float4 *f4 = reinterpret_cast<const float4 *>(A.phi_in + off + p0);
         const float4 f0 = __ldg(f4), f1 = __ldg(f4 + 1);
         const float f[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-        long long s0 = 0, sx = 0;
+        double s0 = 0.0, sx = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int j = j0 + k;
-          const long long q = (j >= sp.x && j < sp.y) ? fix24(f[k]) : 0ll;
+          const double q = (j >= sp.x && j < sp.y) ? (double)fixq(f[k]) : 0.0;
           s0 += q;
-          sx += q * (j - n / 2);
+          sx = fma(q, (double)(j - n / 2), sx);
         }
         l0 += s0;
         lx += sx;
-        ly += s0 * (i - n / 2);
+        ly = fma(s0, (double)(i - n / 2), ly);
       }
     }
   }
@@ -225,7 +222,7 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
       A.part0[((size_t)s * A.nb0 + blockIdx.x) * 5 + 1] = d[1];
     }
   }
-  if (A.apply_plane) plane_sums_add(l0, lx, ly, redl, A.psum_in + (size_t)s * 3);
+  if (A.apply_plane) plane_sums_add(l0, lx, ly, red, A.psum_in + (size_t)s * 3);
 }
 
 // ------------------------------------------------------------------ S1
@@ -264,7 +261,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
     st[0] = mur;
     st[1] = mui;
     if (A.apply_plane) st[2] = c0, st[3] = c1, st[4] = c2;
-    if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0;
+    if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0.0;
   }
   const int2 sp = __ldg(A.rowspan + i);
   const float pyi = fmaf(c2, (float)(i - N / 2), c0);
@@ -392,7 +389,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
       ss[0] = mur;
       ss[1] = mui;
       if (A.apply_plane) ss[2] = c0, ss[3] = c1, ss[4] = c2;
-      if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0;
+      if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0.0;
     }
     const int2 sp = __ldg(A.rowspan + i);
     const float pyi = fmaf(c2, (float)(i - N / 2), c0);
@@ -919,29 +916,61 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
     else
       phiicd_sweep<N, TILE, false>(ps, cts, tid, i0, j0, w, prior);
   }
-  long long e0 = 0, ex = 0, ey = 0;
-  for (int idx = tid; idx < T * (T / 2); idx += NTH) {
-    const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
-    const int li = oi + kHalo;
-    const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
-    const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
-                                : make_float2(ps[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
-                                              ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
-    *reinterpret_cast<float2 *>(A.icd_out + g) = v;
-    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
-    if (A.psum_out) {  // RemoveTipTilt sums of the output phase, for the next frame's S1
-      const int gi = i0 + oi, gj = j0 + 2 * pj;
-      const int2 sp = __ldg(A.rowspan + gi);
-      const long long q0 = (gj >= sp.x && gj < sp.y) ? fix24(v.x) : 0ll;
-      const long long q1 = (gj + 1 >= sp.x && gj + 1 < sp.y) ? fix24(v.y) : 0ll;
-      e0 += q0 + q1;
-      ex += q0 * (gj - N / 2) + q1 * (gj + 1 - N / 2);
-      ey += (q0 + q1) * (gi - N / 2);
+  // output (and the RemoveTipTilt sums of the output phase for the next frame's S1)
+  constexpr int PR = T / 2;  // pixel pairs per tile row
+  double e0 = 0.0, ex = 0.0, ey = 0.0;
+  if constexpr (NTH % PR == 0) {
+    // every thread keeps one column pair: addresses advance by constants, the
+    // x moments come from the two column sums at the end
+    constexpr int RS = NTH / PR;  // tile rows per pass
+    const int pj = tid % PR, oi0 = tid / PR;
+    const int gj = j0 + 2 * pj;
+    const float *psrc = ps + G::sidx(0, 0, pj + kHalo / 2);
+    size_t g = off + (size_t)(i0 + oi0) * N + gj;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll 2
+    for (int oi = oi0; oi < T; oi += RS, g += (size_t)RS * N) {
+      const int li = oi + kHalo;
+      const float *q = psrc + (2 * (li & 1) * G::kSub + (li >> 1)) * G::kSubP;
+      const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off)) : make_float2(q[0], q[G::kSub * G::kSubP]);
+      *reinterpret_cast<float2 *>(A.icd_out + g) = v;
+      if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+      if (A.psum_out) {
+        const int gi = i0 + oi;
+        const int2 sp = __ldg(A.rowspan + gi);
+        const double q0 = (gj >= sp.x && gj < sp.y) ? (double)fixq(v.x) : 0.0;
+        const double q1 = (gj + 1 >= sp.x && gj + 1 < sp.y) ? (double)fixq(v.y) : 0.0;
+        c0 += q0;
+        c1 += q1;
+        ey = fma(q0 + q1, (double)(gi - N / 2), ey);
+      }
+    }
+    e0 = c0 + c1;
+    ex = fma(c0, (double)(gj - N / 2), c1 * (double)(gj + 1 - N / 2));
+  } else {
+    for (int idx = tid; idx < T * PR; idx += NTH) {
+      const int oi = idx / PR, pj = idx - oi * PR;
+      const int li = oi + kHalo;
+      const size_t g = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
+      const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off))
+                                  : make_float2(ps[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
+                                                ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
+      *reinterpret_cast<float2 *>(A.icd_out + g) = v;
+      if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+      if (A.psum_out) {
+        const int gi = i0 + oi, gj = j0 + 2 * pj;
+        const int2 sp = __ldg(A.rowspan + gi);
+        const double q0 = (gj >= sp.x && gj < sp.y) ? (double)fixq(v.x) : 0.0;
+        const double q1 = (gj + 1 >= sp.x && gj + 1 < sp.y) ? (double)fixq(v.y) : 0.0;
+        e0 += q0 + q1;
+        ex = fma(q0, (double)(gj - N / 2), fma(q1, (double)(gj + 1 - N / 2), ex));
+        ey = fma(q0 + q1, (double)(gi - N / 2), ey);
+      }
     }
   }
   if (A.psum_out) {
-    __shared__ long long redl[32 * 3];
-    plane_sums_add(e0, ex, ey, redl, A.psum_out + (size_t)s * 3);
+    __shared__ double redd[32 * 3];
+    plane_sums_add(e0, ex, ey, redd, A.psum_out + (size_t)s * 3);
   }
 }
 
