@@ -405,6 +405,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
             DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
+            c->launches += ddh::icd_launches(b, true) - 1;
           }
           if (last && y_next) {  // y sums of the next frame of this call, beside S4 / S5
             StepArgs yb = b;
@@ -422,6 +423,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.apply_plane = k == 0 ? plane_it : 0;
             b.psum_out = (k == sw - 1 && last) ? psum_next : nullptr;  // sums of the frame's phase
             DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
+            c->launches += ddh::icd_launches(b, false) - 1;
             b.psum_out = nullptr;
           }
           if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
@@ -1249,6 +1251,7 @@ ddh_status ddh_test_ricd(ddh_ctx *c, const float *r_in, const float *q, int32_t 
       a.icd_out = k == sw - 1 ? r_out + off : c->rtmp[k & 1];
       a.icd_copy = nullptr;
       DDH_LAUNCH(c, K_S3, ddh::launch_s3(a, c->st));
+      c->launches += ddh::icd_launches(a, true) - 1;
     }
   }
   return DDH_OK;
@@ -1279,6 +1282,7 @@ ddh_status ddh_test_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, con
       a.icd_out = k == sw - 1 ? phi_out + off : c->ptmp[k & 1];
       a.icd_copy = nullptr;
       DDH_LAUNCH(c, K_S5, ddh::launch_s5(a, c->st));
+      c->launches += ddh::icd_launches(a, false) - 1;
     }
   }
   return DDH_OK;

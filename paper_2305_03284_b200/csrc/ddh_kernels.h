@@ -124,6 +124,7 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
+int icd_launches(const StepArgs &a, bool r_icd);  // kernels one launch_s3 / launch_s5 enqueues (4: colour passes)
 
 // stage entry points of the streaming kernels (ddh_test_*)
 cudaError_t launch_test_fft_stream(int n, const float2 *in, float2 *out, int B, int inverse, const float4 *tw4,

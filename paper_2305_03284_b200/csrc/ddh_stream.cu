@@ -27,6 +27,7 @@
 // N <= 256), all arithmetic on complex pairs uses packed FP32x2 instructions.
 // The ICD kernels store the tile colour-separated (four (i mod 2, j mod 2)
 // sub-grids), so a colour phase reads and writes consecutive words.
+#include <algorithm>
 #include <cstdlib>
 
 #include "ddh_common.cuh"
@@ -764,8 +765,12 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
       __syncthreads();
     }
   }
-  for (int idx = tid; idx < T * (T / 2); idx += NTH) {
-    const int oi = idx / (T / 2), pj = idx - oi * (T / 2);
+  constexpr int PR = T / 2;  // pixel pairs per tile row
+  // one column pair per thread when the thread count allows it (constant address steps)
+  constexpr int STEP = NTH % PR == 0 ? NTH : 1;
+  const int pj0 = tid % PR, oi0 = tid / PR;
+  for (int idx = NTH % PR == 0 ? oi0 * PR + pj0 : tid; idx < T * PR; idx += (NTH % PR == 0 ? STEP : NTH)) {
+    const int oi = idx / PR, pj = idx - oi * PR;
     const int li = oi + kHalo;
     const size_t gidx = off + (size_t)(i0 + oi) * N + (j0 + 2 * pj);
     DDH_DBG(i0 + oi < N && j0 + 2 * pj + 1 < N && gidx + 1 < (size_t)A.sc * P);
@@ -974,6 +979,67 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
   }
 }
 
+// ----------------------------------------- r-ICD as global colour passes
+// Large launches: the colour-ordered sweep (R8) as four kernels, one per
+// colour class (i mod 2, j mod 2) in the order (0,0),(0,1),(1,0),(1,1), one
+// thread per pixel of the class.  A neighbour of a lower colour is read from
+// the sweep's output (already updated by an earlier pass), of a higher colour
+// from its input; pixels of one class never neighbour each other, so a pass
+// has no intra-kernel dependency: no tile, no halo, no barrier, and the whole
+// GPU is one pool of independent updates.  The per-pixel arithmetic is the
+// tile kernels' (same expressions, same order), so the results are the same
+// bits as the halo-tile kernels (tests/test_gpu_parity.py kernel variants).
+
+// neighbour (DI, DJ) of a colour-C pixel (i, j), periodic boundary (r-ICD)
+template <int N, int C, int DI, int DJ>
+__device__ __forceinline__ float rnb(const float *__restrict__ in, const float *out, int i, int j) {
+  constexpr int CI = C >> 1, CJ = C & 1, NC = 2 * ((CI + DI) & 1) + ((CJ + DJ) & 1);
+  const float *src = NC < C ? out : in;  // lower colours were written by earlier passes (read-only now)
+  return __ldg(src + (size_t)((i + DI) & (N - 1)) * N + ((j + DJ) & (N - 1)));
+}
+
+template <int N, int C>
+__device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
+  constexpr int CI = C >> 1, CJ = C & 1, H = N / 2, P = N * N;
+  const int i = 2 * (p / H) + CI, j = 2 * (p % H) + CJ;
+  const size_t off = (size_t)s * P, g = (size_t)i * N + j;
+  const float *__restrict__ in = A.icd_in + off;
+  float *out = A.icd_out + off;
+  const bool degenerate = A.sstat[(size_t)s * kStatW + 6] != 0.f;
+  DDH_DBG(i < N && j < N);
+  float v;
+  if (degenerate) {
+    v = in[g];
+  } else if (!A.r_prior) {
+    v = fmaxf(__ldg(A.q + off + g), A.r_min);
+  } else {
+    const float q = __ldg(A.q + off + g);
+    const float ri = in[g];
+    const float2 nA = make_float2(rnb<N, C, -1, 0>(in, out, i, j), rnb<N, C, 1, 0>(in, out, i, j));
+    const float2 nB = make_float2(rnb<N, C, 0, -1>(in, out, i, j), rnb<N, C, 0, 1>(in, out, i, j));
+    const float2 dA = make_float2(rnb<N, C, -1, -1>(in, out, i, j), rnb<N, C, -1, 1>(in, out, i, j));
+    const float2 dB = make_float2(rnb<N, C, 1, -1>(in, out, i, j), rnb<N, C, 1, 1>(in, out, i, j));
+    const float h = A.r_h, gg = A.r_g, kq = A.r_k;
+    const float2 wA = qgg_w2(ri, nA, h, gg, kq), wB = qgg_w2(ri, nB, h, gg, kq);
+    const float2 wC = qgg_w2(ri, dA, h, gg, kq), wD = qgg_w2(ri, dB, h, gg, kq);
+    const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+    const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+    v = r_update(ri, q, A.r_b6 * (bs.x + bs.y), A.r_b6 * (ss.x + ss.y), A.r_min);
+  }
+  out[g] = v;
+  if (A.icd_copy) A.icd_copy[off + g] = v;
+}
+
+// one thread per pixel of the class; grid (N^2/4 / 256, streams).  (A
+// grid-stride form sized to the resident CTA slots measured slower in the
+// concurrent step: 134.9 vs 128.5 us at c3.)
+template <int N, int C>
+__global__ void __launch_bounds__(256) ks_ricd_pass(StepArgs A) {
+  DDH_PDL_TRIGGER();
+  DDH_PDL_WAIT();
+  ricd_pass_px<N, C>(A, blockIdx.y, blockIdx.x * 256 + threadIdx.x);
+}
+
 // ------------------------------------------------- stage entry points
 // (ddh_test_*: the streaming kernels' own device code on caller buffers)
 
@@ -1170,8 +1236,32 @@ static cudaError_t launch_icd(void (*k)(StepArgs), const StepArgs &a, cudaStream
   constexpr int T = N < TILE ? N : TILE;
   return launch_pdl(k, dim3(N / T, N / T, a.sc), dim3(IcdT<TILE>::NTH), smem, st, a);
 }
+// the global colour passes for the r-ICD launches that would use the 64-tiles
+// (DDH_RICD_PASSES=0: the tiles; diagnostic).  The phi-ICD stays on tiles: its
+// cheap update is bound by operand traffic, and the passes' per-neighbour
+// global loads (no shared tile) measured 44.4 vs 33.3 us at c3.
+template <int N>
+static bool use_passes(int sc, bool r) {
+  static const int on = getenv("DDH_RICD_PASSES") ? atoi(getenv("DDH_RICD_PASSES")) : 1;
+  return r && on && !small_tiles<N>(sc) && !tiny_tiles<N>(sc);
+}
+int icd_launches(const StepArgs &a, bool r) { DDH_SDISPATCH(a.n, return use_passes<N>(a.sc, r) ? 4 : 1); return 1; }
+template <int N>
+static cudaError_t launch_passes(const StepArgs &a, cudaStream_t st, void (*k0)(StepArgs), void (*k1)(StepArgs),
+                                 void (*k2)(StepArgs), void (*k3)(StepArgs)) {
+  const dim3 grid((N / 2) * (N / 2) / 256, a.sc);
+  cudaError_t e = launch_pdl(k0, grid, dim3(256), 0, st, a);
+  if (e == cudaSuccess) e = launch_pdl(k1, grid, dim3(256), 0, st, a);
+  if (e == cudaSuccess) e = launch_pdl(k2, grid, dim3(256), 0, st, a);
+  if (e == cudaSuccess) e = launch_pdl(k3, grid, dim3(256), 0, st, a);
+  return e;
+}
+
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
+                  if (use_passes<N>(a.sc, true))
+                    return launch_passes<N>(a, st, ks_ricd_pass<N, 0>, ks_ricd_pass<N, 1>, ks_ricd_pass<N, 2>,
+                                                    ks_ricd_pass<N, 3>);
                   if (tiny_tiles<N>(a.sc))
                     return launch_pdl(ks_ricd<N, 16>, dim3(N / 16, N / 16, a.sc), dim3(kSThreads),
                                       Icd<16>::kIcdGrid * sizeof(float), st, a);
