@@ -84,6 +84,14 @@ struct ddh_ctx {
   bool l2_window = false;  // holds the device's persisting-L2 carve-out
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
+  // inside a multi-frame call the join of a lane's r-ICD side stream is
+  // deferred to the next S2 (the first kernel that needs it), so S1 of the next
+  // frame overlaps the r-ICD; the next frame's S0 y sums run on a stream of
+  // their own, forked after S1 (which reads the partials they overwrite)
+  bool side_pending[8] = {};
+  cudaStream_t ypf_st[8] = {};
+  cudaEvent_t ypf_fork[8] = {}, ypf_join[8] = {};
+  bool ypf_pending[8] = {};
   // CUDA graphs of single-frame steps (DDH_F_GRAPHS): a key (frame, outputs,
   // phi parity) seen twice within the last kKeyWindow calls is captured once
   // and replayed afterwards (the host then enqueues one graph instead of ~10
@@ -392,7 +400,32 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
           }
           b.status = (first && status) ? status + s0 + g0 : nullptr;
           b.psum_out = first ? psum_next : nullptr;  // S1 zeroes the next frame's sums
+          if (first && c->ypf_pending[l]) {  // this frame's S0 y sums, prefetched during the last frame
+            DDH_CK(c, cudaStreamWaitEvent(st, c->ypf_join[l], 0));
+            c->ypf_pending[l] = false;
+          }
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
+          if (last && y_next) {  // y sums of the next frame of this call, after S1 read the partials
+            StepArgs yb = b;
+            yb.y = y_next + go;
+            yb.want_y = 1;
+            yb.apply_plane = 0;
+            cudaStream_t yst = st;
+            if (c->split_r) {
+              yst = c->ypf_st[l];
+              DDH_CK(c, cudaEventRecord(c->ypf_fork[l], st));
+              DDH_CK(c, cudaStreamWaitEvent(yst, c->ypf_fork[l], 0));
+            }
+            DDH_LAUNCH_ON(c, K_S0, yst, ddh::launch_s0(yb, yst));
+            if (c->split_r) {
+              DDH_CK(c, cudaEventRecord(c->ypf_join[l], yst));
+              c->ypf_pending[l] = true;
+            }
+          }
+          if (c->side_pending[l]) {  // S2 overwrites r0, q and reads r: the previous r-ICD must be done
+            DDH_CK(c, cudaStreamWaitEvent(st, c->side_join[l], 0));
+            c->side_pending[l] = false;
+          }
           DDH_LAUNCH_ON(c, K_S2, st, ddh::launch_s2(b, st));
           cudaStream_t rst = st;
           if (c->split_r) {  // fork: S3 after S2, beside S4/S5
@@ -407,13 +440,6 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
             c->launches += ddh::icd_launches(b, true) - 1;
           }
-          if (last && y_next) {  // y sums of the next frame of this call, beside S4 / S5
-            StepArgs yb = b;
-            yb.y = y_next + go;
-            yb.want_y = 1;
-            yb.apply_plane = 0;
-            DDH_LAUNCH_ON(c, K_S0, rst, ddh::launch_s0(yb, rst));
-          }
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
           const int plane_it = b.apply_plane;
           for (int k = 0; k < sw; ++k) {  // phi M-step sweeps (plane removed in the first)
@@ -426,9 +452,13 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             c->launches += ddh::icd_launches(b, false) - 1;
             b.psum_out = nullptr;
           }
-          if (c->split_r) {  // join: the next S2 reads r, the next S1 overwrites nothing S3 reads
+          if (c->split_r) {  // join: the next S2 reads r; S1 overwrites nothing S3 reads
             DDH_CK(c, cudaEventRecord(c->side_join[l], rst));
-            DDH_CK(c, cudaStreamWaitEvent(st, c->side_join[l], 0));
+            if (last && y_next) {
+              c->side_pending[l] = true;  // deferred to the next frame's S2
+            } else {
+              DDH_CK(c, cudaStreamWaitEvent(st, c->side_join[l], 0));
+            }
           }
           cl ^= 1;
         }
@@ -603,6 +633,9 @@ void free_ctx(ddh_ctx *c) {
     if (c->side_st[l]) cudaStreamDestroy(c->side_st[l]);
     if (c->side_fork[l]) cudaEventDestroy(c->side_fork[l]);
     if (c->side_join[l]) cudaEventDestroy(c->side_join[l]);
+    if (c->ypf_st[l]) cudaStreamDestroy(c->ypf_st[l]);
+    if (c->ypf_fork[l]) cudaEventDestroy(c->ypf_fork[l]);
+    if (c->ypf_join[l]) cudaEventDestroy(c->ypf_join[l]);
   }
   void *ptrs[] = {c->r, c->phi[0], c->phi[1], c->cbuf, c->rinit, c->q, c->cc, c->theta, c->rtmp[0], c->rtmp[1],
                   c->ptmp[0], c->ptmp[1], c->part0, c->part1, c->stats, c->pmax, c->rowspan, c->tw, c->tw4,
@@ -815,6 +848,9 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
         A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));
         A(cudaEventCreateWithFlags(&c->side_fork[l], cudaEventDisableTiming));
         A(cudaEventCreateWithFlags(&c->side_join[l], cudaEventDisableTiming));
+        A(cudaStreamCreateWithFlags(&c->ypf_st[l], cudaStreamNonBlocking));
+        A(cudaEventCreateWithFlags(&c->ypf_fork[l], cudaEventDisableTiming));
+        A(cudaEventCreateWithFlags(&c->ypf_join[l], cudaEventDisableTiming));
       }
     }
   }
