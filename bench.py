@@ -382,7 +382,10 @@ def ctx_lanes(ctx):
         flags = ctx.params.flags
         if flags & 8:
             return 1
-        L = min(2, max(1, ctx_chunk(ctx) // 32))
+        import torch
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+        sc, tiles = ctx_chunk(ctx), (ctx.n // 64) ** 2
+        L = next((l for l in (3, 2) if sc // l >= 16 and tiles * (sc // l) >= 2 * sms), 1)
     return max(1, min(8, L))
 
 

@@ -833,8 +833,20 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
   if (c->streaming) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = (p.flags & DDH_F_SERIAL) ? 1 : ev ? std::atoi(ev) : p.lanes;
-    if (c->lanes <= 0)  // measured at 256^2 x 64 streams: 2
-      c->lanes = std::min(2, std::max(1, c->sc / 32));
+    if (c->lanes <= 0) {  // auto: up to 3 lanes, each keeping the large-launch kernels
+      // (ICD tiles of 64 / r-ICD colour passes: >= 2 64-tiles per SM) and >= 16 streams
+      // (c3, 64 streams at 256^2: 1 lane 140.8, 2 lanes 126.5, 3 lanes 125.6 us per step)
+      int sms = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const long tiles = (long)(n / 64) * (n / 64);
+      c->lanes = 1;
+      for (int L = 3; L > 1; --L)
+        if (c->sc / L >= 16 && tiles * (c->sc / L) >= 2L * sms) {
+          c->lanes = L;
+          break;
+        }
+    }
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
       for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
@@ -845,7 +857,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
 
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
-        A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));
+        {  // diagnostic: DDH_SIDE_PRIO = priority of the r-ICD side streams (lower = higher priority)
+          const char *sp = std::getenv("DDH_SIDE_PRIO");
+          if (sp) A(cudaStreamCreateWithPriority(&c->side_st[l], cudaStreamNonBlocking, std::atoi(sp)));
+          else A(cudaStreamCreateWithFlags(&c->side_st[l], cudaStreamNonBlocking));
+        }
         A(cudaEventCreateWithFlags(&c->side_fork[l], cudaEventDisableTiming));
         A(cudaEventCreateWithFlags(&c->side_join[l], cudaEventDisableTiming));
         A(cudaStreamCreateWithFlags(&c->ypf_st[l], cudaStreamNonBlocking));
