@@ -341,7 +341,21 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
   char *stage0 = reinterpret_cast<char *>(smem4 + N);           // 2 x [y rows | phi rows]
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t mb[2];
+  // per-item stream scalars, staged one item ahead by 8-byte cp.async: the S0
+  // partials (sum y re, im of nb0 blocks) and the fixed-point plane sums
+  __shared__ double scal[2][2 * 64 + 3];
   const int tid = threadIdx.x, G = gridDim.x, total = NR * A.sc;
+  const int nsc = 2 * A.nb0 + (A.apply_plane ? 3 : 0);
+  auto issue_scal = [&](int item, int slot) {
+    const int s = item / NR;
+    const unsigned dst = smem_u32(&scal[slot][0]);
+    for (int idx = tid; idx < nsc; idx += NT) {
+      const double *src = idx < 2 * A.nb0 ? A.part0 + ((size_t)s * A.nb0 + (idx >> 1)) * 5 + (idx & 1)
+                                          : A.psum_in + (size_t)s * 3 + (idx - 2 * A.nb0);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8 * idx), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
   const int t = tid % TPV, b = tid / TPV;
   auto issue = [&](int item, int st, bool y_part, bool phi_part) {  // thread 0
     const int bx = item % NR, s = item / NR;
@@ -371,7 +385,9 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
     if (blockIdx.x < total) issue(blockIdx.x, 0, false, true);
     if (blockIdx.x + G < total) issue(blockIdx.x + G, 1, false, true);
   }
-  __syncthreads();  // twiddles
+  if ((int)blockIdx.x < total) issue_scal(blockIdx.x, 0);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // twiddles, first item's scalars
   int k = 0;
   for (int item = blockIdx.x; item < total; item += G, ++k) {
     const int st = k & 1, bx = item % NR, s = item / NR;
@@ -380,9 +396,16 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
     char *stg = stage0 + st * Q::STAGE;
     const float2 *ys = reinterpret_cast<const float2 *>(stg) + b * N;
     const float *fs = reinterpret_cast<const float *>(stg + Q::YB) + b * N;
-    double sums[5], cpl[3] = {0, 0, 0};
-    sum_part0(A.part0, A.nb0, s, sums);
-    if (A.apply_plane) plane_from_fix(A.psum_in + (size_t)s * 3, A.minv, cpl);
+    if (item + G < total) issue_scal(item + G, st ^ 1);  // the next item's scalars, in flight during this one
+    double sums[5] = {0, 0, 0, 0, 0}, cpl[3] = {0, 0, 0};
+    {  // stream totals from the staged partials (same order as sum_part0: lane b, b + 32, ...; xor tree)
+      const int lane = tid & 31;
+      double v0 = 0.0, v1 = 0.0;
+      for (int bb = lane; bb < A.nb0; bb += 32) v0 += scal[st][2 * bb], v1 += scal[st][2 * bb + 1];
+      sums[0] = warp_sum(v0);
+      sums[1] = warp_sum(v1);
+      if (A.apply_plane) plane_from_fix(&scal[st][2 * A.nb0], A.minv, cpl);
+    }
     const float mur = (float)(sums[0] / P), mui = (float)(sums[1] / P);
     const float c0 = (float)cpl[0], c1 = (float)cpl[1], c2 = (float)cpl[2];
     if (bx == 0 && tid == 0) {  // per-stream scalars for S4 / S5
@@ -417,7 +440,8 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
     fft_reg<N>(v, t, reinterpret_cast<float2 *>(stg) + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
 #pragma unroll
     for (int e = 0; e < E; ++e) A.cbuf[row + t + TPV * out_comb<N>(e)] = v[e];
-    __syncthreads();  // the stage (FFT exchange) is free
+    asm volatile("cp.async.wait_group 0;" ::: "memory");  // the next item's scalars
+    __syncthreads();  // the stage (FFT exchange) is free; the next item's scalars are visible
     if (tid == 0 && item + 2 * G < total) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(item + 2 * G, st, true, true);
