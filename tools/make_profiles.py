@@ -68,6 +68,7 @@ if os.path.exists(rep):
             "launch__block_size", "launch__cluster_dim_x", "lts__t_bytes.sum"]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3, "nsecond": 1e-9}
     lines = []
+    passes = {}
     for r in rows[2:]:
         name = short(r[hdr.index("Kernel Name")])
         d = {}
@@ -84,8 +85,24 @@ if os.path.exists(rep):
         summary["kernels"][name] = d
         rb, wb = d.get("dram__bytes_read.sum", 0), d.get("dram__bytes_write.sum", 0)
         base = name.split("<")[0]
-        summary["dram_bytes_per_launch"][base] = rb + wb
+        if base != "ks_ricd_pass":
+            summary["dram_bytes_per_launch"][base] = rb + wb
+        # the r-ICD colour passes are four kernels per library launch (kind ks_ricd): per-pass
+        # values are listed, and their sum over the four passes is kept under the kind's name
+        if base == "ks_ricd_pass":
+            m = re.search(r"<\d+,(\d)>", name)
+            passes.setdefault(m.group(1) if m else name, d)
         lines.append(f"{name}\n" + "\n".join(f"  {k}: {v}" for k, v in d.items()))
+    if passes:
+        agg = {}
+        for k in ("gpu__time_duration.sum [us]", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                  "smsp__inst_executed.sum [inst]"):
+            agg[k] = sum(float(v.get(k, 0)) for v in passes.values())
+        agg["passes"] = sorted(passes)
+        summary["kernels"]["ks_ricd"] = agg  # the library's kind: the 4 colour passes
+        summary["dram_bytes_per_launch"]["ks_ricd"] = agg["dram__bytes_read.sum"] + agg["dram__bytes_write.sum"]
+        lines.append("ks_ricd (sum of the 4 colour passes = one library launch)\n" +
+                     "\n".join(f"  {k}: {v}" for k, v in agg.items()))
     with open(os.path.join(out_dir, f"{rnd}_ncu_full.txt"), "w") as f:
         f.write("# ncu --set full --clock-control none --import-source on -k regex:'ks_' -s 18 -c 13\n"
                 "# (bench.py --steps 5 --warmup 3 --frames 8 --serial: the kernels of two time steps in the middle of a\n"
