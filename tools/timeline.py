@@ -13,8 +13,20 @@ from paper_2305_03284_b200 import sched  # noqa: E402
 
 K = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/timeline.json"
-cfg = synth.CONFIGS["c3"]
-u = sched.StreamRank(cfg, 0, cfg["streams"], 0, 16, flags=64)
+cname = sys.argv[3] if len(sys.argv) > 3 else "c3"
+cfg = synth.CONFIGS[cname]
+if cname == "c2":  # latency mode: one synchronous single-frame call per frame, graph replay
+    u = sched.StreamRank(cfg, 0, 1, 0, 16, source="host", flags=32)
+    ybuf = torch.empty_like(u.y_dev[0:1])
+
+    def frames(k):
+        for t in range(k):
+            ybuf.copy_(u.y_dev[t % 16:t % 16 + 1])
+            u.ctx.step(ybuf)
+            torch.cuda.synchronize()
+    u.steps = frames
+else:
+    u = sched.StreamRank(cfg, 0, cfg["streams"], 0, 16, flags=64)
 u.steps(8)
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
