@@ -1225,17 +1225,20 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
 // staged form for launches of at most two slabs per SM (few streams: c2 step
 // 28.8 -> 25.3 us); at 64 streams the plain kernel is as fast
 template <int N>
-static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, bool staged_ok, int sms) {
+static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, int staged, int sms) {
   if constexpr (N <= 256) {
     const int total = N / SCfg<N>::W * a.sc;
-    if (staged_ok && total <= 2 * sms)
-      return launch_pdl(ks_cols_p<N>, dim3(total), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
+    if (staged == 2 || (staged && total <= 2 * sms))  // 2: persistent staged form for every launch (diagnostic)
+      return launch_pdl(ks_cols_p<N>, dim3(total < 2 * sms ? total : 2 * sms), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
   }
   return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a);
 }
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
-  static const int staged = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 1;  // diagnostic
-  DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged != 0, device_sms()));
+  // the persistent staged form for every launch at N <= 256 (c3: 509.7 -> 513.3 k
+  // frames/s; round 1, before the r-ICD passes freed the shared memory, it was neutral
+  // there); DDH_S2P=1: only small launches, 0: never (diagnostic)
+  static const int staged = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 2;
+  DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged, device_sms()));
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
