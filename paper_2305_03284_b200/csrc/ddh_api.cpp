@@ -850,7 +850,13 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     }
     c->lanes = std::max(1, std::min(8, c->lanes));
     if (c->lanes > 1) {
-      for (int l = 0; l < c->lanes; ++l) A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
+      {  // diagnostic: DDH_LANE_PRIO = priority of the lane streams (lower = higher priority)
+        const char *lp = std::getenv("DDH_LANE_PRIO");
+        for (int l = 0; l < c->lanes; ++l) {
+          if (lp) A(cudaStreamCreateWithPriority(&c->lane_st[l], cudaStreamNonBlocking, std::atoi(lp)));
+          else A(cudaStreamCreateWithFlags(&c->lane_st[l], cudaStreamNonBlocking));
+        }
+      }
       for (int l = 0; l < 9; ++l) A(cudaEventCreateWithFlags(&c->lane_ev[l], cudaEventDisableTiming));
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
