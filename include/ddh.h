@@ -102,7 +102,8 @@ typedef struct {
   int32_t lanes;        /* streaming path: concurrent sub-groups of a launch group, each on
                            its own CUDA stream forked from / joined to the ctx stream, so
                            the kernels of different sub-groups share the SMs; 1..8, 0 =
-                           auto (streams/32 in [1,2]).  Results do not depend on it.      */
+                           auto (up to 3 lanes of >= 16 streams that keep >= 2 64-pixel
+                           ICD tiles per SM).  Results do not depend on it.               */
 } ddh_params;
 
 /* Defaults: N=256, S=1, device 0, D=N, sigma^2=0.1, lambda=0.45, alpha=0.025,
@@ -217,7 +218,8 @@ int64_t ddh_frame_index(const ddh_ctx *c);
  * Kernel kinds: 0 K0 stats, 1 K1 rows_fwd, 2 K2a cols, 3 K2b r-ICD,
  * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
  * 8-10 unused (the retired cluster path); 11 S0 ks_stats, 12 S1 ks_rows_fwd,
- * 13 S2 ks_cols, 14 S3 ks_ricd, 15 S4 ks_rows_inv, 16 S5 ks_phiicd
+ * 13 S2 ks_cols, 14 S3 ks_ricd (for large launches the four colour passes
+ * ks_ricd_pass, timed as one), 15 S4 ks_rows_inv, 16 S5 ks_phiicd
  * (streaming path, default).
  * When enabled, every launch of the ctx is bracketed by two events. */
 #define DDH_KIND_COUNT 17
