@@ -1270,6 +1270,7 @@ static cudaError_t launch_icd(void (*k)(StepArgs), const StepArgs &a, cudaStream
 template <int N>
 static bool use_passes(int sc, bool r) {
   static const int on = getenv("DDH_RICD_PASSES") ? atoi(getenv("DDH_RICD_PASSES")) : 1;
+  if (on == 2) return r;  // diagnostic: passes at every size
   return r && on && !small_tiles<N>(sc) && !tiny_tiles<N>(sc);
 }
 int icd_launches(const StepArgs &a, bool r) { DDH_SDISPATCH(a.n, return use_passes<N>(a.sc, r) ? 4 : 1); return 1; }
