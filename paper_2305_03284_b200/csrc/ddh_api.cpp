@@ -178,10 +178,16 @@ cudaEvent_t *prof_begin(ddh_ctx *c, int kind, cudaStream_t st) {
   return &c->ev_pool[2 * i + 1];
 }
 
+// DDH_SKIP=<mask of S0..S5>: those launches are not issued (diagnostic: marginal cost
+// of a kernel inside the concurrent step; results invalid)
+static int skip_mask() {
+  static const int m = std::getenv("DDH_SKIP") ? std::atoi(std::getenv("DDH_SKIP")) : 0;
+  return m;
+}
 #define DDH_LAUNCH_ON(c, kind, st, call)                \
   do {                                                  \
     cudaEvent_t *end_ = prof_begin((c), (kind), (st));  \
-    DDH_CK(c, call);                                    \
+    if ((kind) < K_S0 || !(skip_mask() & (1 << ((kind) - K_S0)))) DDH_CK(c, call); \
     if (end_) cudaEventRecord(*end_, (st));             \
     (c)->launches++;                                    \
   } while (0)
@@ -405,7 +411,8 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             c->ypf_pending[l] = false;
           }
           DDH_LAUNCH_ON(c, K_S1, st, ddh::launch_s1(b, st));
-          if (last && y_next) {  // y sums of the next frame of this call, after S1 read the partials
+          const bool s4_sums = last && y_next && ddh::s4_sums_next(c->n);
+          if (last && y_next && !s4_sums) {  // y sums of the next frame of this call, after S1 read the partials
             StepArgs yb = b;
             yb.y = y_next + go;
             yb.want_y = 1;
@@ -440,7 +447,9 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
             c->launches += ddh::icd_launches(b, true) - 1;
           }
+          b.ynx = s4_sums ? y_next + go : nullptr;  // S4 forms the next frame's y sums (after S1 read them)
           DDH_LAUNCH_ON(c, K_S4, st, ddh::launch_s4(b, st));
+          b.ynx = nullptr;
           const int plane_it = b.apply_plane;
           for (int k = 0; k < sw; ++k) {  // phi M-step sweeps (plane removed in the first)
             b.icd_in = k == 0 ? c->phi[cl] + go : c->ptmp[(k - 1) & 1] + wo;

@@ -60,6 +60,7 @@ struct StepArgs {
   float *sstat;           // [sc][8] per-stream scalars of the step (ddh_stream.cu kStatW)
   double *psum_in;        // [sc][3] RemoveTipTilt sums of phi_in, 2^-16 fixed point (integer-valued; S0 adds / S1 reads)
   double *psum_out;       // [sc][3] the same sums of the output phase (S1 zeroes, last S5 adds) or null
+  const float2 *ynx;      // S4: the next frame of the call [sc][N][N] (its S0 y sums are formed here) or null
   int dbg_fault;          // debug build only (DDH_DEBUG_FAULT): a deliberately failing check, to show the checks run
 };
 
@@ -123,6 +124,8 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
+// S4 can form the next frame's S0 y sums (StepArgs::ynx) at this N
+bool s4_sums_next(int n);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
 int icd_launches(const StepArgs &a, bool r_icd);  // kernels one launch_s3 / launch_s5 enqueues (4: colour passes)
 

@@ -661,6 +661,31 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
     }
     A.cbuf[row + j] = make_float2(c, th);  // in place: this CTA read its spectrum rows before the FFT
   }
+  if (A.ynx) {  // the next frame's S0 y sums over this CTA's rows (after S1 of this frame read part0)
+    static_assert(NT == kSThreads, "S0 thread mapping");
+    __shared__ double red[32 * 2];
+    const int per = P / A.nb0, nbk = H * N / per;  // S0 blocks in this CTA (s4_sums_next: integral)
+    for (int kb = 0; kb < nbk; ++kb) {
+      const size_t base = (size_t)bx * H * N + (size_t)kb * per;
+      double yr = 0.0, yi = 0.0;
+      // ks_stats' partition and order: thread t sums the 8-pixel chunks base + 8 t + 2048 k
+      // (balanced FP32 tree per chunk, FP64 accumulation), then the same block tree
+      for (size_t p0 = base + (size_t)tid * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
+        const float4 *y4 = reinterpret_cast<const float4 *>(A.ynx + (size_t)s * P + p0);
+        float4 a[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = __ldg(y4 + k);
+        yr += (double)(((a[0].x + a[0].z) + (a[1].x + a[1].z)) + ((a[2].x + a[2].z) + (a[3].x + a[3].z)));
+        yi += (double)(((a[0].y + a[0].w) + (a[1].y + a[1].w)) + ((a[2].y + a[2].w) + (a[3].y + a[3].w)));
+      }
+      double d[2] = {yr, yi};
+      block_sum<2>(d, red);
+      if (tid == 0) {
+        A.part0[((size_t)s * A.nb0 + base / per) * 5 + 0] = d[0];
+        A.part0[((size_t)s * A.nb0 + base / per) * 5 + 1] = d[1];
+      }
+    }
+  }
 }
 
 template <int N>
@@ -1239,6 +1264,23 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
   // there); DDH_S2P=1: only small launches, 0: never (diagnostic)
   static const int staged = getenv("DDH_S2P") ? atoi(getenv("DDH_S2P")) : 2;
   DDH_SDISPATCH(a.n, return launch_s2_n<N>(a, st, staged, device_sms()));
+}
+template <int N>
+static bool s4_sums_fit() {  // a row CTA holds whole S0 blocks, with S0's thread count
+  const int per = N * N / stream_nb0(N);
+  return SCfg<N>::NTR == kSThreads && (SCfg<N>::H * N) % per == 0;
+}
+bool s4_sums_next(int n) {
+  static const int on = getenv("DDH_S4_SUMS") ? atoi(getenv("DDH_S4_SUMS")) : 1;  // 0: S0 on its own stream (diagnostic)
+  if (!on) return false;
+  switch (n) {
+    case 64: return s4_sums_fit<64>();
+    case 128: return s4_sums_fit<128>();
+    case 256: return s4_sums_fit<256>();
+    case 512: return s4_sums_fit<512>();
+    case 1024: return s4_sums_fit<1024>();
+  }
+  return false;
 }
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, return launch_pdl(ks_rows_inv<N>, dim3(N / SCfg<N>::H, a.sc), dim3(SCfg<N>::NTR), srowi_smem<N>(), st, a));
