@@ -239,13 +239,15 @@ def run_ours(args):
     if args.unfused:
         args.path = "multipass"
     # DDH_F_L2_PERSIST (64): the opt-in persisting-L2 window over the spectrum buffer
-    extra["flags"] = {"stream": 0, "multipass": 2}[args.path] | (8 if args.serial else 0) | (64 if args.l2_persist else 0)
+    extra["flags"] = {"stream": 0, "multipass": 2}[args.path] | (8 if args.serial else 0) | (64 if args.l2_persist else 0) \
+        | (128 if args.call_graphs else 0)
     t0 = time.time()
     unit = sched.StreamRank(cfg, first, S, local, F, source=args.synth, want_host=True, chunk_streams=args.chunk, **extra)
     gen_s = time.time() - t0
     ctx, y_dev, y_host, stream = unit.ctx, unit.y_dev, unit.y_host, unit.stream
     K, W = args.steps, args.warmup
     unit.steps(W)
+    unit.prime_graphs()  # untimed: capture the call graphs the timed steps replay (both parities)
     # parity sample (rank 0): one GPU step vs the oracle from the same FP32 state
     parity = None
     if rank == 0 and not args.no_parity:
@@ -345,7 +347,7 @@ def run_ours(args):
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": dict(workload_config(cfg), parallelism=f"streams x{ws} GPUs",
                                                            lanes=lanes, path=args.path, synth=args.synth,
-                                                           l2_persist=bool(args.l2_persist),
+                                                           l2_persist=bool(args.l2_persist), call_graphs=bool(args.call_graphs),
                                                            synth_seconds=round(gen_s, 1)),
         "roofline": roofline, "gpu_launches": launches, "clocks": clocks,
         "attribution_pass": {"value": frames_total / (ms_attr * 1e-3), "ms_per_step": ms_attr / K, "lanes": 1,
@@ -558,6 +560,8 @@ def main():
     ap.add_argument("--serial", action="store_true",
                     help="profiling aid: DDH_F_SERIAL for the main ctx too (the launch configuration of the "
                          "attribution pass, for ncu captures)")
+    ap.add_argument("--call-graphs", action="store_true",
+                    help="DDH_F_CALL_GRAPHS: replay multi-frame calls from chunk graphs (host-bound mode)")
     ap.add_argument("--no-l2-persist", dest="l2_persist", action="store_false",
                     help="do not opt in to the persisting-L2 window (DDH_F_L2_PERSIST)")
     ap.add_argument("--path", choices=["stream", "multipass"], default="stream",

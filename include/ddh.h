@@ -66,6 +66,19 @@ typedef enum {
                                without it (graph boundaries stop the overlap of
                                consecutive steps)                                 */
 
+#define DDH_F_CALL_GRAPHS 128u /* opt-in host-bound mode for multi-frame ddh_step: whole
+                               chunks of 8 frames (DDH_CHUNK) of a call are replayed
+                               from CUDA graphs captured once per (state parity,
+                               outputs) with stand-in buffers, the call's buffers
+                               passed through a device-side descriptor, so the host
+                               enqueues 2 operations per chunk instead of ~25 per
+                               frame (c3: 105 -> 2 us of host time per frame).  The
+                               device runs the replayed graph ~2 % slower than the
+                               directly launched streams (c3 126.7 vs 124.0 us per
+                               step), so it pays only when the host is the bound.
+                               The first chunk of each key is captured (~ms of host
+                               time); results are bit-identical either way         */
+
 #define DDH_F_L2_PERSIST 64u /* opt-in (device-wide side effect): raise the device's
                                persisting-L2 carve-out to the ctx's spectrum buffer
                                (<= 48 MiB) and give the ctx's own lane streams an

@@ -28,6 +28,11 @@
 using ddh::IcdArgs;
 using ddh::StepArgs;
 using ddh::StrehlArgs;
+using ddh::CallDesc;
+using ddh::kRelY;
+using ddh::kRelCopyPhi;
+using ddh::kRelCopyR;
+using ddh::kRelStatus;
 
 struct ddh_ctx {
   ddh_params p{};
@@ -112,6 +117,30 @@ struct ddh_ctx {
   };
   bool graphs = false;
   cudaStream_t cap_st = nullptr;  // capture stream (the ctx stream may be the legacy default stream)
+  // Call graphs (DDH_F_CALL_GRAPHS; streaming path, multi-frame ddh_step): chunks of `chunk`
+  // frames are captured once per (state parity, outputs) with stand-in
+  // buffer pointers and replayed for every later chunk, the call's real
+  // buffers passed as deltas through a device-side CallDesc (ddh_kernels.h):
+  // the host then enqueues 2 operations per chunk instead of ~25 per frame.
+  struct ChunkKey {
+    int len, cur, pcur;
+    bool pvalid, phi, r, st;
+    bool operator==(const ChunkKey &o) const {
+      return len == o.len && cur == o.cur && pcur == o.pcur && pvalid == o.pvalid && phi == o.phi && r == o.r &&
+             st == o.st;
+    }
+  };
+  struct ChunkEntry {
+    ChunkKey key;
+    cudaGraphExec_t exec;
+    uint64_t launches;
+    int cur, pcur;  // state after the chunk (psum_valid is then true)
+  };
+  bool call_graphs = false;
+  int chunk = 8;
+  bool rel_mode = false;  // capturing a call graph: pointers are stand-ins (StepArgs::rel)
+  CallDesc *desc = nullptr;
+  std::vector<ChunkEntry> ccache;
   std::vector<GraphEntry> gcache;
   std::vector<GraphKey> gseen;
   uint64_t gclock = 0;
@@ -372,6 +401,8 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
         b.part0 = c->part0 + (size_t)g0 * nb0 * 5;
         b.part1 = c->part1 + (size_t)g0 * nb1;
         b.sstat = c->sstat + (size_t)g0 * 8;
+        b.desc = c->desc;
+        b.rel = c->rel_mode ? kRelY : 0;
         b.want_y = 1;
         b.apply_plane = plane ? 1 : 0;
         b.phi_in = c->phi[cur] + go;
@@ -405,6 +436,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.la = (float)c->p.boot_alpha;
           }
           b.status = (first && status) ? status + s0 + g0 : nullptr;
+          b.rel = c->rel_mode ? (kRelY | (b.status ? kRelStatus : 0)) : 0;
           b.psum_out = first ? psum_next : nullptr;  // S1 zeroes the next frame's sums
           if (first && c->ypf_pending[l]) {  // this frame's S0 y sums, prefetched during the last frame
             DDH_CK(c, cudaStreamWaitEvent(st, c->ypf_join[l], 0));
@@ -444,6 +476,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_in = k == 0 ? c->rinit + wo : c->rtmp[(k - 1) & 1] + wo;
             b.icd_out = k == sw - 1 ? c->r + go : c->rtmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && r_out) ? r_out + go : nullptr;
+            if (c->rel_mode) b.rel = (b.rel & ~(kRelCopyPhi | kRelCopyR)) | (b.icd_copy ? kRelCopyR : 0);
             DDH_LAUNCH_ON(c, K_S3, rst, ddh::launch_s3(b, rst));
             c->launches += ddh::icd_launches(b, true) - 1;
           }
@@ -455,6 +488,7 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
             b.icd_in = k == 0 ? c->phi[cl] + go : c->ptmp[(k - 1) & 1] + wo;
             b.icd_out = k == sw - 1 ? c->phi[cl ^ 1] + go : c->ptmp[k & 1] + wo;
             b.icd_copy = (k == sw - 1 && last && phi_out) ? phi_out + go : nullptr;
+            if (c->rel_mode) b.rel = (b.rel & ~(kRelCopyPhi | kRelCopyR)) | (b.icd_copy ? kRelCopyPhi : 0);
             b.apply_plane = k == 0 ? plane_it : 0;
             b.psum_out = (k == sw - 1 && last) ? psum_next : nullptr;  // sums of the frame's phase
             DDH_LAUNCH_ON(c, K_S5, st, ddh::launch_s5(b, st));
@@ -592,6 +626,81 @@ ddh_status step_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out,
   return DDH_OK;
 }
 
+// Stand-in bases of a captured call graph (never dereferenced: the kernels add
+// the CallDesc deltas first).  Far apart, so a chunk's offsets never overlap.
+const uintptr_t kFakeY = (uintptr_t)1 << 44, kFakePhi = (uintptr_t)2 << 44, kFakeR = (uintptr_t)3 << 44,
+                kFakeSt = (uintptr_t)4 << 44;
+
+// `len` frames of a multi-frame call (streaming path, Step mode) from a
+// chunk graph, captured on first use for this (state parity, outputs) key.
+// Chunks start and end with no cross-frame work pending (the last frame of a
+// chunk prefetches nothing), so a graph depends only on the key.
+ddh_status run_chunk(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, uint8_t *status, int len) {
+  const ddh_ctx::ChunkKey key{len, c->cur, c->pcur, c->psum_valid, phi_out != nullptr, r_out != nullptr,
+                              status != nullptr};
+  const ddh_ctx::ChunkEntry *hit = nullptr;
+  for (const auto &e : c->ccache)
+    if (e.key == key) hit = &e;
+  if (!hit) {
+    if (!c->cap_st) DDH_CK(c, cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+    const int cur0 = c->cur, pcur0 = c->pcur;
+    const bool pvalid0 = c->psum_valid;
+    const uint64_t l0 = c->launches;
+    const size_t fs = (size_t)c->S * c->P;
+    cudaStream_t user_st = c->st;
+    DDH_CK(c, cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+    c->st = c->cap_st;
+    c->rel_mode = true;
+    ddh_status s = DDH_OK;
+    for (int k = 0; k < len && s == DDH_OK; ++k) {
+      const float2 *yk = reinterpret_cast<const float2 *>(kFakeY) + k * fs;
+      s = run_frame(c, yk, phi_out ? reinterpret_cast<float *>(kFakePhi) + k * fs : nullptr,
+                    r_out ? reinterpret_cast<float *>(kFakeR) + k * fs : nullptr,
+                    status ? reinterpret_cast<uint8_t *>(kFakeSt) + (size_t)k * c->S : nullptr, Mode::Step,
+                    c->p.n_k, k + 1 < len ? yk + fs : nullptr);
+    }
+    c->rel_mode = false;
+    c->st = user_st;
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(c->cap_st, &graph);
+    const int cur1 = c->cur, pcur1 = c->pcur;
+    c->cur = cur0;
+    c->pcur = pcur0;
+    c->psum_valid = pvalid0;
+    c->y_prefetched = nullptr;
+    const uint64_t nl = c->launches - l0;
+    c->launches = l0;
+    if (s != DDH_OK || ec != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      if (s != DDH_OK) return s;
+      return fail(c, DDH_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(ec));
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ei != cudaSuccess) return fail(c, DDH_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ei));
+    if (c->ccache.size() >= kGraphCache) {
+      cudaGraphExecDestroy(c->ccache.front().exec);
+      c->ccache.erase(c->ccache.begin());
+    }
+    c->ccache.push_back({key, exec, nl, cur1, pcur1});
+    hit = &c->ccache.back();
+  }
+  CallDesc d;
+  d.dy = (unsigned long long)((uintptr_t)y - kFakeY);
+  d.dphi = (unsigned long long)((uintptr_t)phi_out - kFakePhi);
+  d.dr = (unsigned long long)((uintptr_t)r_out - kFakeR);
+  d.dst = (unsigned long long)((uintptr_t)status - kFakeSt);
+  DDH_CK(c, ddh::launch_set_desc(c->desc, d, c->st));
+  DDH_CK(c, cudaGraphLaunch(hit->exec, c->st));
+  c->launches += hit->launches + 1;
+  c->cur = hit->cur;
+  c->pcur = hit->pcur;
+  c->psum_valid = true;
+  c->y_prefetched = nullptr;
+  return DDH_OK;
+}
+
 double inv3(const double G[9], double out[9]) {
   const double a = G[0], b = G[1], cc = G[2], d = G[3], e = G[4], f = G[5], g = G[6], h = G[7], i = G[8];
   const double A = e * i - f * h, B = -(d * i - f * g), C = d * h - e * g;
@@ -625,6 +734,8 @@ void free_ctx(ddh_ctx *c) {
     }
   }
   for (auto &g : c->gcache) cudaGraphExecDestroy(g.exec);
+  for (auto &g : c->ccache) cudaGraphExecDestroy(g.exec);
+  if (c->desc) cudaFree(c->desc);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->lane_ev)
@@ -840,6 +951,14 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     c->graphs = gr ? std::atoi(gr) != 0 : (p.flags & DDH_F_GRAPHS) != 0;
   }
   if (c->streaming) A(ddh::init_stream(n));
+  if (c->streaming) {  // call graphs (DDH_F_CALL_GRAPHS; DDH_CALL_GRAPHS=0/1 overrides; DDH_CHUNK: frames per graph)
+    const char *cg = std::getenv("DDH_CALL_GRAPHS");
+    const char *ck = std::getenv("DDH_CHUNK");
+    c->call_graphs = cg ? std::atoi(cg) != 0 : (p.flags & DDH_F_CALL_GRAPHS) && !(p.flags & DDH_F_SERIAL);
+    c->chunk = std::max(2, ck ? std::atoi(ck) : 8);
+    A(cudaMalloc((void **)&c->desc, sizeof(CallDesc)));
+    A(cudaMemset(c->desc, 0, sizeof(CallDesc)));
+  }
   if (c->streaming) {
     const char *ev = std::getenv("DDH_LANES");  // diagnostic override
     c->lanes = (p.flags & DDH_F_SERIAL) ? 1 : ev ? std::atoi(ev) : p.lanes;
@@ -1007,7 +1126,18 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
     return fail(c, DDH_E_INVAL, "ddh_step: y must be 16-byte aligned, phi_out / r_out 8-byte aligned");
   DDH_CK(c, cudaSetDevice(c->p.device));
   const size_t fs = (size_t)c->S * c->P;
-  for (int t = 0; t < T; ++t) {
+  int t = 0;
+  // whole chunks from call graphs (one launch group, no profiling; frames still in
+  // flight from the host pipeline are ordered by the ctx stream)
+  if (c->call_graphs && c->streaming && !c->profiling && c->sc == c->S && !c->y_prefetched) {
+    for (; t + c->chunk <= T; t += c->chunk) {
+      s = run_chunk(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
+                    r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr, c->chunk);
+      if (s != DDH_OK) return s;
+      c->frame += c->chunk;
+    }
+  }
+  for (; t < T; ++t) {
     s = step_frame(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
                    r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr,
                    t + 1 < T ? (const float2 *)y + (t + 1) * fs : nullptr);

@@ -21,6 +21,15 @@
 
 namespace ddh {
 
+// Base pointers of one multi-frame call replayed from a CUDA graph (ddh_api.cpp
+// call graphs): the graph's kernels carry offsets from fixed stand-in bases and
+// add these deltas (real base - stand-in base, modulo 2^64) at entry, so one
+// captured chunk of frames serves every call whatever its buffers.
+struct CallDesc {
+  unsigned long long dy, dphi, dr, dst;  // y (and the next frame), phi_out, r_out, status
+};
+enum : int { kRelY = 1, kRelCopyPhi = 2, kRelCopyR = 4, kRelStatus = 8 };
+
 struct StepArgs {
   int n;        // N
   int sc;       // streams in this launch group
@@ -60,6 +69,8 @@ struct StepArgs {
   float *sstat;           // [sc][8] per-stream scalars of the step (ddh_stream.cu kStatW)
   double *psum_in;        // [sc][3] RemoveTipTilt sums of phi_in, 2^-16 fixed point (integer-valued; S0 adds / S1 reads)
   double *psum_out;       // [sc][3] the same sums of the output phase (S1 zeroes, last S5 adds) or null
+  const CallDesc *desc;   // call-graph replay: deltas for the pointers flagged in `rel`, else unused
+  int rel;                // kRel* bits: y / ynx, icd_copy (phi_out or r_out), status are stand-in pointers
   const float2 *ynx;      // S4: the next frame of the call [sc][N][N] (its S0 y sums are formed here) or null
   int dbg_fault;          // debug build only (DDH_DEBUG_FAULT): a deliberately failing check, to show the checks run
 };
@@ -124,6 +135,7 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s2(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st);
 cudaError_t launch_s4(const StepArgs &a, cudaStream_t st);
+cudaError_t launch_set_desc(CallDesc *d, const CallDesc &v, cudaStream_t st);
 // S4 can form the next frame's S0 y sums (StepArgs::ynx) at this N
 bool s4_sums_next(int n);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);

@@ -54,6 +54,25 @@ namespace {
 //   [0] Re mu  [1] Im mu  [2..4] plane c0, c1, c2  [5] kappa  [6] degenerate (0 / 1)
 constexpr int kStatW = 8;
 
+// Call-graph replay (CallDesc): the stand-in pointers of a captured chunk
+// become this call's buffers at their point of use (the kernels never modify
+// their argument struct: a written kernel parameter is copied to local memory).
+template <typename T>
+__device__ __forceinline__ T *add_delta(T *p, unsigned long long d) {
+  return reinterpret_cast<T *>(reinterpret_cast<unsigned long long>(p) + d);
+}
+__device__ __forceinline__ const float2 *call_y(const StepArgs &A, const float2 *p) {
+  return (A.rel & kRelY) ? add_delta(p, A.desc->dy) : p;
+}
+__device__ __forceinline__ float *call_copy(const StepArgs &A) {
+  if (A.rel & kRelCopyPhi) return add_delta(A.icd_copy, A.desc->dphi);
+  if (A.rel & kRelCopyR) return add_delta(A.icd_copy, A.desc->dr);
+  return A.icd_copy;
+}
+__device__ __forceinline__ uint8_t *call_status(const StepArgs &A) {
+  return (A.rel & kRelStatus) ? add_delta(A.status, A.desc->dst) : A.status;
+}
+
 constexpr int kSThreads = 256;
 #ifndef DDH_ROW_THREADS
 #define DDH_ROW_THREADS 256
@@ -185,9 +204,10 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
   double yr = 0.0, yi = 0.0;
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
+  const float2 *Y = A.want_y ? call_y(A, A.y) : nullptr;
   for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
     if (A.want_y) {
-      const float4 *y4 = reinterpret_cast<const float4 *>(A.y + off + p0);
+      const float4 *y4 = reinterpret_cast<const float4 *>(Y + off + p0);
       float4 a[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) a[k] = __ldg(y4 + k);  // kept in L2 for S1
@@ -244,9 +264,10 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
   // issue the loads first (y: 8 B, phi: 4 B per pixel, comb t + TPV e); the
   // frames are read-only user input, so they may be read before the wait
   DDH_PDL_TRIGGER();
+  const float2 *Y = call_y(A, A.y);
   float2 v[E];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = A.y[row + t + TPV * e];
+  for (int e = 0; e < E; ++e) v[e] = Y[row + t + TPV * e];
   load_tw<N>(tw, A.tw4, tid, NT);
   DDH_PDL_WAIT();
   if (t == 0) {  // phi row -> L2 (read after the stats)
@@ -363,7 +384,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
     const size_t row0 = (size_t)s * P + (size_t)bx * H * N;
     if (y_part) {
       mbar_expect_tx(&mb[st], Q::YB + Q::FB);
-      bulk_g2s(dst, A.y + row0, Q::YB, &mb[st]);
+      bulk_g2s(dst, call_y(A, A.y) + row0, Q::YB, &mb[st]);
     }
     if (phi_part) bulk_g2s(dst + Q::YB, A.phi_in + row0, Q::FB, &mb[st]);
   };
@@ -490,7 +511,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   const bool degenerate = !(d2 > 0.0);
   const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
   if (blockIdx.x == 0 && tid == 0) {
-    if (A.status) A.status[s] = degenerate ? 1 : 0;
+    if (A.status) call_status(A)[s] = degenerate ? 1 : 0;
     A.sstat[(size_t)s * kStatW + 5] = kappa;
     A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
   }
@@ -573,7 +594,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 2) ks_cols_p(StepArgs A) {
     const bool degenerate = !(d2 > 0.0);
     const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
     if (bx == 0 && tid == 0) {
-      if (A.status) A.status[s] = degenerate ? 1 : 0;
+      if (A.status) call_status(A)[s] = degenerate ? 1 : 0;
       A.sstat[(size_t)s * kStatW + 5] = kappa;
       A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
     }
@@ -626,7 +647,7 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   const size_t row = (size_t)s * P + (size_t)i * N;
   DDH_PDL_TRIGGER();
   {  // y is read-only user input: staged before the wait
-    const char *src = reinterpret_cast<const char *>(A.y + (size_t)s * P + (size_t)bx * H * N);
+    const char *src = reinterpret_cast<const char *>(call_y(A, A.y) + (size_t)s * P + (size_t)bx * H * N);
     const unsigned dst = (unsigned)__cvta_generic_to_shared(ys);
     for (int k = tid * 16; k < H * N * 8; k += NT * 16)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k), "l"(src + k));
@@ -665,13 +686,14 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
     static_assert(NT == kSThreads, "S0 thread mapping");
     __shared__ double red[32 * 2];
     const int per = P / A.nb0, nbk = H * N / per;  // S0 blocks in this CTA (s4_sums_next: integral)
+    const float2 *YN = call_y(A, A.ynx);
     for (int kb = 0; kb < nbk; ++kb) {
       const size_t base = (size_t)bx * H * N + (size_t)kb * per;
       double yr = 0.0, yi = 0.0;
       // ks_stats' partition and order: thread t sums the 8-pixel chunks base + 8 t + 2048 k
       // (balanced FP32 tree per chunk, FP64 accumulation), then the same block tree
       for (size_t p0 = base + (size_t)tid * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
-        const float4 *y4 = reinterpret_cast<const float4 *>(A.ynx + (size_t)s * P + p0);
+        const float4 *y4 = reinterpret_cast<const float4 *>(YN + (size_t)s * P + p0);
         float4 a[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) a[k] = __ldg(y4 + k);
@@ -818,6 +840,7 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   // one column pair per thread when the thread count allows it (constant address steps)
   constexpr int STEP = NTH % PR == 0 ? NTH : 1;
   const int pj0 = tid % PR, oi0 = tid / PR;
+  float *const copy = call_copy(A);
   for (int idx = NTH % PR == 0 ? oi0 * PR + pj0 : tid; idx < T * PR; idx += (NTH % PR == 0 ? STEP : NTH)) {
     const int oi = idx / PR, pj = idx - oi * PR;
     const int li = oi + kHalo;
@@ -830,7 +853,7 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
       v = make_float2(fmaxf(qv.x, A.r_min), fmaxf(qv.y, A.r_min));
     }
     *reinterpret_cast<float2 *>(A.icd_out + gidx) = v;
-    if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + gidx) = v;
+    if (copy) *reinterpret_cast<float2 *>(copy + gidx) = v;
   }
 }
 
@@ -971,6 +994,7 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
       phiicd_sweep<N, TILE, false>(ps, cts, tid, i0, j0, w, prior);
   }
   // output (and the RemoveTipTilt sums of the output phase for the next frame's S1)
+  float *const copy = call_copy(A);
   constexpr int PR = T / 2;  // pixel pairs per tile row
   double e0 = 0.0, ex = 0.0, ey = 0.0;
   if constexpr (NTH % PR == 0) {
@@ -988,7 +1012,7 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
       const float *q = psrc + (2 * (li & 1) * G::kSub + (li >> 1)) * G::kSubP;
       const float2 v = degenerate ? *reinterpret_cast<const float2 *>(pin + (g - off)) : make_float2(q[0], q[G::kSub * G::kSubP]);
       *reinterpret_cast<float2 *>(A.icd_out + g) = v;
-      if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+      if (copy) *reinterpret_cast<float2 *>(copy + g) = v;
       if (A.psum_out) {
         const int gi = i0 + oi;
         const int2 sp = __ldg(A.rowspan + gi);
@@ -1010,7 +1034,7 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
                                   : make_float2(ps[G::sidx(2 * (li & 1), li >> 1, pj + kHalo / 2)],
                                                 ps[G::sidx(2 * (li & 1) + 1, li >> 1, pj + kHalo / 2)]);
       *reinterpret_cast<float2 *>(A.icd_out + g) = v;
-      if (A.icd_copy) *reinterpret_cast<float2 *>(A.icd_copy + g) = v;
+      if (copy) *reinterpret_cast<float2 *>(copy + g) = v;
       if (A.psum_out) {
         const int gi = i0 + oi, gj = j0 + 2 * pj;
         const int2 sp = __ldg(A.rowspan + gi);
@@ -1076,7 +1100,7 @@ __device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
     v = r_update(ri, q, A.r_b6 * (bs.x + bs.y), A.r_b6 * (ss.x + ss.y), A.r_min);
   }
   out[g] = v;
-  if (A.icd_copy) A.icd_copy[off + g] = v;
+  if (A.icd_copy) call_copy(A)[off + g] = v;
 }
 
 // one thread per pixel of the class; grid (N^2/4 / 256, streams).  (A
@@ -1269,6 +1293,11 @@ template <int N>
 static bool s4_sums_fit() {  // a row CTA holds whole S0 blocks, with S0's thread count
   const int per = N * N / stream_nb0(N);
   return SCfg<N>::NTR == kSThreads && (SCfg<N>::H * N) % per == 0;
+}
+__global__ void ks_set_desc(CallDesc *d, CallDesc v) { *d = v; }
+cudaError_t launch_set_desc(CallDesc *d, const CallDesc &v, cudaStream_t st) {
+  ks_set_desc<<<1, 1, 0, st>>>(d, v);
+  return cudaGetLastError();
 }
 bool s4_sums_next(int n) {
   static const int on = getenv("DDH_S4_SUMS") ? atoi(getenv("DDH_S4_SUMS")) : 1;  // 0: S0 on its own stream (diagnostic)

@@ -17,6 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DDH_LIB") or os.path.join(_HERE, "lib", "libddh.so")
 
 DDH_F_NO_TIPTILT = 1
+DDH_F_CALL_GRAPHS = 128  # multi-frame calls replayed from chunk graphs (include/ddh.h)
 
 _STATUS = {0: "DDH_OK", 1: "DDH_E_INVAL", 2: "DDH_E_CUDA", 3: "DDH_E_NOMEM", 4: "DDH_E_STATE"}
 

@@ -497,6 +497,35 @@ def test_state_continuity_bit_exact():
     assert torch.equal(pa, pc)
 
 
+def test_call_graphs_bit_exact():
+    """Multi-frame calls replay captured chunk graphs (include/ddh.h
+    DDH_F_CALL_GRAPHS): graphs captured with stand-in buffers and replayed on other
+    buffers, chunks of both state parities and a direct remainder give the
+    same bits as direct launches (phi-hat, r-hat, status, state), with lanes,
+    the r-ICD side stream and the fused next-frame sums in play."""
+    from paper_2305_03284_b200.ddh import DDH_F_CALL_GRAPHS
+    n, S, T = 256, 40, 19
+    y, _, _ = frames(n, S, T)
+    yt = torch.from_numpy(y).to(DEV)
+    res = []
+    for flags in (0, DDH_F_CALL_GRAPHS):
+        ctx = DDH(n, S, noise_var=0.1, flags=flags)
+        po = torch.empty((T, S, n, n), device=DEV)
+        ro = torch.empty_like(po)
+        st = torch.empty((T, S), dtype=torch.uint8, device=DEV)
+        ctx.step(yt[:9].contiguous(), po[:9], ro[:9], st[:9])          # chunk (captured) + 1 frame
+        ctx.step(yt[9:].contiguous(), po[9:], ro[9:], st[9:])          # other parity: captured; then 2 frames
+        po2 = torch.empty((8, S, n, n), device=DEV)
+        ctx.step(yt[:8].contiguous(), po2)                             # replay on new buffers, phi only
+        r_, p_, f_ = ctx.get_state()
+        res.append((po, ro, st, po2, r_, p_, f_))
+    for a, b in zip(res[0], res[1]):
+        if isinstance(a, torch.Tensor):
+            assert torch.equal(a, b)
+        else:
+            assert a == b
+
+
 def test_sharding_and_launch_groups_bit_exact():
     """Streams are independent: the per-stream results do not depend on how
     streams are grouped into launches or split over contexts (G-GPU sharding
