@@ -74,13 +74,19 @@ __device__ __forceinline__ uint8_t *call_status(const StepArgs &A) {
 }
 
 constexpr int kSThreads = 256;
+// 128-thread row CTAs (S1, S4) and S0 blocks: c3 124.0 -> 120.4 us per step, c4 +1.8 %,
+// c2 -0.5 %, c5 -1.8 % against 256 (the S4-fused next-frame sums need S0's thread count)
 #ifndef DDH_ROW_THREADS
-#define DDH_ROW_THREADS 256
+#define DDH_ROW_THREADS 128
 #endif
 #ifndef DDH_COL_THREADS
 #define DDH_COL_THREADS 256
 #endif
 constexpr int kRowThreads = DDH_ROW_THREADS, kColThreads = DDH_COL_THREADS;
+#ifndef DDH_S0_THREADS
+#define DDH_S0_THREADS DDH_ROW_THREADS
+#endif
+constexpr int kS0Threads = DDH_S0_THREADS;  // S0 (and S4's fused next-frame sums): threads per block
 
 template <int N> struct SCfg {
   static constexpr int E = RPlan<N>::E;
@@ -183,7 +189,7 @@ __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g
 
 // ------------------------------------------------------------------ S0
 
-// grid (nb0, sc), block 256: block b sums pixels [b P/nb0, (b+1) P/nb0) of
+// grid (nb0, sc), block kS0Threads: block b sums pixels [b P/nb0, (b+1) P/nb0) of
 // stream s in chunks of 8 consecutive pixels (16-byte loads); nb0 depends on
 // N only (2048-pixel blocks, at most 64), so the partials and everything
 // downstream are independent of the launch grouping, and a single stream's
@@ -192,7 +198,7 @@ __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g
 // balanced FP32 tree (exact for a constant frame, so the degenerate test
 // ||y - mu|| = 0 of R31 stays exact) and accumulated in FP64; phi plane sums:
 // FP32 per-thread partials; FP64 block sums.
-__global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
+__global__ void __launch_bounds__(kS0Threads) ks_stats(StepArgs A) {
   __shared__ double red[32 * 3];
   const int n = A.n, lg = 31 - __clz(n);
   const size_t P = (size_t)n * n;
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(kSThreads) ks_stats(StepArgs A) {
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
   const float2 *Y = A.want_y ? call_y(A, A.y) : nullptr;
-  for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
+  for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kS0Threads * 8) {
     if (A.want_y) {
       const float4 *y4 = reinterpret_cast<const float4 *>(Y + off + p0);
       float4 a[4];
@@ -353,7 +359,7 @@ template <int N> struct S1P {
 };
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTR, 2) ks_rows_fwd_p(StepArgs A) {
+__global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_p(StepArgs A) {
   using C = SCfg<N>;
   using Q = S1P<N>;
   constexpr int E = C::E, TPV = C::TPV, H = C::H, NT = C::NTR, P = N * N, NR = N / H;
@@ -682,17 +688,17 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
     }
     A.cbuf[row + j] = make_float2(c, th);  // in place: this CTA read its spectrum rows before the FFT
   }
+  if constexpr (NT == kS0Threads) {  // S0's thread mapping (s4_sums_next checks it on the host)
   if (A.ynx) {  // the next frame's S0 y sums over this CTA's rows (after S1 of this frame read part0)
-    static_assert(NT == kSThreads, "S0 thread mapping");
     __shared__ double red[32 * 2];
     const int per = P / A.nb0, nbk = H * N / per;  // S0 blocks in this CTA (s4_sums_next: integral)
     const float2 *YN = call_y(A, A.ynx);
     for (int kb = 0; kb < nbk; ++kb) {
       const size_t base = (size_t)bx * H * N + (size_t)kb * per;
       double yr = 0.0, yi = 0.0;
-      // ks_stats' partition and order: thread t sums the 8-pixel chunks base + 8 t + 2048 k
+      // ks_stats' partition and order: thread t sums the 8-pixel chunks base + 8 t + 8 kS0Threads k
       // (balanced FP32 tree per chunk, FP64 accumulation), then the same block tree
-      for (size_t p0 = base + (size_t)tid * 8; p0 < base + per; p0 += (size_t)kSThreads * 8) {
+      for (size_t p0 = base + (size_t)tid * 8; p0 < base + per; p0 += (size_t)kS0Threads * 8) {
         const float4 *y4 = reinterpret_cast<const float4 *>(YN + (size_t)s * P + p0);
         float4 a[4];
 #pragma unroll
@@ -707,6 +713,7 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
         A.part0[((size_t)s * A.nb0 + base / per) * 5 + 1] = d[1];
       }
     }
+  }
   }
 }
 
@@ -1252,12 +1259,12 @@ static cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 
 cudaError_t init_stream(int n) { DDH_SDISPATCH(n, return init_stream_n<N>()); }
 int stream_nb1(int n) { DDH_SDISPATCH(n, return N / SCfg<N>::H); }
-// S0 pixel blocks per stream: 2048-pixel blocks (one pass of a 256-thread
-// CTA), at most 64 (the partials every later stage adds per warp)
+// S0 pixel blocks per stream: 2048-pixel blocks (8-pixel chunks, kS0Threads
+// per pass), at most 64 (the partials every later stage adds per warp)
 int stream_nb0(int n) { return n * n / 2048 < 64 ? (n * n / 2048 < 1 ? 1 : n * n / 2048) : 64; }
 
 cudaError_t launch_s0(const StepArgs &a, cudaStream_t st) {
-  return launch_pdl(ks_stats, dim3(a.nb0, a.sc), dim3(kSThreads), 0, st, a);
+  return launch_pdl(ks_stats, dim3(a.nb0, a.sc), dim3(kS0Threads), 0, st, a);
 }
 cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   static const int persist = getenv("DDH_S1P") ? atoi(getenv("DDH_S1P")) : 1;
@@ -1265,7 +1272,8 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   if (persist) {
     DDH_SDISPATCH(a.n, ({
                     const int total = N / SCfg<N>::H * a.sc;
-                    const int grid = total < 2 * sms ? total : 2 * sms;
+                    constexpr int per_sm = 512 / SCfg<N>::NTR;  // resident CTAs per SM (smem, registers)
+                    const int grid = total < per_sm * sms ? total : per_sm * sms;
                     return launch_pdl(ks_rows_fwd_p<N>, dim3(grid), dim3(SCfg<N>::NTR), S1P<N>::SMEM, st, a);
                   }));
   }
@@ -1292,7 +1300,7 @@ cudaError_t launch_s2(const StepArgs &a, cudaStream_t st) {
 template <int N>
 static bool s4_sums_fit() {  // a row CTA holds whole S0 blocks, with S0's thread count
   const int per = N * N / stream_nb0(N);
-  return SCfg<N>::NTR == kSThreads && (SCfg<N>::H * N) % per == 0;
+  return SCfg<N>::NTR == kS0Threads && (SCfg<N>::H * N) % per == 0;
 }
 __global__ void ks_set_desc(CallDesc *d, CallDesc v) { *d = v; }
 cudaError_t launch_set_desc(CallDesc *d, const CallDesc &v, cudaStream_t st) {
