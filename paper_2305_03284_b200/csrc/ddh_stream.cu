@@ -82,6 +82,9 @@ constexpr int kSThreads = 256;
 #ifndef DDH_COL_THREADS
 #define DDH_COL_THREADS 256
 #endif
+#ifndef DDH_COL_MINW
+#define DDH_COL_MINW 16
+#endif
 constexpr int kRowThreads = DDH_ROW_THREADS, kColThreads = DDH_COL_THREADS;
 #ifndef DDH_S0_THREADS
 #define DDH_S0_THREADS DDH_ROW_THREADS
@@ -93,7 +96,7 @@ template <int N> struct SCfg {
   static constexpr int TPV = N / E;                                  // threads per vector
   static constexpr int H = (kRowThreads / TPV) < 1 ? 1 : kRowThreads / TPV;  // rows per row CTA
   static constexpr int NTR = H * TPV;                                // threads per row CTA
-  static constexpr int W = (kColThreads / TPV) < 16 ? 16 : kColThreads / TPV;  // cols per col CTA
+  static constexpr int W = (kColThreads / TPV) < DDH_COL_MINW ? DDH_COL_MINW : kColThreads / TPV;  // cols per col CTA
   static constexpr int NTC = W * TPV;                                // threads per col CTA
   static constexpr int RPITCH = N + N / 16;                          // padded row pitch
 };
@@ -557,11 +560,10 @@ template <int N> struct S2P {
 };
 
 template <int N>
-__global__ void __launch_bounds__(SCfg<N>::NTC, 2) ks_cols_p(StepArgs A) {
+__global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(StepArgs A) {
   using C = SCfg<N>;
   using Q = S2P<N>;
   constexpr int E = C::E, TPV = C::TPV, W = C::W, NT = C::NTC, P = N * N, NC = N / W;
-  static_assert(NT == 256, "256-thread column CTAs");
   extern __shared__ float4 smem4[];
   float4 *tw = smem4;
   char *stage0 = reinterpret_cast<char *>(smem4 + N);
@@ -1285,8 +1287,9 @@ template <int N>
 static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, int staged, int sms) {
   if constexpr (N <= 256) {
     const int total = N / SCfg<N>::W * a.sc;
+    constexpr int per_sm = 512 / SCfg<N>::NTC;  // resident CTAs per SM (smem, registers)
     if (staged == 2 || (staged && total <= 2 * sms))  // 2: persistent staged form for every launch (diagnostic)
-      return launch_pdl(ks_cols_p<N>, dim3(total < 2 * sms ? total : 2 * sms), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
+      return launch_pdl(ks_cols_p<N>, dim3(total < per_sm * sms ? total : per_sm * sms), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
   }
   return launch_pdl(ks_cols<N>, dim3(N / SCfg<N>::W, a.sc), dim3(SCfg<N>::NTC), scol_smem<N>(), st, a);
 }
