@@ -1073,40 +1073,71 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
 // bits as the halo-tile kernels (tests/test_gpu_parity.py kernel variants).
 
 // neighbour (DI, DJ) of a colour-C pixel (i, j), periodic boundary (r-ICD)
+template <typename T>
+__device__ __forceinline__ T *opaque_ptr(T *p) {
+  asm("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
+
+// One qGGMRF r update (R6-R9) from the pixel's value ri, its q and its 8
+// neighbours as (n(-1,0), n(1,0)), (n(0,-1), n(0,1)), (d(-1,-1), d(-1,1)),
+// (d(1,-1), d(1,1)): the expressions and their order of the tile kernels, so
+// every r-ICD kernel produces the same bits.
+__device__ __forceinline__ float ricd_px(const StepArgs &A, float ri, float q, float2 nA, float2 nB, float2 dA,
+                                         float2 dB) {
+  const float h = A.r_h, gg = A.r_g, kq = A.r_k;
+  const float2 wA = qgg_w2(ri, nA, h, gg, kq), wB = qgg_w2(ri, nB, h, gg, kq);
+  const float2 wC = qgg_w2(ri, dA, h, gg, kq), wD = qgg_w2(ri, dB, h, gg, kq);
+  const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+  const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+  return r_update(ri, q, A.r_b6 * (bs.x + bs.y), A.r_b6 * (ss.x + ss.y), A.r_min);
+}
+
+// Indices are 32-bit within the stream (N^2 <= 2^20): one row offset per
+// neighbour row and one wrapped column per neighbour column, so each load is
+// one 32-bit add and one wide multiply-add onto the stream base.
 template <int N, int C, int DI, int DJ>
-__device__ __forceinline__ float rnb(const float *__restrict__ in, const float *out, int i, int j) {
+__device__ __forceinline__ float rnb(const float *__restrict__ in, const float *out, const int (&ro)[3],
+                                     const int (&co)[3]) {
   constexpr int CI = C >> 1, CJ = C & 1, NC = 2 * ((CI + DI) & 1) + ((CJ + DJ) & 1);
   const float *src = NC < C ? out : in;  // lower colours were written by earlier passes (read-only now)
-  return __ldg(src + (size_t)((i + DI) & (N - 1)) * N + ((j + DJ) & (N - 1)));
+  return __ldg(src + (unsigned)(ro[DI + 1] + co[DJ + 1]));
 }
 
 template <int N, int C>
 __device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
   constexpr int CI = C >> 1, CJ = C & 1, H = N / 2, P = N * N;
   const int i = 2 * (p / H) + CI, j = 2 * (p % H) + CJ;
-  const size_t off = (size_t)s * P, g = (size_t)i * N + j;
-  const float *__restrict__ in = A.icd_in + off;
-  float *out = A.icd_out + off;
-  const bool degenerate = A.sstat[(size_t)s * kStatW + 6] != 0.f;
+  const size_t off = (size_t)s * P;
+  const unsigned g = (unsigned)(i * N + j);
+  // stream bases made opaque, so every neighbour address is one wide
+  // multiply-add of its 32-bit index (not a 64-bit add chain per load)
+  const float *__restrict__ in = opaque_ptr(A.icd_in + off);
+  float *out = opaque_ptr(A.icd_out + off);
+  // the degenerate flag is loaded beside the pixel's operands, not before them
+  const float dflag = A.sstat[(size_t)s * kStatW + 6];
   DDH_DBG(i < N && j < N);
   float v;
-  if (degenerate) {
-    v = in[g];
-  } else if (!A.r_prior) {
-    v = fmaxf(__ldg(A.q + off + g), A.r_min);
+  if (!A.r_prior) {
+    v = dflag != 0.f ? in[g] : fmaxf(__ldg(A.q + off + g), A.r_min);
   } else {
-    const float q = __ldg(A.q + off + g);
-    const float ri = in[g];
-    const float2 nA = make_float2(rnb<N, C, -1, 0>(in, out, i, j), rnb<N, C, 1, 0>(in, out, i, j));
-    const float2 nB = make_float2(rnb<N, C, 0, -1>(in, out, i, j), rnb<N, C, 0, 1>(in, out, i, j));
-    const float2 dA = make_float2(rnb<N, C, -1, -1>(in, out, i, j), rnb<N, C, -1, 1>(in, out, i, j));
-    const float2 dB = make_float2(rnb<N, C, 1, -1>(in, out, i, j), rnb<N, C, 1, 1>(in, out, i, j));
-    const float h = A.r_h, gg = A.r_g, kq = A.r_k;
-    const float2 wA = qgg_w2(ri, nA, h, gg, kq), wB = qgg_w2(ri, nB, h, gg, kq);
-    const float2 wC = qgg_w2(ri, dA, h, gg, kq), wD = qgg_w2(ri, dB, h, gg, kq);
-    const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
-    const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
-    v = r_update(ri, q, A.r_b6 * (bs.x + bs.y), A.r_b6 * (ss.x + ss.y), A.r_min);
+    // q is issued with the neighbour loads (volatile: left to itself the
+    // compiler sinks it behind the weights, exposing its latency in r_update)
+    float q;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(q) : "l"(A.q + off + g));
+    const float ri = __ldg(in + g);  // written only by this thread, after this read
+    // periodic neighbour rows / columns (only one side of a colour class can wrap)
+    const int ro[3] = {CI == 0 ? ((i - 1) & (N - 1)) * N : (i - 1) * N, i * N,
+                       CI == 1 ? ((i + 1) & (N - 1)) * N : (i + 1) * N};
+    const int co[3] = {CJ == 0 ? (j - 1) & (N - 1) : j - 1, j, CJ == 1 ? (j + 1) & (N - 1) : j + 1};
+    const float2 nA = make_float2(rnb<N, C, -1, 0>(in, out, ro, co), rnb<N, C, 1, 0>(in, out, ro, co));
+    const float2 nB = make_float2(rnb<N, C, 0, -1>(in, out, ro, co), rnb<N, C, 0, 1>(in, out, ro, co));
+    const float2 dA = make_float2(rnb<N, C, -1, -1>(in, out, ro, co), rnb<N, C, -1, 1>(in, out, ro, co));
+    const float2 dB = make_float2(rnb<N, C, 1, -1>(in, out, ro, co), rnb<N, C, 1, 1>(in, out, ro, co));
+    // a degenerate frame keeps r (its root is computed and discarded, so no
+    // load waits for the flag)
+    const float x = ricd_px(A, ri, q, nA, nB, dA, dB);
+    v = dflag != 0.f ? ri : x;
   }
   out[g] = v;
   if (A.icd_copy) call_copy(A)[off + g] = v;
@@ -1115,11 +1146,87 @@ __device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
 // one thread per pixel of the class; grid (N^2/4 / 256, streams).  (A
 // grid-stride form sized to the resident CTA slots measured slower in the
 // concurrent step: 134.9 vs 128.5 us at c3.)
+#ifndef DDH_RICD_MINB
+#define DDH_RICD_MINB 8
+#endif
 template <int N, int C>
-__global__ void __launch_bounds__(256) ks_ricd_pass(StepArgs A) {
+__global__ void __launch_bounds__(256, DDH_RICD_MINB) ks_ricd_pass(StepArgs A) {
   DDH_PDL_TRIGGER();
   DDH_PDL_WAIT();
   ricd_pass_px<N, C>(A, blockIdx.y, blockIdx.x * 256 + threadIdx.x);
+}
+
+// ----------------------------------- r-ICD as two row-parity launches
+// The four colour passes folded in pairs: launch RP = 0 updates colours 0 and
+// 1 (rows i even), launch RP = 1 colours 2 and 3 (rows i odd).  A thread owns
+// the pixel pair (i, 2p), (i, 2p+1) and a CTA whole rows, so the pair's
+// colour-(RP,1) pixel finds the new colour-(RP,0) values of (i, 2p) and
+// (i, 2p+2) -- including the periodic wrap of the row -- in shared memory
+// after one barrier.  Each thread loads one float2 from each of rows i-1, i,
+// i+1 and of q (the columns 2p-1 and 2p+2 come from the neighbouring pairs
+// through shared memory): 4 vector loads per pixel pair instead of 20 scalar
+// loads, and two launches per sweep instead of four.  Rows i +- 1 are of the
+// other parity: not yet updated for RP = 0 (read from the sweep's input),
+// already updated for RP = 1 (read from its output).  Same arithmetic
+// (ricd_px) and colour order as the passes and the tiles, so the same bits.
+#ifndef DDH_ROWS_NT
+#define DDH_ROWS_NT 128
+#endif
+#ifndef DDH_ROWS_MINB
+#define DDH_ROWS_MINB 1
+#endif
+template <int N> struct RowsCfg {
+  static constexpr int H = N / 2, NT = H > DDH_ROWS_NT ? H : DDH_ROWS_NT, RPC = NT / H;  // pairs per row, threads, rows per CTA
+  static constexpr int MINB = DDH_ROWS_MINB * DDH_ROWS_NT / NT > 0 ? DDH_ROWS_MINB * DDH_ROWS_NT / NT : 1;
+};
+template <int N, int RP>
+__global__ void __launch_bounds__(RowsCfg<N>::NT, RowsCfg<N>::MINB) ks_ricd_rows(StepArgs A) {
+  using RC = RowsCfg<N>;
+  constexpr int H = RC::H, NT = RC::NT, RPC = RC::RPC, P = N * N;
+  __shared__ float2 sh[3][NT];  // rows i-1, i, i+1 of every pair of the CTA (input values)
+  __shared__ float c0n[NT];     // new colour-(RP,0) values
+  const int tid = threadIdx.x, s = blockIdx.y;
+  const int lr = tid / H, p = tid - lr * H;
+  const int i = 2 * (blockIdx.x * RPC + lr) + RP;
+  const size_t off = (size_t)s * P;
+  const float *__restrict__ in = opaque_ptr(A.icd_in + off);
+  const float *__restrict__ nbs = RP == 0 ? in : opaque_ptr(A.icd_out + off);  // rows i +- 1
+  const unsigned gm = (unsigned)(((i - 1) & (N - 1)) * N + 2 * p), g0 = (unsigned)(i * N + 2 * p),
+                 gp = (unsigned)(((i + 1) & (N - 1)) * N + 2 * p);
+  DDH_DBG(i < N && 2 * p + 1 < N && lr < RPC);
+  DDH_PDL_TRIGGER();
+  DDH_PDL_WAIT();
+  const float dflag = A.sstat[(size_t)s * kStatW + 6];
+  const float2 M = __ldg(reinterpret_cast<const float2 *>(in + g0));
+  float2 v;
+  if (!A.r_prior) {
+    const float2 Q = __ldg(reinterpret_cast<const float2 *>(A.q + off + g0));
+    v = dflag != 0.f ? M : make_float2(fmaxf(Q.x, A.r_min), fmaxf(Q.y, A.r_min));
+  } else {
+    const float2 U = __ldg(reinterpret_cast<const float2 *>(nbs + gm));
+    const float2 D = __ldg(reinterpret_cast<const float2 *>(nbs + gp));
+    const float2 Q = __ldg(reinterpret_cast<const float2 *>(A.q + off + g0));
+    const int base = lr * H, pl = base + ((p - 1) & (H - 1)), pr = base + ((p + 1) & (H - 1));
+    sh[0][tid] = U;
+    sh[1][tid] = M;
+    sh[2][tid] = D;
+    __syncthreads();
+    const float Ul = sh[0][pl].y, Ml = sh[1][pl].y, Dl = sh[2][pl].y;  // column 2p-1
+    const float Ur = sh[0][pr].x, Dr = sh[2][pr].x;                    // column 2p+2
+    // colour (RP,0) at (i, 2p): every in-row neighbour is of colour (RP,1), not yet updated
+    const float x0 = ricd_px(A, M.x, Q.x, make_float2(U.x, D.x), make_float2(Ml, M.y), make_float2(Ul, U.y),
+                             make_float2(Dl, D.y));
+    const float v0 = dflag != 0.f ? M.x : x0;
+    c0n[tid] = v0;
+    __syncthreads();
+    const float v0r = c0n[pr];  // new value at (i, 2p+2)
+    // colour (RP,1) at (i, 2p+1): in-row neighbours (i, 2p), (i, 2p+2) updated just now
+    const float x1 = ricd_px(A, M.y, Q.y, make_float2(U.y, D.y), make_float2(v0, v0r), make_float2(U.x, Ur),
+                             make_float2(D.x, Dr));
+    v = make_float2(v0, dflag != 0.f ? M.y : x1);
+  }
+  *reinterpret_cast<float2 *>(A.icd_out + off + g0) = v;
+  if (A.icd_copy) *reinterpret_cast<float2 *>(call_copy(A) + off + g0) = v;
 }
 
 // ------------------------------------------------- stage entry points
@@ -1355,7 +1462,33 @@ static bool use_passes(int sc, bool r) {
   if (on == 2) return r;  // diagnostic: passes at every size
   return r && on && !small_tiles<N>(sc) && !tiny_tiles<N>(sc);
 }
-int icd_launches(const StepArgs &a, bool r) { DDH_SDISPATCH(a.n, return use_passes<N>(a.sc, r) ? 4 : 1); return 1; }
+// The two row-parity launches (ks_ricd_rows) for every r-ICD launch at
+// N >= 512 (measured, one B200: c4 116.0 -> 119.5 k frames/s against the
+// passes, c5 15.2 -> 15.6 k against the 32-tiles), not at N <= 256: c3's three
+// concurrent lanes 120.3 -> 123.9 us per step (the barrier-free passes fill the
+// gaps between the other lanes' kernels better), c2 23.7 -> 26.7 us against
+// the 16-tiles.  DDH_RICD_ROWS (diagnostic): 0 never, 2 wherever the passes
+// would run, 3 at every size.
+template <int N>
+static bool use_rows(int sc) {
+  static const int on = getenv("DDH_RICD_ROWS") ? atoi(getenv("DDH_RICD_ROWS")) : 1;
+  if (on == 0) return false;
+  if (on == 3) return true;
+  if (on == 2) return use_passes<N>(sc, true);
+  return N >= 512;
+}
+int icd_launches(const StepArgs &a, bool r) {
+  DDH_SDISPATCH(a.n, return r && use_rows<N>(a.sc) ? 2 : use_passes<N>(a.sc, r) ? 4 : 1);
+  return 1;
+}
+template <int N>
+static cudaError_t launch_rows(const StepArgs &a, cudaStream_t st) {
+  using RC = RowsCfg<N>;
+  const dim3 grid((N / 2) / RC::RPC, a.sc);
+  cudaError_t e = launch_pdl(ks_ricd_rows<N, 0>, grid, dim3(RC::NT), 0, st, a);
+  if (e == cudaSuccess) e = launch_pdl(ks_ricd_rows<N, 1>, grid, dim3(RC::NT), 0, st, a);
+  return e;
+}
 template <int N>
 static cudaError_t launch_passes(const StepArgs &a, cudaStream_t st, void (*k0)(StepArgs), void (*k1)(StepArgs),
                                  void (*k2)(StepArgs), void (*k3)(StepArgs)) {
@@ -1369,6 +1502,7 @@ static cudaError_t launch_passes(const StepArgs &a, cudaStream_t st, void (*k0)(
 
 cudaError_t launch_s3(const StepArgs &a, cudaStream_t st) {
   DDH_SDISPATCH(a.n, ({
+                  if (use_rows<N>(a.sc)) return launch_rows<N>(a, st);
                   if (use_passes<N>(a.sc, true))
                     return launch_passes<N>(a, st, ks_ricd_pass<N, 0>, ks_ricd_pass<N, 1>, ks_ricd_pass<N, 2>,
                                                     ks_ricd_pass<N, 3>);

@@ -203,6 +203,38 @@ def test_ricd_stage_parity(n, kind, sweeps, flags):
         assert e < 1e-5 and emax < 1e-3, (b, e, emax)
 
 
+@pytest.mark.parametrize("n,B,sweeps", [(64, 300, 1), (256, 20, 1), (256, 20, 2), (512, 2, 1), (512, 2, 2),
+                                         (1024, 1, 1)])
+def test_ricd_large_launch_stage_parity(n, B, sweeps):
+    """The r-ICD kernels of large launches against the oracle's colour-ordered
+    sweep, every pixel of the first and last stream: the four colour passes
+    (N <= 256 with >= 2 64-tiles per SM) and the two row-parity kernels
+    (colours 0+1, then 2+3; N >= 512 at every launch size, 256- and
+    512-thread CTAs)."""
+    g = np.random.default_rng(11 + n)
+    r = (g.random((B, n, n)) * 2 + 1e-3).astype(np.float32)
+    q = (g.random((B, n, n)) * 2 + 1e-4).astype(np.float32)
+    p = oracle_params(n)
+    p.icd_sweeps = sweeps
+    ctx = DDH(n, B, **gpu_kwargs(p))
+    out = ctx.test_ricd(torch.from_numpy(r).to(DEV), torch.from_numpy(q).to(DEV)).cpu().numpy()
+    outs = [out]
+    if sweeps > 1:
+        c1 = DDH(n, B, **dict(gpu_kwargs(p), icd_sweeps=1))
+        cur, outs = torch.from_numpy(r).to(DEV), []
+        for _ in range(sweeps):
+            cur = c1.test_ricd(cur, torch.from_numpy(q).to(DEV))
+            outs.append(cur.cpu().numpy())
+        assert np.array_equal(outs[-1], out)
+    p1 = O.OracleParams(**{**p.__dict__, "icd_sweeps": 1})
+    for b in (0, B - 1):
+        ref = r[b].astype(np.float64)
+        for k in range(sweeps):
+            ref = O.r_icd(ref, q[b].astype(np.float64), p1, guide=outs[k][b].astype(np.float64))
+        e, emax = r_errs(out[b], ref)
+        assert e < 1e-5 and emax < 1e-3, (b, e, emax)
+
+
 def test_ricd_prior_off_is_clamp():
     n = 64
     g = np.random.default_rng(3)
