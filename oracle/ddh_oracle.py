@@ -1,8 +1,9 @@
 """FP64 CPU oracle for the Dynamic DH-MBIR (DDH-MBIR) hot path.
 
-TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
-``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference`` arm) may import
-this module.  The product path (``paper_2305_03284_b200``, ``include/ddh.h``,
+TEST INFRASTRUCTURE ONLY.  Only ``tests/`` (incl. the developer scripts in
+``tests/tools/``), ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg, its ``--impl reference`` arm and the parity sample
+printed beside the number) may import this module.  The product path (``paper_2305_03284_b200``, ``include/ddh.h``,
 ``csrc/``) never imports, links or calls it, and the two share no code: this
 file uses numpy's FFT and LAPACK (``eigvals``) as library primitives, the CUDA
 path uses its own kernels.

@@ -181,7 +181,7 @@ __host__ __device__ __forceinline__ float sqrt_approx(float x) {
 #define DDH_FDIV(a, b) ((a) * rcp_approx(b))
 
 // Monotone Newton on g: three unrolled steps (enough for ~95% of pixels on the
-// BASELINE workloads, measured with tools/check_r_update.py) then a guarded
+// BASELINE workloads, measured with tests/tools/check_r_update.py) then a guarded
 // loop for the stragglers.
 __host__ __device__ __forceinline__ float newton_root(float x, float B2, float S2, float B6, float S4, float q) {
   float dx = 0.f;
@@ -212,7 +212,7 @@ __host__ __device__ __forceinline__ float newton_root(float x, float B2, float S
 // Halley's method on g (cubic convergence; g'' = 12 B x - 4 S), from the same
 // start points as the monotone Newton runs: two unrolled steps, then a guarded
 // loop.  Checked against the oracle's exact minimiser on 6e5 random cases and
-// the c3 ICD inputs (tools/check_r_update.py: same roots, max relative error
+// the c3 ICD inputs (tests/tools/check_r_update.py: same roots, max relative error
 // 1e-6); 3.6 instead of 4.9 iterations for the slowest lane of a warp.
 __host__ __device__ __forceinline__ float halley_root(float x, float B2, float S2, float B6, float S4, float q) {
   float dx = 0.f, D = 1.f, H = 0.f;
@@ -235,7 +235,7 @@ __host__ __device__ __forceinline__ float halley_root(float x, float B2, float S
   // (g''' = 12 B) at the second step's start point, required below 2e-8 |x|,
   // and only inside the region where the bound holds (|dx g''| <= g'/10).
   // Multiplied through by 4 g'^2 (g' > 0): no division.  Saves the third,
-  // verifying step in ~3 of 4 warps on the c3 ICD inputs (tools/r_iter_study.py).
+  // verifying step in ~3 of 4 warps on the c3 ICD inputs (tests/tools/r_iter_study.py).
   {
     const float adx = fabsf(dx), c4 = fabsf(fmaf(H, H, -4.f * B2 * D));  // |g''^2 - 8 B g'|
     if (D > 0.f && adx * fabsf(H) <= 0.1f * D && c4 * (adx * adx * adx) <= 8e-8f * fabsf(x) * (D * D)) return x;

@@ -1,7 +1,7 @@
-"""Host check of the device r-update (tools/r_update_host.cu) against the oracle."""
+"""Host check of the device r-update (tests/tools/r_update_host.cu) against the oracle."""
 import subprocess, sys
 import numpy as np
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))))
 import oracle.ddh_oracle as O
 _HERE = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
 subprocess.run(["nvcc", "-x", "cu", "-O2", "-o", "/tmp/r_update_host", __import__("os").path.join(_HERE, "r_update_host.cu")],

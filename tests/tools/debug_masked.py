@@ -1,6 +1,6 @@
 import sys, os, numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import oracle.ddh_oracle as O, synth
 from test_gpu_parity import frames, gpu_kwargs, oracle_params, phi_err, r_err
 from paper_2305_03284_b200 import DDH

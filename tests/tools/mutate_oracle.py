@@ -7,7 +7,7 @@ tests is made, the mutation applied, and ``tests/test_oracle_pins.py`` run.
 A mutation that passes every pin is a SURVIVOR: some part of the oracle is
 not pinned.  Writes a JSON report (default ``profiles/r02_oracle_mutations.json``).
 
-    python tools/mutate_oracle.py [--out FILE]
+    python tests/tools/mutate_oracle.py [--out FILE]
 """
 import argparse
 import json
@@ -17,7 +17,7 @@ import subprocess
 import sys
 import tempfile
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 ORACLE = "oracle/ddh_oracle.py"
 
 # (name, description, old text, new text): old must occur exactly once; a list of
