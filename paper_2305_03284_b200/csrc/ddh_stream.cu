@@ -1381,7 +1381,11 @@ cudaError_t launch_s1(const StepArgs &a, cudaStream_t st) {
   if (persist) {
     DDH_SDISPATCH(a.n, ({
                     const int total = N / SCfg<N>::H * a.sc;
+#ifdef DDH_S1P_PER_SM
+                    constexpr int per_sm = DDH_S1P_PER_SM;
+#else
                     constexpr int per_sm = 512 / SCfg<N>::NTR;  // resident CTAs per SM (smem, registers)
+#endif
                     const int grid = total < per_sm * sms ? total : per_sm * sms;
                     return launch_pdl(ks_rows_fwd_p<N>, dim3(grid), dim3(SCfg<N>::NTR), S1P<N>::SMEM, st, a);
                   }));
@@ -1394,7 +1398,11 @@ template <int N>
 static cudaError_t launch_s2_n(const StepArgs &a, cudaStream_t st, int staged, int sms) {
   if constexpr (N <= 256) {
     const int total = N / SCfg<N>::W * a.sc;
+#ifdef DDH_S2P_PER_SM
+    constexpr int per_sm = DDH_S2P_PER_SM;
+#else
     constexpr int per_sm = 512 / SCfg<N>::NTC;  // resident CTAs per SM (smem, registers)
+#endif
     if (staged == 2 || (staged && total <= 2 * sms))  // 2: persistent staged form for every launch (diagnostic)
       return launch_pdl(ks_cols_p<N>, dim3(total < per_sm * sms ? total : per_sm * sms), dim3(SCfg<N>::NTC), S2P<N>::SMEM, st, a);
   }
