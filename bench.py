@@ -455,7 +455,7 @@ def e2e_leg(ctx, y_host, K, ws, dev, S, n):
     dt = time.perf_counter() - t0
     dt = reduce_max(dt, ws, dev)
     P = n * n
-    h2d_gbs, d2h_gbs = pcie_gbs(y_pin[0], torch.stack([phi_pin[0], r_pin[0]]), dev)  # the leg's own pinned buffers
+    h2d_gbs, d2h_gbs = pcie_gbs(y_pin[:Tc], [phi_pin, r_pin], dev)  # the leg's own pinned buffers and copies
     bin_, bout = S * P * 8, S * P * 8
     ceiling = min(h2d_gbs * 1e9 / bin_, d2h_gbs * 1e9 / bout) * S * ws
     value = Ke * S * ws / dt
@@ -464,32 +464,38 @@ def e2e_leg(ctx, y_host, K, ws, dev, S, n):
             "api": "ddh_step_host_async x calls + ddh_sync (pinned host y in; phi-hat and r-hat out; one "
                    "copy/compute pipeline across the calls), host wall clock, max over ranks",
             "pcie": {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "ceiling": ceiling, "frac": value / ceiling,
-                     "note": "copies of one step's frames in and phi-hat + r-hat out between the e2e leg's own "
-                             "pinned buffers and the device, both directions at once on two streams, measured "
-                             "right after the leg"}}
+                     "note": "the e2e leg's own copies (per step: its frames in; phi-hat and r-hat out) cycling "
+                             "over the leg's whole pinned buffers, both directions at once on two streams, "
+                             "measured right after the leg"}}
 
 
-def pcie_gbs(h_in, h_out, dev, reps=40):
-    """Concurrent pinned H2D (from h_in) and D2H (into h_out) bandwidth, GB/s:
-    one step's frames in and phi out, the same pinned buffers as the e2e leg."""
+def pcie_gbs(h_in, h_outs, dev, reps=None):
+    """Concurrent pinned H2D and D2H bandwidth, GB/s, with the e2e leg's own
+    copies: per step one H2D of that step's frames (h_in[t]) and one D2H into
+    each output buffer (h_outs[j][t]), cycling over the leg's whole pinned
+    buffers (a single step's buffer copied again and again would partly come
+    from the host's caches and overstate the ceiling)."""
     import torch
-    if not h_out.is_pinned():
-        h_out = h_out.pin_memory()
-    b_in, b_out = h_in.numel() * h_in.element_size(), h_out.numel() * h_out.element_size()
-    d_in = torch.empty_like(h_in, device=dev)
-    d_out = torch.empty_like(h_out, device=dev)
+    E = h_in.shape[0]
+    reps = reps or 3 * E
+    b_in = h_in[0].numel() * h_in.element_size()
+    b_out = sum(h[0].numel() * h.element_size() for h in h_outs)
+    d_in = torch.empty_like(h_in[0], device=dev)
+    d_outs = [torch.empty_like(h[0], device=dev) for h in h_outs]
     s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     main = torch.cuda.current_stream(dev)
+
     def burst(k):
         e = torch.cuda.Event()
         e.record(main)
         s1.wait_event(e)
         s2.wait_event(e)
-        for _ in range(k):
+        for i in range(k):
             with torch.cuda.stream(s1):
-                d_in.copy_(h_in, non_blocking=True)
+                d_in.copy_(h_in[i % E], non_blocking=True)
             with torch.cuda.stream(s2):
-                h_out.copy_(d_out, non_blocking=True)
+                for h, d in zip(h_outs, d_outs):
+                    h[i % E].copy_(d, non_blocking=True)
         main.wait_stream(s1)
         main.wait_stream(s2)
     burst(3)
