@@ -80,9 +80,12 @@ class ClockSampler(threading.Thread):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.stop_ev = threading.Event()
+        self.go_ev = threading.Event()
         self.max_mhz = None
-        self.ok = True
+        self.ok = os.environ.get("DDH_BENCH_NO_CLOCKS", "0") == "0"  # diagnostic: no sampler
         try:
+            if not self.ok:
+                raise RuntimeError("sampler disabled")
             import pynvml
             pynvml.nvmlInit()
             self.nv = pynvml
@@ -95,19 +98,29 @@ class ClockSampler(threading.Thread):
         if not self.ok:
             return
         nv = self.nv
+        # the first sample waits until the host has enqueued the timed work (go()) or
+        # 20 ms have passed: an NVML query issued while the host enqueues a short region
+        # delays its launches (K = 20 at c3: 503-508 vs 515-517 k frames/s)
+        self.go_ev.wait(0.02)
+        what = os.environ.get("DDH_BENCH_CLOCKS", "both")  # diagnostic: both | clock | reasons
         while not self.stop_ev.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                try:
-                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                except AttributeError:
-                    mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
+                if what != "reasons":
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                if what != "clock":
+                    try:
+                        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    except AttributeError:
+                        mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                    for bit, name in self.REASONS.items():
+                        if mask & bit and name != "gpu_idle":
+                            self.reasons.add(name)
             except Exception:
                 pass
             time.sleep(self.period)
+
+    def go(self):
+        self.go_ev.set()
 
     def stop(self):
         self.stop_ev.set()
@@ -264,6 +277,7 @@ def run_ours(args):
     e0.record(stream)
     unit.steps(K)
     e1.record(stream)
+    clk.go()  # samples while the GPU still runs the enqueued steps
     torch.cuda.synchronize()
     clocks = clk.stop()
     barrier(ws)

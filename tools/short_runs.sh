@@ -1,10 +1,8 @@
 #!/bin/bash
-# c3 value at the driver's --steps 20 vs 300, with and without call graphs (run under gpurun)
-for rep in 1 2; do
-for K in 20 300; do
-  for G in "" "--call-graphs"; do
-    timeout 600 python bench.py --steps $K --warmup 5 --no-e2e --no-latency --no-cpu-baseline --no-parity $G > gpurun_out/sr.log 2>/dev/null
-    python -c "import json; d=json.loads(open('gpurun_out/sr.log').read().strip().splitlines()[-1]); print('K=$K $G', round(d['value']), round(d['ms_per_step']*1000,1))"
+# c3 value at the driver's --steps 20 (run under gpurun): clock-sampler variants
+for rep in 1 2 3; do
+  for V in "DDH_BENCH_CLOCKS=both" "DDH_BENCH_CLOCKS=clock" "DDH_BENCH_CLOCKS=reasons" "DDH_BENCH_NO_CLOCKS=1"; do
+    env $V timeout 600 python bench.py --steps 20 --warmup 5 --no-e2e --no-latency --no-cpu-baseline --no-parity "$@" > gpurun_out/sr.log 2>/dev/null
+    python -c "import json; d=json.loads(open('gpurun_out/sr.log').read().strip().splitlines()[-1]); print('$V', round(d['value']), round(d['ms_per_step']*1000,1), d['clocks']['samples'])"
   done
-done
 done
