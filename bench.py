@@ -348,11 +348,20 @@ def run_ours(args):
     step_bytes = STEP_BYTES_PER_PX * P * S
     step_gbs = step_bytes / (ms_max / K * 1e-3) / 1e9
     step_traffic = sum(summ.get("dram_bytes_per_launch", {}).values()) or None
+    # what reaches HBM with warm caches in the lane pipeline (tools/ncu_warm.sh, latest profiles/*_warm_traffic.json)
+    warm = {}
+    wfiles = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_warm_traffic.json"))
+    if wfiles:
+        wd = json.load(open(os.path.join(ROOT, "profiles", wfiles[-1])))
+        warm = {"per_step_bytes": wd.get("per_step_bytes"),
+                "source": f"{wfiles[-1]}: ncu --cache-control none, the library's lanes, kernels serialised by ncu"}
     roofline = {"bound": "hbm", "kernel": "step: the six kernels of one time step (S0..S5), 64 streams",
                 "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
                 "traffic": step_traffic, "algorithmic_bytes_per_step": step_bytes, "peak_source": peak_src,
                 "traffic_source": f"sum of dram__bytes_read+write over the six kernels, ncu --set full "
                                   f"{summ.get('round', '?')} (cold-cache, serialised)",
+                "traffic_warm": warm.get("per_step_bytes"),
+                "traffic_warm_source": warm.get("source"),
                 "dominant_kernel": {"name": dom, "hbm": dict(hbm, traffic=traffic), "issue_slot": issue,
                                     "timed_in": "attribution pass (DDH_F_SERIAL: serialised kernels, per-launch "
                                                 "CUDA events)"}}
