@@ -158,7 +158,11 @@ ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *statu
  * of whole rows).  phi_out, r_out: device float32 [T][S][N][N], 8-byte
  * aligned, or NULL (the state always advances).  status: device uint8 [T][S]
  * or NULL.  Errors: DDH_E_INVAL (T < 0, NULL y with T > 0, misaligned
- * pointers), DDH_E_CUDA. */
+ * pointers), DDH_E_CUDA.
+ * At N = 64 the frame's N_k iterations may run as one on-chip chain kernel
+ * (one CTA per stream, the frame in shared memory) where that measured faster
+ * (N_k >= 4, or N_k >= 2 with one full wave of resident CTAs); the results
+ * agree with the six-kernel path at the parity tolerance. */
 ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float *r_out,
                     uint8_t *status);
 
@@ -230,7 +234,9 @@ int64_t ddh_frame_index(const ddh_ctx *c);
 /* ---- instrumentation: per-kernel device time (CUDA events on the ctx stream) ----
  * Kernel kinds: 0 K0 stats, 1 K1 rows_fwd, 2 K2a cols, 3 K2b r-ICD,
  * 4 K3a rows_inv, 5 K3b phi-ICD, 6 fill, 7 Strehl (multi-pass path);
- * 8-10 unused (the retired cluster path); 11 S0 ks_stats, 12 S1 ks_rows_fwd,
+ * 8 ks_chain (the on-chip multi-iteration chain at N = 64: one launch per
+ * launch group and frame, all N_k iterations); 9-10 unused (the retired
+ * cluster path); 11 S0 ks_stats, 12 S1 ks_rows_fwd,
  * 13 S2 ks_cols, 14 S3 ks_ricd (for large launches the four colour passes
  * ks_ricd_pass, timed as one), 15 S4 ks_rows_inv, 16 S5 ks_phiicd
  * (streaming path, default).

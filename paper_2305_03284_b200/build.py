@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "lib", "libddh.so")
 # wrong-colour shared-memory indices and out-of-range global indices), the
 # sanitizer substitute run by tests/test_gpu_debug.py
 LIB_DEBUG = os.path.join(HERE, "lib", "libddh_debug.so")
-SOURCES = ["ddh_kernels.cu", "ddh_stream.cu", "ddh_synth.cu", "ddh_api.cpp"]
+SOURCES = ["ddh_kernels.cu", "ddh_stream.cu", "ddh_chain.cu", "ddh_synth.cu", "ddh_api.cpp"]
 HEADERS = ["ddh_kernels.h", "ddh_fft.cuh", "ddh_common.cuh", "ddh_f32x2.cuh", "ddh_fft_reg.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

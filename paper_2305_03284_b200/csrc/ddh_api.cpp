@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+using ddh::ChainArgs;
 using ddh::IcdArgs;
 using ddh::StepArgs;
 using ddh::StrehlArgs;
@@ -86,6 +87,12 @@ struct ddh_ctx {
   // streaming path: the r M-step (S3) of a lane runs on a side stream,
   // concurrently with the phi branch (S4, S5) it does not depend on (R12)
   bool split_r = false;
+  // on-chip multi-iteration chain (ddh_chain.cu): Step frames of the streaming path at
+  // N = 64 run as one CTA per stream holding the frame in shared memory when that
+  // is faster than the six kernels (profiles/r02e_chain64.json, use_chain()).
+  // DDH_CHAIN: 0 never, 1 always (tests, measurements)
+  bool chain = false;
+  bool chain_force = false;
   bool l2_window = false;  // holds the device's persisting-L2 carve-out
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
@@ -186,11 +193,11 @@ ddh_status fail(ddh_ctx *c, ddh_status s, const std::string &msg) {
       return fail((c), DDH_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
-enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_KA, K_KB, K_KC,
+enum Kind { K_STATS = 0, K_ROWS_FWD, K_COLS, K_RICD, K_ROWS_INV, K_PHIICD, K_FILL, K_STREHL, K_CHAIN, K_KB, K_KC,
             K_S0, K_S1, K_S2, K_S3, K_S4, K_S5 };
 const char *kKindNames[DDH_KIND_COUNT] = {"k0_stats", "k1_rows_fwd", "k2a_cols", "k2b_ricd",
                                           "k3a_rows_inv", "k3b_phiicd", "k_fill", "ks_strehl",
-                                          "unused8", "unused9", "unused10",
+                                          "ks_chain", "unused9", "unused10",
                                           "ks_stats", "ks_rows_fwd", "ks_cols", "ks_ricd", "ks_rows_inv", "ks_phiicd"};
 
 // Event pair for a launch of `kind` when profiling (nullptr otherwise).
@@ -349,6 +356,24 @@ ddh_status run_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const fl
 
 enum class Mode { Step, Boot };
 
+// The chain for a Step frame of N_k iterations (measured at 64^2, one B200,
+// profiles/r02e_chain64.json): every N_k >= 4 (174 vs 194, 274 vs 384, 909 vs
+// 946 us at 64 / 296 / 1024 streams for N_k = 8); N_k = 2 (and 3) only when the
+// launch group is one full wave of resident CTAs (296 streams: 78 vs 95 us; 64
+// streams, 0.2 waves: 51.4 vs 50.2; 592 streams, 2 waves: 151 vs 150; 1024
+// streams, 3.46 waves: 255 vs 245); N_k = 1 never (the kernels' per-frame cost is
+// lower: 28 vs 31 and 126 vs 148 us).
+bool use_chain(const ddh_ctx *c, int iters) {
+  if (!c->chain) return false;
+  if (c->chain_force) return true;
+  if (iters >= 4) return true;
+  if (iters < 2) return false;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const double slots = (double)ddh::chain_ctas_per_sm() * sms;
+  return c->sc >= 0.95 * slots && c->sc <= slots;
+}
+
 // One frame batch (all streams) through the loop body.  y: device frames
 // [S][N][N] of this time step.  Outputs (may be null) are [S][N][N] / [S].
 // Mode::Step: DDH step (Fig. 1).  Mode::Boot: cold start + `iters` iterations
@@ -362,6 +387,35 @@ ddh_status run_frame(ddh_ctx *c, const float2 *y, float *phi_out, float *r_out, 
   const size_t P = c->P;
   const int cur0 = c->cur;
   const bool plane = (mode == Mode::Step) && !(c->p.flags & DDH_F_NO_TIPTILT);
+  if (mode == Mode::Step && use_chain(c, iters)) {  // the on-chip chain: all N_k iterations
+    for (int l = 0; l < 8; ++l) {  // streaming work still pending from a bootstrap
+      if (c->side_pending[l]) DDH_CK(c, cudaStreamWaitEvent(c->st, c->side_join[l], 0));
+      if (c->ypf_pending[l]) DDH_CK(c, cudaStreamWaitEvent(c->st, c->ypf_join[l], 0));
+      c->side_pending[l] = c->ypf_pending[l] = false;
+    }
+    for (int s0 = 0; s0 < c->S; s0 += c->sc) {
+      const int sc = std::min(c->sc, c->S - s0);
+      const size_t so = (size_t)s0 * P;
+      ChainArgs ca{};
+      ca.a = base_args(c, s0, sc);
+      ca.a.y = y + so;
+      ca.a.phi_in = c->phi[cur0] + so;
+      ca.a.apply_plane = plane ? 1 : 0;
+      ca.a.warm = 1;
+      ca.a.oml = (float)(1.0 - c->p.lambda);
+      ca.a.la = (float)(c->p.lambda * c->p.alpha);
+      ca.a.status = status ? status + s0 : nullptr;
+      ca.phi_next = c->phi[cur0 ^ 1] + so;
+      ca.phi_copy = phi_out ? phi_out + so : nullptr;
+      ca.r_copy = r_out ? r_out + so : nullptr;
+      ca.iters = iters;
+      DDH_LAUNCH(c, K_CHAIN, ddh::launch_chain(ca, c->st));
+    }
+    c->cur = cur0 ^ 1;
+    c->y_prefetched = nullptr;
+    c->psum_valid = false;  // the streaming path's fixed-point plane sums are not kept
+    return DDH_OK;
+  }
   for (int s0 = 0; s0 < c->S; s0 += c->sc) {
     const int sc = std::min(c->sc, c->S - s0);
     const size_t so = (size_t)s0 * P;
@@ -989,6 +1043,9 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     }
     const char *sr = std::getenv("DDH_SPLIT_R");  // diagnostic override
     c->split_r = c->streaming && !(p.flags & DDH_F_SERIAL) && (sr ? std::atoi(sr) != 0 : true);
+    const char *ch = std::getenv("DDH_CHAIN");
+    c->chain = c->streaming && ddh::chain_fits(n) && (ch ? std::atoi(ch) != 0 : true);
+    c->chain_force = c->chain && ch && std::atoi(ch) == 1;
 
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
@@ -1129,7 +1186,8 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
   int t = 0;
   // whole chunks from call graphs (one launch group, no profiling; frames still in
   // flight from the host pipeline are ordered by the ctx stream)
-  if (c->call_graphs && c->streaming && !c->profiling && c->sc == c->S && !c->y_prefetched) {
+  if (c->call_graphs && c->streaming && !use_chain(c, c->p.n_k) && !c->profiling && c->sc == c->S &&
+      !c->y_prefetched) {
     for (; t + c->chunk <= T; t += c->chunk) {
       s = run_chunk(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
                     r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr, c->chunk);

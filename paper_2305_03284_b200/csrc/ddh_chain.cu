@@ -1,0 +1,276 @@
+// ddh_chain.cu -- the on-chip multi-iteration chain for
+// N = 64: one CTA per stream holds the whole frame (y, the complex work
+// array, r, q / c, theta, phi: 97 KB of shared memory, two CTAs per SM; y is re-read from L2) and runs Fig. 1's
+// loop body for the frame -- Normalize (Eq. 4), RemoveTipTilt,
+// then N_k x [FFT1 = back-projection (Eq. 3 on the first), E-step, qGGMRF
+// r-ICD, FFT2 + phase correlation, GMRF phi-ICD] -- reading y, r and phi from
+// HBM once and writing r and phi once, whatever N_k is.  Each extra EM
+// iteration costs shared-memory passes only (the streaming path's six
+// kernels move ~112 B/px through HBM / L2 per iteration).
+//
+// The arithmetic is the multi-pass path's (ddh_kernels.cu K0-K3b: the same
+// expressions, the same Stockham FFT, qgg_w / r_update / phi_update of
+// ddh_common.cuh), reductions in FP64 in a fixed order; parity with the oracle
+// in tests/test_gpu_parity.py (test_chain_*).
+#include "ddh_common.cuh"
+#include "ddh_fft.cuh"
+#include "ddh_kernels.h"
+
+namespace ddh {
+namespace {
+
+constexpr int kCN = 64, kCP = kCN * kCN, kCPitch = kCN + 1, kCThreads = 512;
+
+#ifndef DDH_CHAIN_MINB
+#define DDH_CHAIN_MINB 2
+#endif
+// y stays in global memory (L2-resident after the first read; 32 KB more shared
+// memory per CTA would leave one CTA per SM instead of two)
+struct ChainSmem {
+  float2 X[kCN * kCPitch];  // complex work array (row pitch N + 1)
+  float rs[kCP];            // r (in place through Eq. 3 and the r-ICD)
+  float qs[kCP];            // q (E-step), then c (phase correlation)
+  float ts[kCP];            // theta
+  float ps[kCP];            // phi (plane removed)
+  float2 tw[kCN];
+  int2 span[kCN];
+  double red[32 * 5];
+  double scal[8];
+};
+
+// qGGMRF coefficients B, S of pixel (i, j) (periodic 8-neighbourhood, R6-R8):
+// the K2b expressions
+__device__ __forceinline__ void chain_rBS(const float *rs, int i, int j, float b0, float inv_Tsig, float tmq,
+                                          float &B, float &S) {
+  const float ri = rs[i * kCN + j];
+  B = 0.f;
+  S = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int ni = (i + nb_di(k)) & (kCN - 1), nj = (j + nb_dj(k)) & (kCN - 1);
+    const float rj = rs[ni * kCN + nj];
+    const float bt = nb_w(k) * b0 * qgg_w(ri - rj, inv_Tsig, tmq);
+    B += bt;
+    S = fmaf(bt, rj, S);
+  }
+}
+
+__global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs C) {
+  const StepArgs &A = C.a;
+  extern __shared__ __align__(16) unsigned char chain_sm[];
+  ChainSmem &M = *reinterpret_cast<ChainSmem *>(chain_sm);
+  const int tid = threadIdx.x, s = blockIdx.x;
+  const size_t off = (size_t)s * kCP;
+  if (tid < kCN) {
+    M.tw[tid] = A.tw[tid];
+    M.span[tid] = A.rowspan[tid];
+  }
+  __syncthreads();
+  auto ap = [&](int i, int j) { return j >= M.span[i].x && j < M.span[i].y; };
+  // ---- load the frame and the state; sums for Normalize (Eq. 4) and RemoveTipTilt
+  double v[5] = {0, 0, 0, 0, 0};
+  for (int idx = tid; idx < kCP; idx += kCThreads) {
+    const int i = idx / kCN, j = idx & (kCN - 1);
+    const float2 y = A.y[off + idx];
+    v[0] += (double)y.x;
+    v[1] += (double)y.y;
+    const float ph = A.phi_in[off + idx];
+    M.ps[idx] = ph;
+    M.rs[idx] = A.r_state[off + idx];
+    if (A.apply_plane && ap(i, j)) {
+      v[2] += (double)ph;
+      v[3] += (double)ph * (double)(j - kCN / 2);
+      v[4] += (double)ph * (double)(i - kCN / 2);
+    }
+  }
+  block_sum<5>(v, M.red);
+  if (tid == 0) {
+    M.scal[0] = v[0] / kCP;
+    M.scal[1] = v[1] / kCP;
+    double c[3] = {0, 0, 0};
+    if (A.apply_plane) plane_from_sums(v, A.minv, c);
+    M.scal[2] = c[0];
+    M.scal[3] = c[1];
+    M.scal[4] = c[2];
+  }
+  __syncthreads();
+  const float mur = (float)M.scal[0], mui = (float)M.scal[1];
+  const float c0 = (float)M.scal[2], c1 = (float)M.scal[3], c2 = (float)M.scal[4];
+  double a1[1] = {0.0};
+  for (int idx = tid; idx < kCP; idx += kCThreads) {
+    const float2 y = A.y[off + idx];
+    const float dr = y.x - mur, di = y.y - mui;
+    a1[0] += (double)dr * dr + (double)di * di;
+  }
+  block_sum<1>(a1, M.red);
+  if (tid == 0) M.scal[5] = a1[0];
+  __syncthreads();
+  const double d2 = M.scal[5];
+  const bool degenerate = !(d2 > 0.0);
+  if (A.status && tid == 0) A.status[s] = degenerate ? 1 : 0;
+  if (degenerate) {  // state unchanged (no tip/tilt removal either)
+    for (int idx = tid; idx < kCP; idx += kCThreads) {
+      const float p = M.ps[idx], r = M.rs[idx];
+      C.phi_next[off + idx] = p;
+      if (C.phi_copy) C.phi_copy[off + idx] = p;
+      if (C.r_copy) C.r_copy[off + idx] = r;
+    }
+    return;
+  }
+  const float kappa = (float)sqrt((double)kCP / d2);  // Eq. 4: sqrt(p) / ||y - mu||
+  const float scale = kappa / (float)kCN;             // unitary F_c = chi F chi / N
+  if (A.apply_plane) {
+    for (int idx = tid; idx < kCP; idx += kCThreads) {
+      const int i = idx / kCN, j = idx & (kCN - 1);
+      M.ps[idx] -= (c0 + c1 * (float)(j - kCN / 2) + c2 * (float)(i - kCN / 2));
+    }
+  }
+  const int fb = tid % kCN, ft = tid / kCN;  // FFT: vector fb, lane ft (8 threads per 64-point vector)
+  const float inv_n = 1.f / (float)kCN, two_s2 = 2.f / A.s2;
+  for (int it = 0; it < C.iters; ++it) {
+    __syncthreads();
+    // ---- FFT1: z = chi a e^{-j phi'} (y - mu), forward rows then columns (K1, K2a)
+    for (int idx = tid; idx < kCP; idx += kCThreads) {
+      const int i = idx / kCN, j = idx & (kCN - 1);
+      float2 z = make_float2(0.f, 0.f);
+      if (ap(i, j)) {
+        const float2 y = __ldg(A.y + off + idx);
+        const float dr = y.x - mur, di = y.y - mui;
+        float sn, cs;
+        sincosf(M.ps[idx], &sn, &cs);
+        z = make_float2(dr * cs + di * sn, di * cs - dr * sn);
+        if ((i + j) & 1) z = make_float2(-z.x, -z.y);
+      }
+      M.X[i * kCPitch + j] = z;
+    }
+    __syncthreads();
+    block_fft<kCN, -1>(M.X + fb * kCPitch, true, ft, 1, M.tw);
+    block_fft<kCN, -1>(M.X + fb, true, ft, kCPitch, M.tw);
+    // ---- u = A^H y-hat; Eq. 3 warm start on the first iteration; E-step (R1)
+    const bool warm = A.warm && it == 0;
+    for (int idx = tid; idx < kCP; idx += kCThreads) {
+      const int ki = idx / kCN, kj = idx & (kCN - 1);
+      const float sg = ((ki + kj) & 1) ? -scale : scale;
+      const float2 X = M.X[ki * kCPitch + kj];
+      const float2 u = make_float2(X.x * sg, X.y * sg);
+      const float rp = M.rs[idx];
+      float r0 = rp;
+      if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);  // Eq. 3
+      const float w = r0 / (r0 + A.s2);
+      const float2 mu = make_float2(w * u.x, w * u.y);
+      M.rs[idx] = r0;
+      M.qs[idx] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
+      const float cs = ((ki + kj) & 1) ? -1.f : 1.f;
+      M.X[ki * kCPitch + kj] = make_float2(cs * mu.x, cs * mu.y);
+    }
+    __syncthreads();
+    // ---- r M-step: colour-ordered qGGMRF ICD in place (R6-R9), periodic
+    if (A.r_prior) {
+      for (int sw = 0; sw < A.sweeps; ++sw) {
+        for (int c = 0; c < 4; ++c) {
+          const int ci = c >> 1, cj = c & 1;
+          for (int p = tid; p < kCP / 4; p += kCThreads) {
+            const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
+            float B, S;
+            chain_rBS(M.rs, i, j, A.r_b0, A.r_inv_Tsig, A.r_tmq, B, S);
+            M.rs[i * kCN + j] = r_update(M.rs[i * kCN + j], M.qs[i * kCN + j], B, S, A.r_min);
+          }
+          __syncthreads();
+        }
+      }
+    } else {
+      for (int idx = tid; idx < kCP; idx += kCThreads) M.rs[idx] = fmaxf(M.qs[idx], A.r_min);
+    }
+    // ---- FFT2: f = F_c^{-1} mu (inverse columns then rows: K2a, K3a)
+    block_fft<kCN, +1>(M.X + fb, true, ft, kCPitch, M.tw);
+    block_fft<kCN, +1>(M.X + fb * kCPitch, true, ft, 1, M.tw);
+    // ---- phase correlation: c = (2/s2) a |y-hat| |f|, theta = arg(y-hat conj f)
+    for (int idx = tid; idx < kCP; idx += kCThreads) {
+      const int i = idx / kCN, j = idx & (kCN - 1);
+      float c = 0.f, th = 0.f;
+      if (ap(i, j)) {
+        const float sg = ((i + j) & 1) ? -inv_n : inv_n;
+        const float2 X = M.X[i * kCPitch + j];
+        const float2 f = make_float2(X.x * sg, X.y * sg);
+        const float2 y = __ldg(A.y + off + idx);
+        const float2 yh = make_float2(kappa * (y.x - mur), kappa * (y.y - mui));
+        const float2 z = make_float2(yh.x * f.x + yh.y * f.y, yh.y * f.x - yh.x * f.y);
+        c = two_s2 * hypotf(z.x, z.y);
+        th = atan2f(z.y, z.x);
+      }
+      M.qs[idx] = c;
+      M.ts[idx] = th;
+    }
+    __syncthreads();
+    // ---- phi M-step: colour-ordered GMRF ICD in place (R10-R11), free boundary
+    for (int sw = 0; sw < A.sweeps; ++sw) {
+      for (int c = 0; c < 4; ++c) {
+        const int ci = c >> 1, cj = c & 1;
+        for (int p = tid; p < kCP / 4; p += kCThreads) {
+          const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
+          float nb = 0.f, sb = 0.f;
+          if (A.phi_prior) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int ni = i + nb_di(k), nj = j + nb_dj(k);
+              if (ni >= 0 && ni < kCN && nj >= 0 && nj < kCN) {
+                nb = fmaf(nb_w(k), M.ps[ni * kCN + nj], nb);
+                sb += nb_w(k);
+              }
+            }
+          }
+          const int g = i * kCN + j;
+          M.ps[g] = phi_update(M.ps[g], M.qs[g], M.ts[g], nb, sb, A.phi_w, A.phi_prior != 0);
+        }
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  // ---- WriteData: the new state (and the caller's copies)
+  for (int idx = tid; idx < kCP; idx += kCThreads) {
+    const float p = M.ps[idx], r = M.rs[idx];
+    C.phi_next[off + idx] = p;
+    A.r_state[off + idx] = r;
+    if (C.phi_copy) C.phi_copy[off + idx] = p;
+    if (C.r_copy) C.r_copy[off + idx] = r;
+  }
+}
+
+}  // namespace
+
+bool chain_fits(int n) { return n == kCN; }
+
+// resident chain CTAs per SM on the current device (occupancy calculator; cached)
+int chain_ctas_per_sm() {
+  static int cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 1;
+  if (!cache[dev]) {
+    int nb = 0;
+    if (cudaFuncSetAttribute(ks_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ChainSmem)) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ks_chain, kCThreads, sizeof(ChainSmem)) != cudaSuccess)
+      nb = 1;
+    cache[dev] = nb > 0 ? nb : 1;
+  }
+  return cache[dev];
+}
+
+cudaError_t launch_chain(const ChainArgs &c, cudaStream_t st) {
+  if (c.a.n != kCN) return cudaErrorInvalidValue;
+  static bool init[64] = {};  // the shared-memory opt-in is per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!init[dev]) {
+    e = cudaFuncSetAttribute(ks_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ChainSmem));
+    if (e != cudaSuccess) return e;
+    init[dev] = true;
+  }
+  ks_chain<<<c.a.sc, kCThreads, sizeof(ChainSmem), st>>>(c);
+  return cudaGetLastError();
+}
+
+}  // namespace ddh

@@ -75,6 +75,16 @@ struct StepArgs {
   int dbg_fault;          // debug build only (DDH_DEBUG_FAULT): a deliberately failing check, to show the checks run
 };
 
+// On-chip multi-iteration chain (ddh_chain.cu, N = 64): one CTA per stream runs
+// the whole frame, N_k iterations, in shared memory.
+struct ChainArgs {
+  StepArgs a;        // y, r_state (updated in place), phi_in, status, priors, plane, Eq. 3 weights
+  float *phi_next;   // new phase state [sc][N][N]
+  float *phi_copy;   // caller's phi_out or null
+  float *r_copy;     // caller's r_out or null
+  int iters;         // N_k
+};
+
 struct IcdArgs {
   int n;
   const float *in;       // r_in or phi_in [sc][N][N]
@@ -140,6 +150,10 @@ cudaError_t launch_set_desc(CallDesc *d, const CallDesc &v, cudaStream_t st);
 bool s4_sums_next(int n);
 cudaError_t launch_s5(const StepArgs &a, cudaStream_t st);
 int icd_launches(const StepArgs &a, bool r_icd);  // kernels one launch_s3 / launch_s5 enqueues (4: colour passes)
+
+bool chain_fits(int n);  // the on-chip chain holds an N x N frame in one CTA
+int chain_ctas_per_sm();  // its resident CTAs per SM
+cudaError_t launch_chain(const ChainArgs &c, cudaStream_t st);
 
 // stage entry points of the streaming kernels (ddh_test_*)
 cudaError_t launch_test_fft_stream(int n, const float2 *in, float2 *out, int B, int inverse, const float4 *tw4,

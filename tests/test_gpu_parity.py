@@ -17,6 +17,7 @@ Tolerances (north_star, DESIGN.md "Parity"):
     (FP32 floor ~ eps log2 N), E-step <= 1e-6, ICDs <= 1e-5.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -54,7 +55,25 @@ def oracle_params(n, diam=None, **kw):
     return p
 
 
-PATH_FLAGS = {"stream": 0, "multipass": 2, False: 0, True: 2}
+PATH_FLAGS = {"stream": 0, "multipass": 2, "nochain": 0, False: 0, True: 2}
+
+
+class chain_env:
+    """Context manager: DDH contexts created inside use (on=True) or do not use
+    (on=False) the on-chip chain at N = 64 (DDH_CHAIN, read by ddh_create)."""
+
+    def __init__(self, on):
+        self.on = on
+
+    def __enter__(self):
+        self.old = os.environ.get("DDH_CHAIN")
+        os.environ["DDH_CHAIN"] = "1" if self.on else "0"
+
+    def __exit__(self, *a):
+        if self.old is None:
+            os.environ.pop("DDH_CHAIN", None)
+        else:
+            os.environ["DDH_CHAIN"] = self.old
 
 
 def gpu_kwargs(p: O.OracleParams, unfused=False):
@@ -79,24 +98,47 @@ def r_errs(r_g, r_o):
             float(np.max(np.abs(r_g - r_o) / np.abs(r_o))))
 
 
-def check_step(r_g, phi_g, r_in, phi_in, y, p, a, tol_phi=1e-3, tol_r=1e-4, tol_rmax=1e-3):
+def oracle_step_guided(r, phi, y, p, a, guides):
+    """O.ddh_step (Fig. 1) with the r M-step of EM iteration k guided by
+    guides[k] (the GPU's r after iteration k): the oracle's own functions in
+    O.ddh_step's order, so that at a near-tie of an earlier iteration the oracle
+    follows the GPU's valid choice too."""
+    yhat = O.normalize(y)
+    if p.tiptilt:
+        phi = O.remove_tip_tilt(phi, a)
+    u = O.adjoint(phi, yhat, a)
+    r = O.warm_start(r, u, p.lam, p.alpha, p.r_min)
+    for k in range(p.n_k):
+        if k > 0:
+            u = O.adjoint(phi, yhat, a)
+        r, phi = O.em_update(r, phi, yhat, u, a, p, None, guides[k])
+    return r, phi
+
+
+def check_step(r_g, phi_g, r_in, phi_in, y, p, a, tol_phi=1e-3, tol_r=1e-4, tol_rmax=1e-3, guides=None):
     """One oracle step from (r_in, phi_in) on frame y against the GPU's
     (r_g, phi_g); near-tie pixels follow the GPU's valid choice (guided
-    oracle).  Returns a dict of the errors and the tie / guided counts."""
+    oracle; with N_k > 1, `guides` = the GPU's r after each iteration, from
+    runs with N_k = 1, 2, ... from the same state).  Returns a dict of the
+    errors and the tie / guided counts."""
     n = r_in.shape[0]
     gaps = np.full((n, n), np.inf)
     r_def, _, _ = O.ddh_step(r_in, phi_in, y, p, a, gaps)
-    r_ref, phi_ref, st = O.ddh_step(r_in, phi_in, y, p, a, guide=r_g.astype(np.float64))
+    if guides is not None and p.n_k > 1:
+        r_ref, phi_ref = oracle_step_guided(r_in, phi_in, y, p, a, [g.astype(np.float64) for g in guides])
+    else:
+        r_ref, phi_ref, st = O.ddh_step(r_in, phi_in, y, p, a, guide=r_g.astype(np.float64))
     ep = phi_err(phi_g, phi_ref, a)
     er, emax = r_errs(r_g, r_ref)
     res = {"phi": ep, "r_l2": er, "r_max": emax, "ties": int((gaps < 1e-6).sum()),
            "guided": int(np.sum(np.abs(r_ref - r_def) > 1e-6 * np.abs(r_def)))}
-    if p.n_k > 1 or p.icd_sweeps > 1:
-        # the GPU's choices at near-ties of earlier sweeps / iterations are not
-        # observable (only the final r is), so the guide is exact for the last
-        # sweep only; a different valid choice in an earlier sweep moves the
-        # pixels that later colour phases reach from it.  The pointwise bound
-        # then holds for 99.9 % of the pixels; the L2 bound covers every pixel.
+    if (p.n_k > 1 and guides is None) or p.icd_sweeps > 1:
+        # the GPU's choices at near-ties of earlier sweeps (or, without per-
+        # iteration guides, iterations) are not observable (only the final r
+        # is), so the guide is exact for the last sweep only; a different valid
+        # choice in an earlier sweep moves the pixels that later colour phases
+        # reach from it.  The pointwise bound then holds for 99.9 % of the
+        # pixels; the L2 bound covers every pixel.
         rel = np.abs(r_g.astype(np.float64) - r_ref) / np.abs(r_ref)
         res.update(r_max_all=emax, r_p999=float(np.quantile(rel, 0.999)))
         emax = res["r_max"] = res["r_p999"]
@@ -276,7 +318,10 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, unfused=
     r32 = orc.r.astype(np.float32)
     p32 = orc.phi.astype(np.float32)
     orc.set_state(r32, p32, 1)
-    ctx = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(p, unfused))
+    if unfused == "nochain" and n != 64:
+        pytest.skip("the on-chip chain exists at N = 64 only")
+    with chain_env(unfused != "nochain"):
+        ctx = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(p, unfused))
     ctx.set_state(torch.from_numpy(r32).to(DEV), torch.from_numpy(p32).to(DEV), 1)
     yt = torch.from_numpy(y[1:2]).to(DEV)
     phi_o = torch.empty((1, S, n, n), device=DEV)
@@ -291,15 +336,30 @@ def _step_parity(n, S, p, cfg="c1", chunk=0, pre_boot=8, seed_frames=3, unfused=
     r_s, phi_s, fi = ctx.get_state()
     assert fi == 2
     assert np.array_equal(r_s.cpu().numpy(), r_g) and np.array_equal(phi_s.cpu().numpy(), phi_g)
+    guides = None
+    if p.n_k > 1:  # the GPU's r after EM iterations 1 .. N_k - 1: the same step with fewer iterations
+        guides = []
+        for k in range(1, p.n_k):
+            pk = O.OracleParams(**{**p.__dict__, "n_k": k})
+            with chain_env(unfused != "nochain"):
+                ck = DDH(n, S, chunk_streams=chunk, **gpu_kwargs(pk, unfused))
+            ck.set_state(torch.from_numpy(r32).to(DEV), torch.from_numpy(p32).to(DEV), 1)
+            rk = torch.empty_like(r_o)
+            ck.step(yt, None, rk)
+            guides.append(rk.cpu().numpy()[0])
+        guides.append(r_g)
     worst = (0.0, 0.0)
     for s in range(S):
-        res = check_step(r_g[s], phi_g[s], orc.r[s], orc.phi[s], y[1, s], p, a)
+        res = check_step(r_g[s], phi_g[s], orc.r[s], orc.phi[s], y[1, s], p, a,
+                         guides=None if guides is None else [g[s] for g in guides])
         worst = (max(worst[0], res["phi"]), max(worst[1], res["r_l2"]))
     return worst
 
 
-# the two implementations of the EM iteration: streaming (default), multi-pass
-PATHS = [pytest.param("stream", id="stream"), pytest.param("multipass", id="multipass")]
+# the implementations of the EM iteration: streaming (default; at N = 64 the
+# on-chip chain), multi-pass, and at N = 64 the streaming kernels without the chain
+PATHS = [pytest.param("stream", id="stream"), pytest.param("multipass", id="multipass"),
+         pytest.param("nochain", id="nochain")]
 
 
 @pytest.mark.parametrize("unfused", PATHS)
@@ -328,6 +388,40 @@ def test_step_parity_masked_aperture(unfused):
     n = 64
     p = oracle_params(n, diam=50, noise_var=0.15)
     _step_parity(n, 2, p, unfused=unfused)
+
+
+@pytest.mark.parametrize("n_k,tiptilt,priors,sweeps", [(1, True, True, 1), (2, True, True, 1), (4, True, True, 1),
+                                                         (8, True, True, 1), (2, False, True, 2), (2, True, False, 1)])
+def test_chain_step_parity(n_k, tiptilt, priors, sweeps):
+    """The on-chip chain (one CTA per stream, all N_k EM
+    iterations in shared memory) against the oracle's step, every pixel."""
+    n = 64
+    p = oracle_params(n, noise_var=synth.recon_noise_var(n, n, 10.0), n_k=n_k, tiptilt=tiptilt, icd_sweeps=sweeps,
+                      **({} if priors else dict(r_sigma=0.0, phi_sigma=0.0)))
+    _step_parity(n, 3, p)
+
+
+def test_chain_and_streaming_kernels_agree():
+    """At N = 64 the chain and the streaming kernels compute the same steps
+    (FP32 rounding order differs: parity tolerance, 4 frames, N_k = 2)."""
+    n, S, T = 64, 3, 4
+    y, _, _ = frames(n, S, T)
+    yt = torch.from_numpy(y).to(DEV)
+    outs = []
+    for on in (True, False):
+        with chain_env(on):
+            ctx = DDH(n, S, noise_var=0.2, n_k=2)
+        l0 = ctx.kernel_launches
+        po = torch.empty((T, S, n, n), device=DEV)
+        ro = torch.empty_like(po)
+        ctx.step(yt, po, ro)
+        outs.append((po.cpu().numpy(), ro.cpu().numpy(), ctx.kernel_launches - l0))
+    assert outs[0][2] == T  # one chain launch per frame
+    a = O.aperture(n, n)
+    for t in range(T):
+        for s in range(S):
+            assert phi_err(outs[0][0][t, s], outs[1][0][t, s].astype(np.float64), a) < 1e-3
+            assert np.linalg.norm(outs[0][1][t, s] - outs[1][1][t, s]) / np.linalg.norm(outs[1][1][t, s]) < 1e-3
 
 
 # -------------------------------------------------- bootstrap and static
@@ -487,10 +581,12 @@ def test_large_grid_sampled(cfgname, S):
 # ------------------------------------------------ edge cases / invariants
 
 
-def test_degenerate_frame_keeps_state():
+@pytest.mark.parametrize("chain", [True, False])
+def test_degenerate_frame_keeps_state(chain):
     n, S = 64, 2
     y, _, _ = frames(n, S, 2)
-    ctx = DDH(n, S, noise_var=0.1)
+    with chain_env(chain):
+        ctx = DDH(n, S, noise_var=0.1)
     ctx.bootstrap(torch.from_numpy(y[0]).to(DEV), 3)
     r0, phi0, _ = ctx.get_state()
     yy = y[1:2].copy()
@@ -504,12 +600,15 @@ def test_degenerate_frame_keeps_state():
     assert fi == 2
 
 
-def test_state_continuity_bit_exact():
+@pytest.mark.parametrize("chain", [True, False])
+def test_state_continuity_bit_exact(chain):
     n, S = 64, 2
     y, _, _ = frames(n, S, 6)
     yt = torch.from_numpy(y).to(DEV)
-    a = DDH(n, S, noise_var=0.1)
-    b = DDH(n, S, noise_var=0.1)
+    with chain_env(chain):
+        a = DDH(n, S, noise_var=0.1)
+        b = DDH(n, S, noise_var=0.1)
+        c = DDH(n, S, noise_var=0.1)
     pa = torch.empty((6, S, n, n), device=DEV)
     pb = torch.empty_like(pa)
     a.step(yt, pa)
@@ -519,7 +618,6 @@ def test_state_continuity_bit_exact():
     # one call per frame (no S0 prefetch inside a call; RemoveTipTilt sums from
     # the previous S5) and a checkpoint / resume in the middle (sums recomputed
     # by S0): the same bits
-    c = DDH(n, S, noise_var=0.1)
     pc = torch.empty_like(pa)
     for t in range(6):
         c.step(yt[t:t + 1].contiguous(), pc[t:t + 1])
@@ -624,7 +722,8 @@ def test_step_host_async_pipeline_matches_device_path():
 
 def test_kernel_launch_count_and_empty_call():
     n, S = 64, 1
-    ctx = DDH(n, S, noise_var=0.1)
+    with chain_env(False):
+        ctx = DDH(n, S, noise_var=0.1)
     l0 = ctx.kernel_launches
     ctx.step(torch.empty((0, S, n, n), dtype=torch.complex64, device=DEV))
     assert ctx.kernel_launches == l0
