@@ -8,10 +8,11 @@
 // iteration costs shared-memory passes only (the streaming path's six
 // kernels move ~112 B/px through HBM / L2 per iteration).
 //
-// The arithmetic is the multi-pass path's (ddh_kernels.cu K0-K3b: the same
-// expressions, the same Stockham FFT, qgg_w / r_update / phi_update of
-// ddh_common.cuh), reductions in FP64 in a fixed order; parity with the oracle
-// in tests/test_gpu_parity.py (test_chain_*).
+// The arithmetic is the other paths': the multi-pass path's Stockham FFT and
+// elementwise stages (ddh_kernels.cu K1-K3a), the streaming path's packed
+// qGGMRF weights, E-step reciprocal, reduced sincos and polynomial atan2
+// (ddh_common.cuh), r_update / phi_update; reductions in FP64 in a fixed order.
+// Parity with the oracle in tests/test_gpu_parity.py (test_chain_*).
 #include "ddh_common.cuh"
 #include "ddh_fft.cuh"
 #include "ddh_kernels.h"
@@ -38,21 +39,46 @@ struct ChainSmem {
   double scal[8];
 };
 
-// qGGMRF coefficients B, S of pixel (i, j) (periodic 8-neighbourhood, R6-R8):
-// the K2b expressions
-__device__ __forceinline__ void chain_rBS(const float *rs, int i, int j, float b0, float inv_Tsig, float tmq,
-                                          float &B, float &S) {
-  const float ri = rs[i * kCN + j];
-  B = 0.f;
-  S = 0.f;
+// One qGGMRF r update of pixel (i, j) (R6-R9, periodic 8-neighbourhood) in
+// place: the streaming path's packed-pair weights (qgg_w2) and the shared root
+// finder r_update
+__device__ __forceinline__ void chain_rupd(float *rs, const float *qs, int i, int j, const StepArgs &A) {
+  const int im = ((i - 1) & (kCN - 1)) * kCN, i0 = i * kCN, ip = ((i + 1) & (kCN - 1)) * kCN;
+  const int jm = (j - 1) & (kCN - 1), jp = (j + 1) & (kCN - 1);
+  const float ri = rs[i0 + j];
+  const float2 nA = make_float2(rs[im + j], rs[ip + j]), nB = make_float2(rs[i0 + jm], rs[i0 + jp]);
+  const float2 dA = make_float2(rs[im + jm], rs[im + jp]), dB = make_float2(rs[ip + jm], rs[ip + jp]);
+  const float2 wA = qgg_w2(ri, nA, A.r_h, A.r_g, A.r_k), wB = qgg_w2(ri, nB, A.r_h, A.r_g, A.r_k);
+  const float2 wC = qgg_w2(ri, dA, A.r_h, A.r_g, A.r_k), wD = qgg_w2(ri, dB, A.r_h, A.r_g, A.r_k);
+  const float2 bs = p_fma(p_add(wC, wD), bc2(0.5f), p_add(wA, wB));
+  const float2 ss = p_fma(p_fma(wC, dA, p_mul(wD, dB)), bc2(0.5f), p_fma(wA, nA, p_mul(wB, nB)));
+  rs[i0 + j] = r_update(ri, qs[i0 + j], A.r_b6 * (bs.x + bs.y), A.r_b6 * (ss.x + ss.y), A.r_min);
+}
+
+// One GMRF phi update of pixel (i, j) (R10-R11) in place, free boundary: the
+// neighbours outside the frame are absent from both sums
+__device__ __forceinline__ void chain_phiupd(float *ps, const float *cs, const float *ts, int i, int j,
+                                             const StepArgs &A) {
+  const int g = i * kCN + j;
+  float nb = 0.f, sb = 0.f;
+  if (A.phi_prior) {
+    if (i > 0 && i < kCN - 1 && j > 0 && j < kCN - 1) {  // interior: all eight neighbours
+      const float n4 = (ps[g - kCN] + ps[g + kCN]) + (ps[g - 1] + ps[g + 1]);
+      const float nd = (ps[g - kCN - 1] + ps[g - kCN + 1]) + (ps[g + kCN - 1] + ps[g + kCN + 1]);
+      nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
+      sb = 1.f;
+    } else {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int ni = (i + nb_di(k)) & (kCN - 1), nj = (j + nb_dj(k)) & (kCN - 1);
-    const float rj = rs[ni * kCN + nj];
-    const float bt = nb_w(k) * b0 * qgg_w(ri - rj, inv_Tsig, tmq);
-    B += bt;
-    S = fmaf(bt, rj, S);
+      for (int k = 0; k < 8; ++k) {
+        const int ni = i + nb_di(k), nj = j + nb_dj(k);
+        if (ni >= 0 && ni < kCN && nj >= 0 && nj < kCN) {
+          nb = fmaf(nb_w(k), ps[ni * kCN + nj], nb);
+          sb += nb_w(k);
+        }
+      }
+    }
   }
+  ps[g] = phi_update(ps[g], cs[g], ts[g], nb, sb, A.phi_w, A.phi_prior != 0);
 }
 
 __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs C) {
@@ -137,7 +163,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
         const float2 y = __ldg(A.y + off + idx);
         const float dr = y.x - mur, di = y.y - mui;
         float sn, cs;
-        sincosf(M.ps[idx], &sn, &cs);
+        sincos_red(M.ps[idx], sn, cs);
         z = make_float2(dr * cs + di * sn, di * cs - dr * sn);
         if ((i + j) & 1) z = make_float2(-z.x, -z.y);
       }
@@ -156,7 +182,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
       const float rp = M.rs[idx];
       float r0 = rp;
       if (warm) r0 = fmaxf(fmaf(A.oml, rp, A.la * (u.x * u.x + u.y * u.y)), A.r_min);  // Eq. 3
-      const float w = r0 / (r0 + A.s2);
+      const float w = r0 * rcp_approx(r0 + A.s2);
       const float2 mu = make_float2(w * u.x, w * u.y);
       M.rs[idx] = r0;
       M.qs[idx] = fmaf(mu.x, mu.x, fmaf(mu.y, mu.y, w * A.s2));
@@ -171,9 +197,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
           const int ci = c >> 1, cj = c & 1;
           for (int p = tid; p < kCP / 4; p += kCThreads) {
             const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
-            float B, S;
-            chain_rBS(M.rs, i, j, A.r_b0, A.r_inv_Tsig, A.r_tmq, B, S);
-            M.rs[i * kCN + j] = r_update(M.rs[i * kCN + j], M.qs[i * kCN + j], B, S, A.r_min);
+            chain_rupd(M.rs, M.qs, i, j, A);
           }
           __syncthreads();
         }
@@ -195,8 +219,8 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
         const float2 y = __ldg(A.y + off + idx);
         const float2 yh = make_float2(kappa * (y.x - mur), kappa * (y.y - mui));
         const float2 z = make_float2(yh.x * f.x + yh.y * f.y, yh.y * f.x - yh.x * f.y);
-        c = two_s2 * hypotf(z.x, z.y);
-        th = atan2f(z.y, z.x);
+        c = two_s2 * sqrt_approx(fmaf(z.x, z.x, z.y * z.y) + 1e-37f);
+        th = atan2_fast(z.y, z.x);
       }
       M.qs[idx] = c;
       M.ts[idx] = th;
@@ -208,19 +232,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
         const int ci = c >> 1, cj = c & 1;
         for (int p = tid; p < kCP / 4; p += kCThreads) {
           const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
-          float nb = 0.f, sb = 0.f;
-          if (A.phi_prior) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int ni = i + nb_di(k), nj = j + nb_dj(k);
-              if (ni >= 0 && ni < kCN && nj >= 0 && nj < kCN) {
-                nb = fmaf(nb_w(k), M.ps[ni * kCN + nj], nb);
-                sb += nb_w(k);
-              }
-            }
-          }
-          const int g = i * kCN + j;
-          M.ps[g] = phi_update(M.ps[g], M.qs[g], M.ts[g], nb, sb, A.phi_w, A.phi_prior != 0);
+          chain_phiupd(M.ps, M.qs, M.ts, i, j, A);
         }
         __syncthreads();
       }

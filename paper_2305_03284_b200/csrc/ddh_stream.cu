@@ -101,32 +101,7 @@ template <int N> struct SCfg {
   static constexpr int RPITCH = N + N / 16;                          // padded row pitch
 };
 
-__device__ __forceinline__ void sincos_red(float p, float &sn, float &cs) {
-  // |argument| <= pi after one rint reduction, then MUFU sin/cos
-  __sincosf(fmaf(-6.283185307179586f, rintf(p * 0.15915494309189535f), p), &sn, &cs);
-}
-
-// atan2(y, x) for the phase-correlation angle: octant reduction + odd
-// minimax polynomial (degree 13) of atan on [0, 1]; |error| < 5e-7 rad
-// (FP32, measured against FP64 atan).  atan2(0, 0) = 0 (c = 0 there, so
-// theta is irrelevant).
-__device__ __forceinline__ float atan2_fast(float y, float x) {
-  const float ax = fabsf(x), ay = fabsf(y);
-  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  const float a = mx > 0.f ? mn * rcp_approx(mx) : 0.f;
-  const float s = a * a;
-  float p = 0.00681176f;
-  p = fmaf(p, s, -0.03360414f);
-  p = fmaf(p, s, 0.07962359f);
-  p = fmaf(p, s, -0.1323334f);
-  p = fmaf(p, s, 0.19807816f);
-  p = fmaf(p, s, -0.3331737f);
-  p = fmaf(p, s, 0.9999961f);
-  float r = p * a;
-  if (ay > ax) r = 1.5707963267948966f - r;
-  if (x < 0.f) r = 3.141592653589793f - r;
-  return copysignf(r, y);
-}
+// sincos_red, atan2_fast: ddh_common.cuh (shared with the on-chip chain)
 
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
