@@ -45,6 +45,7 @@ struct ChainSmem {
 __device__ __forceinline__ void chain_rupd(float *rs, const float *qs, int i, int j, const StepArgs &A) {
   const int im = ((i - 1) & (kCN - 1)) * kCN, i0 = i * kCN, ip = ((i + 1) & (kCN - 1)) * kCN;
   const int jm = (j - 1) & (kCN - 1), jp = (j + 1) & (kCN - 1);
+  DDH_DBG(i >= 0 && i < kCN && j >= 0 && j < kCN);
   const float ri = rs[i0 + j];
   const float2 nA = make_float2(rs[im + j], rs[ip + j]), nB = make_float2(rs[i0 + jm], rs[i0 + jp]);
   const float2 dA = make_float2(rs[im + jm], rs[im + jp]), dB = make_float2(rs[ip + jm], rs[ip + jp]);
@@ -60,6 +61,7 @@ __device__ __forceinline__ void chain_rupd(float *rs, const float *qs, int i, in
 __device__ __forceinline__ void chain_phiupd(float *ps, const float *cs, const float *ts, int i, int j,
                                              const StepArgs &A) {
   const int g = i * kCN + j;
+  DDH_DBG(i >= 0 && i < kCN && j >= 0 && j < kCN);
   float nb = 0.f, sb = 0.f;
   if (A.phi_prior) {
     if (i > 0 && i < kCN - 1 && j > 0 && j < kCN - 1) {  // interior: all eight neighbours
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
           const int ci = c >> 1, cj = c & 1;
           for (int p = tid; p < kCP / 4; p += kCThreads) {
             const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
+            DDH_DBG((i & 1) == ci && (j & 1) == cj);
             chain_rupd(M.rs, M.qs, i, j, A);
           }
           __syncthreads();
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
         const int ci = c >> 1, cj = c & 1;
         for (int p = tid; p < kCP / 4; p += kCThreads) {
           const int i = 2 * (p / (kCN / 2)) + ci, j = 2 * (p % (kCN / 2)) + cj;
+          DDH_DBG((i & 1) == ci && (j & 1) == cj);
           chain_phiupd(M.ps, M.qs, M.ts, i, j, A);
         }
         __syncthreads();

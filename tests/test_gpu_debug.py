@@ -23,7 +23,7 @@ def test_bounds_checked_build_runs_parity_tests():
     from paper_2305_03284_b200 import build
     lib = build.build(debug=True)
     env = dict(os.environ, DDH_LIB=lib)
-    sel = ("ricd_stage or ricd_large_launch or phiicd_stage or step_parity_priors_on and (64 or 128) or step_parity_masked "
+    sel = ("ricd_stage or ricd_large_launch or phiicd_stage or chain_step_parity or step_parity_priors_on and (64 or 128) or step_parity_masked "
            "or kernel_variants or degenerate or end_to_end_c1")
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "tests/test_gpu_parity.py", "-k", sel]
     pr = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=1500)
