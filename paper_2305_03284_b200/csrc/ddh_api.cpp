@@ -70,7 +70,10 @@ struct ddh_ctx {
   double strehl_den = 1.0;
   // host-buffer path: triple-buffered staging, H2D / compute / D2H on three
   // streams so the copies of frames t+1 and t-1 overlap the step of frame t
-  static constexpr int kStages = 3;  // host pipeline depth (frames in flight)
+#ifndef DDH_HOST_STAGES
+#define DDH_HOST_STAGES 3
+#endif
+  static constexpr int kStages = DDH_HOST_STAGES;  // host pipeline depth (frames in flight)
   float2 *y_stage[kStages] = {};
   float *phi_stage[kStages] = {}, *r_stage[kStages] = {};
   uint8_t *status_stage[kStages] = {};
@@ -93,6 +96,7 @@ struct ddh_ctx {
   // DDH_CHAIN: 0 never, 1 always (tests, measurements)
   bool chain = false;
   bool chain_force = false;
+  int chain_slots = 0;  // resident chain CTAs on the device (use_chain)
   bool l2_window = false;  // holds the device's persisting-L2 carve-out
   cudaStream_t side_st[8] = {};
   cudaEvent_t side_fork[8] = {}, side_join[8] = {};
@@ -368,10 +372,7 @@ bool use_chain(const ddh_ctx *c, int iters) {
   if (c->chain_force) return true;
   if (iters >= 4) return true;
   if (iters < 2) return false;
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const double slots = (double)ddh::chain_ctas_per_sm() * sms;
-  return c->sc >= 0.95 * slots && c->sc <= slots;
+  return c->sc >= 0.95 * c->chain_slots && c->sc <= c->chain_slots;
 }
 
 // One frame batch (all streams) through the loop body.  y: device frames
@@ -1046,6 +1047,12 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const char *ch = std::getenv("DDH_CHAIN");
     c->chain = c->streaming && ddh::chain_fits(n) && (ch ? std::atoi(ch) != 0 : true);
     c->chain_force = c->chain && ch && std::atoi(ch) == 1;
+    if (c->chain) {
+      int sms = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      c->chain_slots = ddh::chain_ctas_per_sm() * sms;
+    }
 
     if (c->split_r) {
       for (int l = 0; l < c->lanes; ++l) {
