@@ -175,6 +175,29 @@ __device__ __forceinline__ float atan2_fast(float y, float x) {
   return copysignf(r, y);
 }
 
+// Last read of a buffer in a step (DDH_EVICT_HINTS build knob): a streaming
+// load (ld.global.cs, evict-first) lets the lanes' other data stay in L2
+// (profiles/r02d_warm_traffic.json); otherwise the read-only path
+#ifndef DDH_EVICT_HINTS
+#define DDH_EVICT_HINTS 0
+#endif
+__device__ __forceinline__ float ldg_last(const float *a) {
+  float v;
+#if DDH_EVICT_HINTS
+  v = __ldcs(a);
+#else
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(a));
+#endif
+  return v;
+}
+__device__ __forceinline__ float2 ldg_last2(const float2 *a) {
+#if DDH_EVICT_HINTS
+  return __ldcs(a);
+#else
+  return __ldg(a);
+#endif
+}
+
 // ---- r M-step, one pixel (R9) -------------------------------------------
 // Minimiser over x >= r_min of f(x) = log x + q/x + B x^2 - 2 S x (B > 0).
 // f'(x) = g(x)/x^2 with g(x) = 2B x^3 - 2S x^2 + x - q, g(0) = -q < 0; g is

@@ -874,12 +874,12 @@ __device__ __forceinline__ void phiicd_phase(float *ps, const float2 *cts, int b
   const int gj = J0 + CJ;
   if (bcol < blo || bcol >= bhi || (EDGE && (unsigned)gj >= (unsigned)N)) return;
   auto okk = [&](int a, int gi) { return a >= alo && a < ahi && (!EDGE || (unsigned)gi < (unsigned)N); };
-  float2 cn = okk(arow0, I0 + CI) ? __ldg(cts + (size_t)(I0 + CI) * N + gj) : make_float2(0.f, 0.f);
+  float2 cn = okk(arow0, I0 + CI) ? ldg_last2(cts + (size_t)(I0 + CI) * N + gj) : make_float2(0.f, 0.f);
 #pragma unroll 1
   for (int k = 0; k < KP; ++k) {
     const int a = arow0 + R * k, gi = I0 + 2 * R * k + CI;
     const float2 ctk = cn;
-    if (k + 1 < KP && okk(a + R, gi + 2 * R)) cn = __ldg(cts + (size_t)(gi + 2 * R) * N + gj);
+    if (k + 1 < KP && okk(a + R, gi + 2 * R)) cn = ldg_last2(cts + (size_t)(gi + 2 * R) * N + gj);
     if (!okk(a, gi)) continue;
     const int o = b0 + R * k * G::kSubP;
 #if DDH_DEBUG_BOUNDS
@@ -1098,8 +1098,7 @@ __device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
   } else {
     // q is issued with the neighbour loads (volatile: left to itself the
     // compiler sinks it behind the weights, exposing its latency in r_update)
-    float q;
-    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(q) : "l"(A.q + off + g));
+    const float q = ldg_last(A.q + off + g);
     const float ri = __ldg(in + g);  // written only by this thread, after this read
     // periodic neighbour rows / columns (only one side of a colour class can wrap)
     const int ro[3] = {CI == 0 ? ((i - 1) & (N - 1)) * N : (i - 1) * N, i * N,
