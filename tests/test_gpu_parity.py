@@ -700,11 +700,13 @@ def test_sharding_and_launch_groups_bit_exact():
     assert torch.equal(torch.cat(halves, 1), outs[0])
 
 
-def test_step_host_matches_device_path():
+@pytest.mark.parametrize("chain", [False, True])
+def test_step_host_matches_device_path(chain):
     n, S, T = 64, 2, 3
     y, _, _ = frames(n, S, T)
-    a = DDH(n, S, noise_var=0.1)
-    b = DDH(n, S, noise_var=0.1)
+    with chain_env(chain):
+        a = DDH(n, S, noise_var=0.1)
+        b = DDH(n, S, noise_var=0.1)
     pa = torch.empty((T, S, n, n), device=DEV)
     a.step(torch.from_numpy(y).to(DEV), pa)
     yh = torch.from_numpy(y).pin_memory()
@@ -777,15 +779,17 @@ def test_fused_and_unfused_paths_agree():
                 assert np.linalg.norm(o[1][t, s] - outs[0][1][t, s]) / np.linalg.norm(outs[0][1][t, s]) < 1e-3
 
 
-@pytest.mark.parametrize("flags", [0, 1])
-def test_graph_replay_bit_exact(flags):
+@pytest.mark.parametrize("n,flags", [(128, 0), (128, 1), pytest.param(64, 0, id="chain")])
+def test_graph_replay_bit_exact(n, flags):
     """A recurring single-frame call (fixed frame and output buffers) is
     captured into a CUDA graph on its second occurrence and replayed; results
-    equal the launch-by-launch path bit for bit (phi ping-pong included)."""
-    n, S, T = 128, 2, 6
+    equal the launch-by-launch path bit for bit (phi ping-pong included; at
+    N = 64 the on-chip chain)."""
+    S, T = 2, 6
     y, _, _ = frames(n, S, T)
     yt = torch.from_numpy(y).to(DEV)
-    ctxs = [DDH(n, S, noise_var=0.1, flags=flags | 32), DDH(n, S, noise_var=0.1, flags=flags)]
+    with chain_env(n == 64):
+        ctxs = [DDH(n, S, noise_var=0.1, flags=flags | 32), DDH(n, S, noise_var=0.1, flags=flags)]
     bufs = [torch.empty((1, S, n, n), dtype=torch.complex64, device=DEV) for _ in ctxs]
     outs = [(torch.empty((1, S, n, n), device=DEV), torch.empty((1, S, n, n), device=DEV)) for _ in ctxs]
     for t in range(T):
