@@ -161,7 +161,7 @@ ddh_status ddh_bootstrap(ddh_ctx *c, const void *y0, int32_t k_b, uint8_t *statu
  * pointers), DDH_E_CUDA.
  * At N = 64 the frame's N_k iterations may run as one on-chip chain kernel
  * (one CTA per stream, the frame in shared memory) where that measured faster
- * (N_k >= 4, or N_k >= 2 with one full wave of resident CTAs); the results
+ * (N_k >= 2, or N_k = 1 with one full wave of resident CTAs); the results
  * agree with the six-kernel path at the parity tolerance. */
 ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float *r_out,
                     uint8_t *status);

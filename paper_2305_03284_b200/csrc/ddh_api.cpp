@@ -361,17 +361,14 @@ ddh_status run_phiicd(ddh_ctx *c, const float *phi_in, const float *cc, const fl
 enum class Mode { Step, Boot };
 
 // The chain for a Step frame of N_k iterations (measured at 64^2, one B200,
-// profiles/r02e_chain64.json): every N_k >= 4 (174 vs 194, 274 vs 384, 909 vs
-// 946 us at 64 / 296 / 1024 streams for N_k = 8); N_k = 2 (and 3) only when the
-// launch group is one full wave of resident CTAs (296 streams: 78 vs 95 us; 64
-// streams, 0.2 waves: 51.4 vs 50.2; 592 streams, 2 waves: 151 vs 150; 1024
-// streams, 3.46 waves: 255 vs 245); N_k = 1 never (the kernels' per-frame cost is
-// lower: 28 vs 31 and 126 vs 148 us).
+// profiles/r02e_chain64.json, device us per step, chain / six kernels): every
+// N_k >= 2 (N_k = 2: 47.4 / 47.9, 71.9 / 94.7, 231.6 / 245.2 at 64 / 296 / 1024
+// streams; N_k = 8: 161 / 193, 246 / 381, 814 / 942); N_k = 1 only when the
+// launch group is one full wave of resident CTAs (296 streams: 43.1 / 47.5; 64
+// streams, 0.2 waves: 28.9 / 27.8; 1024 streams, 3.46 waves: 137.2 / 125.9).
 bool use_chain(const ddh_ctx *c, int iters) {
   if (!c->chain) return false;
-  if (c->chain_force) return true;
-  if (iters >= 4) return true;
-  if (iters < 2) return false;
+  if (c->chain_force || iters >= 2) return true;
   return c->sc >= 0.95 * c->chain_slots && c->sc <= c->chain_slots;
 }
 

@@ -21,6 +21,9 @@ namespace ddh {
 namespace {
 
 constexpr int kCN = 64, kCP = kCN * kCN, kCPitch = kCN + 1, kCThreads = 512;
+// phi with a zero border (pitch N + 2): the free-boundary neighbours read 0 without a test
+constexpr int kPP = kCN + 2;
+__device__ __forceinline__ int pidx(int i, int j) { return (i + 1) * kPP + j + 1; }
 
 #ifndef DDH_CHAIN_MINB
 #define DDH_CHAIN_MINB 2
@@ -32,7 +35,7 @@ struct ChainSmem {
   float rs[kCP];            // r (in place through Eq. 3 and the r-ICD)
   float qs[kCP];            // q (E-step), then c (phase correlation)
   float ts[kCP];            // theta
-  float ps[kCP];            // phi (plane removed)
+  float ps[kPP * kPP];      // phi (plane removed), zero border
   float2 tw[kCN];
   int2 span[kCN];
   double red[32 * 5];
@@ -57,30 +60,22 @@ __device__ __forceinline__ void chain_rupd(float *rs, const float *qs, int i, in
 }
 
 // One GMRF phi update of pixel (i, j) (R10-R11) in place, free boundary: the
-// neighbours outside the frame are absent from both sums
+// neighbours outside the frame read the zero border and are dropped from sum b
+// (the streaming path's edge expression), so no lane of a warp diverges
 __device__ __forceinline__ void chain_phiupd(float *ps, const float *cs, const float *ts, int i, int j,
                                              const StepArgs &A) {
-  const int g = i * kCN + j;
+  const int g = i * kCN + j, gp = pidx(i, j);
   DDH_DBG(i >= 0 && i < kCN && j >= 0 && j < kCN);
   float nb = 0.f, sb = 0.f;
   if (A.phi_prior) {
-    if (i > 0 && i < kCN - 1 && j > 0 && j < kCN - 1) {  // interior: all eight neighbours
-      const float n4 = (ps[g - kCN] + ps[g + kCN]) + (ps[g - 1] + ps[g + 1]);
-      const float nd = (ps[g - kCN - 1] + ps[g - kCN + 1]) + (ps[g + kCN - 1] + ps[g + kCN + 1]);
-      nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
-      sb = 1.f;
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int ni = i + nb_di(k), nj = j + nb_dj(k);
-        if (ni >= 0 && ni < kCN && nj >= 0 && nj < kCN) {
-          nb = fmaf(nb_w(k), ps[ni * kCN + nj], nb);
-          sb += nb_w(k);
-        }
-      }
-    }
+    const float n4 = (ps[gp - kPP] + ps[gp + kPP]) + (ps[gp - 1] + ps[gp + 1]);
+    const float nd = (ps[gp - kPP - 1] + ps[gp - kPP + 1]) + (ps[gp + kPP - 1] + ps[gp + kPP + 1]);
+    nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
+    const bool tp = i == 0, bt = i == kCN - 1, lf = j == 0, rt = j == kCN - 1;
+    sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
+         (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
   }
-  ps[g] = phi_update(ps[g], cs[g], ts[g], nb, sb, A.phi_w, A.phi_prior != 0);
+  ps[gp] = phi_update(ps[gp], cs[g], ts[g], nb, sb, A.phi_w, A.phi_prior != 0);
 }
 
 __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs C) {
@@ -93,6 +88,11 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
     M.tw[tid] = A.tw[tid];
     M.span[tid] = A.rowspan[tid];
   }
+  for (int k = tid; k < 4 * (kCN + 1); k += kCThreads) {  // the zero border of phi
+    const int e = k / (kCN + 1), t = k % (kCN + 1);
+    const int idx = e == 0 ? t : e == 1 ? (kCN + 1) * kPP + t + 1 : e == 2 ? (t + 1) * kPP : t * kPP + kCN + 1;
+    M.ps[idx] = 0.f;
+  }
   __syncthreads();
   auto ap = [&](int i, int j) { return j >= M.span[i].x && j < M.span[i].y; };
   // ---- load the frame and the state; sums for Normalize (Eq. 4) and RemoveTipTilt
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
     v[0] += (double)y.x;
     v[1] += (double)y.y;
     const float ph = A.phi_in[off + idx];
-    M.ps[idx] = ph;
+    M.ps[pidx(i, j)] = ph;
     M.rs[idx] = A.r_state[off + idx];
     if (A.apply_plane && ap(i, j)) {
       v[2] += (double)ph;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
   if (A.status && tid == 0) A.status[s] = degenerate ? 1 : 0;
   if (degenerate) {  // state unchanged (no tip/tilt removal either)
     for (int idx = tid; idx < kCP; idx += kCThreads) {
-      const float p = M.ps[idx], r = M.rs[idx];
+      const float p = M.ps[pidx(idx / kCN, idx & (kCN - 1))], r = M.rs[idx];
       C.phi_next[off + idx] = p;
       if (C.phi_copy) C.phi_copy[off + idx] = p;
       if (C.r_copy) C.r_copy[off + idx] = r;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
   if (A.apply_plane) {
     for (int idx = tid; idx < kCP; idx += kCThreads) {
       const int i = idx / kCN, j = idx & (kCN - 1);
-      M.ps[idx] -= (c0 + c1 * (float)(j - kCN / 2) + c2 * (float)(i - kCN / 2));
+      M.ps[pidx(i, j)] -= (c0 + c1 * (float)(j - kCN / 2) + c2 * (float)(i - kCN / 2));
     }
   }
   const int fb = tid % kCN, ft = tid / kCN;  // FFT: vector fb, lane ft (8 threads per 64-point vector)
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
         const float2 y = __ldg(A.y + off + idx);
         const float dr = y.x - mur, di = y.y - mui;
         float sn, cs;
-        sincos_red(M.ps[idx], sn, cs);
+        sincos_red(M.ps[pidx(i, j)], sn, cs);
         z = make_float2(dr * cs + di * sn, di * cs - dr * sn);
         if ((i + j) & 1) z = make_float2(-z.x, -z.y);
       }
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kCThreads, DDH_CHAIN_MINB) ks_chain(ChainArgs 
   __syncthreads();
   // ---- WriteData: the new state (and the caller's copies)
   for (int idx = tid; idx < kCP; idx += kCThreads) {
-    const float p = M.ps[idx], r = M.rs[idx];
+    const float p = M.ps[pidx(idx / kCN, idx & (kCN - 1))], r = M.rs[idx];
     C.phi_next[off + idx] = p;
     A.r_state[off + idx] = r;
     if (C.phi_copy) C.phi_copy[off + idx] = p;

@@ -26,12 +26,18 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include "ddh_f32x2.cuh"
+
 namespace ddh {
 
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// complex add / subtract / multiply on packed FP32 pairs (FADD2 / FMUL2 /
+// FFMA2): every lane rounds as the scalar expression would, so the results are
+// the bits of (a.x + b.x, a.y + b.y) and (fma(a.x, b.x, -a.y b.y),
+// fma(a.x, b.y, a.y b.x)); only the instruction count drops
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return p_add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return p_sub(a, b); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+  return p_fma(bc2(a.x), b, p_mul(make_float2(-a.y, a.y), make_float2(b.y, b.x)));
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }

@@ -426,13 +426,14 @@ def test_chain_and_streaming_kernels_agree():
 
 def test_chain_selection_rule():
     """The library's automatic choice at N = 64 (use_chain, ddh_api.cpp): the
-    six kernels at N_k = 1, the chain (one launch per frame) at N_k >= 4."""
+    six kernels at N_k = 1 (2 streams: far from a full wave), the chain (one
+    launch per frame) at N_k >= 2."""
     n, S = 64, 2
     y, _, _ = frames(n, S, 1)
     yt = torch.from_numpy(y).to(DEV)
     old = os.environ.pop("DDH_CHAIN", None)
     try:
-        for nk, per_frame in ((1, 6), (4, 1)):
+        for nk, per_frame in ((1, 6), (2, 1), (4, 1)):
             ctx = DDH(n, S, noise_var=0.1, n_k=nk)
             l0 = ctx.kernel_launches
             ctx.step(yt[:1])
