@@ -424,6 +424,23 @@ def test_chain_and_streaming_kernels_agree():
             assert np.linalg.norm(outs[0][1][t, s] - outs[1][1][t, s]) / np.linalg.norm(outs[1][1][t, s]) < 1e-3
 
 
+def test_chain_launch_groups_bit_exact():
+    """The chain over ragged launch groups (5 streams in groups of 2) equals one
+    group bit for bit (one CTA per stream, no cross-stream arithmetic)."""
+    n, S, T = 64, 5, 3
+    y, _, _ = frames(n, S, T)
+    yt = torch.from_numpy(y).to(DEV)
+    outs = []
+    with chain_env(True):
+        for chunk in (0, 2):
+            ctx = DDH(n, S, noise_var=0.1, n_k=2, chunk_streams=chunk)
+            po = torch.empty((T, S, n, n), device=DEV)
+            ro = torch.empty_like(po)
+            ctx.step(yt, po, ro)
+            outs.append((po, ro))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
 def test_chain_selection_rule():
     """The library's automatic choice at N = 64 (use_chain, ddh_api.cpp): the
     six kernels at N_k = 1 (2 streams: far from a full wave), the chain (one
