@@ -873,14 +873,23 @@ __device__ __forceinline__ void phiicd_phase(float *ps, const float2 *cts, int b
   constexpr int blo = sub_lo(C + 1, CJ), bhi = sub_lo(G::kReg - C - 1, CJ);
   const int gj = J0 + CJ;
   if (bcol < blo || bcol >= bhi || (EDGE && (unsigned)gj >= (unsigned)N)) return;
-  auto okk = [&](int a, int gi) { return a >= alo && a < ahi && (!EDGE || (unsigned)gi < (unsigned)N); };
-  float2 cn = okk(arow0, I0 + CI) ? ldg_last2(cts + (size_t)(I0 + CI) * N + gj) : make_float2(0.f, 0.f);
+  // the thread's slots k of this phase form one range [kb, ke): rows a = arow0 + R k
+  // inside [alo, ahi) and, in EDGE tiles, frame rows gi = I0 + CI + 2 R k inside [0, N)
+  auto cdiv = [](int x, int d) { return x >= 0 ? (x + d - 1) / d : -((-x) / d); };  // ceil(x / d), d > 0
+  int kb = max(0, cdiv(alo - arow0, R)), ke = min(KP, cdiv(ahi - arow0, R));
+  if (EDGE) {
+    kb = max(kb, cdiv(-(I0 + CI), 2 * R));
+    ke = min(ke, cdiv(N - (I0 + CI), 2 * R));
+  }
+  const bool lr_edge = EDGE && (gj == 0 || gj == N - 1);  // this thread's column is a frame edge
+  float2 cn = kb < ke ? ldg_last2(cts + (size_t)(I0 + CI + 2 * R * kb) * N + gj) : make_float2(0.f, 0.f);
 #pragma unroll 1
-  for (int k = 0; k < KP; ++k) {
+  for (int k = kb; k < ke; ++k) {
     const int a = arow0 + R * k, gi = I0 + 2 * R * k + CI;
     const float2 ctk = cn;
-    if (k + 1 < KP && okk(a + R, gi + 2 * R)) cn = ldg_last2(cts + (size_t)(gi + 2 * R) * N + gj);
-    if (!okk(a, gi)) continue;
+    if (k + 1 < ke) cn = ldg_last2(cts + (size_t)(gi + 2 * R) * N + gj);
+    DDH_DBG(a >= alo && a < ahi && (!EDGE || (unsigned)gi < (unsigned)N));
+    (void)a;
     const int o = b0 + R * k * G::kSubP;
 #if DDH_DEBUG_BOUNDS
     DDH_DBG(o == G::sidx(0, a, bcol));
@@ -897,8 +906,8 @@ __device__ __forceinline__ void phiicd_phase(float *ps, const float2 *cts, int b
     const float nd = (ps[o + G::template nidx<CI, CJ, -1, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, -1, 1>(0, 0)]) +
                      (ps[o + G::template nidx<CI, CJ, 1, -1>(0, 0)] + ps[o + G::template nidx<CI, CJ, 1, 1>(0, 0)]);
     const float nb = fmaf(nd, 1.f / 12.f, n4 * (1.f / 6.f));
-    float sb = 1.f;  // sum of b over the existing neighbours
-    if (EDGE) {
+    float sb = 1.f;  // sum of b over the existing neighbours (the expression is exactly 1 inside)
+    if (EDGE && (lr_edge || gi == 0 || gi == N - 1)) {
       const bool tp = gi == 0, bt = gi == N - 1, lf = gj == 0, rt = gj == N - 1;
       sb = 1.f - (1.f / 6.f) * (float)(tp + bt + lf + rt) -
            (1.f / 12.f) * (float)((tp | lf) + (tp | rt) + (bt | lf) + (bt | rt));
