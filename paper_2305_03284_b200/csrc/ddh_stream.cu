@@ -573,15 +573,11 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
     const size_t off = (size_t)s * P;
     float2 *slab = reinterpret_cast<float2 *>(stage0 + st * Q::STAGE);  // [N][W]
     const float *rsl = reinterpret_cast<const float *>(stage0 + st * Q::STAGE + Q::CB);
-    const double d2 = sum_part1(A.part1, A.nb1, s);
-    const bool degenerate = !(d2 > 0.0);
-    const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
-    if (bx == 0 && tid == 0) {
-      if (A.status) call_status(A)[s] = degenerate ? 1 : 0;
-      A.sstat[(size_t)s * kStatW + 5] = kappa;
-      A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
-    }
-    const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
+    // the stream's ||y - mu||^2 partials: loaded now, reduced after the column FFT (the
+    // same per-lane sums and shuffle tree as sum_part1; its L2 latency was 28 % of the
+    // kernel's stall samples when the reduction came first)
+    double p1 = 0.0;
+    for (int bb = tid & 31; bb < A.nb1; bb += 32) p1 += A.part1[(size_t)s * A.nb1 + bb];
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's group (one newer may be pending)
     __syncthreads();  // every thread's chunks (and the twiddles) visible
     float2 v[E];
@@ -589,6 +585,15 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
     for (int e = 0; e < E; ++e) v[e] = slab[(t + TPV * e) * W + b];
     __syncthreads();  // the slab becomes the exchange buffer
     fft_reg<N>(v, t, slab + b, [](int p) { return p * W; }, tw);
+    const double d2 = warp_sum(p1);
+    const bool degenerate = !(d2 > 0.0);
+    const float kappa = degenerate ? 0.f : (float)sqrt((double)P / d2);  // Eq. 4
+    if (bx == 0 && tid == 0) {
+      if (A.status) call_status(A)[s] = degenerate ? 1 : 0;
+      A.sstat[(size_t)s * kStatW + 5] = kappa;
+      A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
+    }
+    const float scale = kappa / (float)N;  // F_c = chi F chi / N
     const bool warm = A.warm && !degenerate;
     float2 w2[E];
 #pragma unroll
