@@ -162,6 +162,15 @@ template <int N>
 __device__ __forceinline__ void load_tw(float4 *tw, const float4 *__restrict__ g, int tid, int nt) {
   for (int k = tid; k < N; k += nt) tw[k] = g[k];
 }
+// the same table by 16-byte cp.async (one commit group; the caller waits for it
+// before the barrier that precedes the first FFT): no register round trip, so
+// the table's L2 latency overlaps the kernel's other loads
+template <int N>
+__device__ __forceinline__ void load_tw_async(float4 *tw, const float4 *__restrict__ g, int tid, int nt) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(tw);
+  for (int k = tid; k < N; k += nt) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * k), "l"(g + k));
+  asm volatile("cp.async.commit_group;");
+}
 
 }  // namespace
 
@@ -384,7 +393,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_
     if (blockIdx.x < total) issue(blockIdx.x, 0, true, false);
     if (blockIdx.x + G < total) issue(blockIdx.x + G, 1, true, false);
   }
-  load_tw<N>(tw, A.tw4, tid, NT);
+  load_tw_async<N>(tw, A.tw4, tid, NT);  // completed by the wait_group 0 below
   DDH_PDL_WAIT();
   if (tid == 0) {
     if (blockIdx.x < total) issue(blockIdx.x, 0, false, true);
@@ -482,7 +491,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   const int col = blockIdx.x * W + b;
   const size_t off = (size_t)s * P;
   DDH_PDL_TRIGGER();
-  load_tw<N>(tw, A.tw4, tid, NT);
+  load_tw_async<N>(tw, A.tw4, tid, NT);
   DDH_PDL_WAIT();
   float2 v[E];
 #pragma unroll
@@ -500,6 +509,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
     A.sstat[(size_t)s * kStatW + 6] = degenerate ? 1.f : 0.f;
   }
   const float scale = kappa / (float)N;                                 // F_c = chi F chi / N
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // twiddles (visible after the FFT's first barrier)
   fft_reg<N>(v, t, buf + b, [](int p) { return p * W; }, tw);
   const bool warm = A.warm && !degenerate;
   float2 w2[E];
@@ -560,7 +570,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
     }
   };
   DDH_PDL_TRIGGER();
-  load_tw<N>(tw, A.tw4, tid, NT);
+  load_tw_async<N>(tw, A.tw4, tid, NT);  // the oldest group: complete at the first wait_group 1
   DDH_PDL_WAIT();
   if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
   asm volatile("cp.async.commit_group;");
@@ -634,20 +644,21 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   const int i = bx * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
   DDH_PDL_TRIGGER();
-  {  // y is read-only user input: staged before the wait
+  load_tw_async<N>(tw, A.tw4, tid, NT);  // commit group 1 of 2
+  {  // y is read-only user input: staged before the wait (commit group 2 of 2)
     const char *src = reinterpret_cast<const char *>(call_y(A, A.y) + (size_t)s * P + (size_t)bx * H * N);
     const unsigned dst = (unsigned)__cvta_generic_to_shared(ys);
     for (int k = tid * 16; k < H * N * 8; k += NT * 16)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k), "l"(src + k));
     asm volatile("cp.async.commit_group;");
   }
-  load_tw<N>(tw, A.tw4, tid, NT);
   DDH_PDL_WAIT();
   float2 v[E];
 #pragma unroll
   for (int e = 0; e < E; ++e) v[e] = A.cbuf[row + t + TPV * e];
   const float *stt = A.sstat + (size_t)s * kStatW;  // from S1 (mu) and S2 (kappa)
   const float mur = stt[0], mui = stt[1], kappa = stt[5];
+  asm volatile("cp.async.wait_group 1;" ::: "memory");  // the twiddle group (y may still be in flight)
   __syncthreads();  // twiddles
   fft_reg<N>(v, t, buf + b * C::RPITCH, [](int p) { return rpad(p); }, tw);
   asm volatile("cp.async.wait_group 0;");
