@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_
     char *stg = stage0 + st * Q::STAGE;
     const float2 *ys = reinterpret_cast<const float2 *>(stg) + b * N;
     const float *fs = reinterpret_cast<const float *>(stg + Q::YB) + b * N;
+    const int2 sp = __ldg(A.rowspan + i);  // issued first: consumed after the mbarrier wait
     if (item + G < total) issue_scal(item + G, st ^ 1);  // the next item's scalars, in flight during this one
     double sums[5] = {0, 0, 0, 0, 0}, cpl[3] = {0, 0, 0};
     {  // stream totals from the staged partials (same order as sum_part0: lane b, b + 32, ...; xor tree)
@@ -429,7 +430,6 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_
       if (A.apply_plane) ss[2] = c0, ss[3] = c1, ss[4] = c2;
       if (A.psum_out) A.psum_out[(size_t)s * 3] = A.psum_out[(size_t)s * 3 + 1] = A.psum_out[(size_t)s * 3 + 2] = 0.0;
     }
-    const int2 sp = __ldg(A.rowspan + i);
     const float pyi = fmaf(c2, (float)(i - N / 2), c0);
     mbar_wait(&mb[st], (k >> 1) & 1);
     float2 v[E];
@@ -587,7 +587,12 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
     // same per-lane sums and shuffle tree as sum_part1; its L2 latency was 28 % of the
     // kernel's stall samples when the reduction came first)
     double p1 = 0.0;
-    for (int bb = tid & 31; bb < A.nb1; bb += 32) p1 += A.part1[(size_t)s * A.nb1 + bb];
+    if (A.nb1 <= 32) {  // one partial per lane: a plain load (0 + x = x), consumed after the FFT
+      const int lane = tid & 31;
+      if (lane < A.nb1) p1 = __ldg(A.part1 + (size_t)s * A.nb1 + lane);
+    } else {
+      for (int bb = tid & 31; bb < A.nb1; bb += 32) p1 += A.part1[(size_t)s * A.nb1 + bb];
+    }
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's group (one newer may be pending)
     __syncthreads();  // every thread's chunks (and the twiddles) visible
     float2 v[E];
@@ -644,6 +649,7 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   const int i = bx * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
   DDH_PDL_TRIGGER();
+  const int2 sp = __ldg(A.rowspan + i);  // constant: loaded before the wait, used in the epilogue
   load_tw_async<N>(tw, A.tw4, tid, NT);  // commit group 1 of 2
   {  // y is read-only user input: staged before the wait (commit group 2 of 2)
     const char *src = reinterpret_cast<const char *>(call_y(A, A.y) + (size_t)s * P + (size_t)bx * H * N);
@@ -665,7 +671,6 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   __syncthreads();  // y rows staged
   // v = G = conj(F) with F = inverse row DFT; f = chi F / N, so
   // z = y-hat conj(f) = y-hat chi G / N
-  const int2 sp = __ldg(A.rowspan + i);
   const float kn = kappa / (float)N, two_s2 = 2.f / A.s2;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
