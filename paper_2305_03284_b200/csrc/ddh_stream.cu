@@ -74,6 +74,10 @@ __device__ __forceinline__ uint8_t *call_status(const StepArgs &A) {
 }
 
 constexpr int kSThreads = 256;
+#ifndef DDH_S5_LOAD_UNROLL
+#define DDH_S5_LOAD_UNROLL 4  // S5 tile-load loop unroll (build knob)
+#endif
+constexpr int kS5LoadUnroll = DDH_S5_LOAD_UNROLL;
 // 128-thread row CTAs (S1, S4) and S0 blocks: c3 124.0 -> 120.4 us per step, c4 +1.8 %,
 // c2 -0.5 %, c5 -1.8 % against 256 (the S4-fused next-frame sums need S0's thread count)
 #ifndef DDH_ROW_THREADS
@@ -982,7 +986,7 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
       const bool jin = gj >= 0 && gj < N;  // pairs are both inside or both outside
       const float px = fmaf(c1, (float)(gj - N / 2), c0);
       const float *src = pin + gj;
-#pragma unroll 4
+#pragma unroll kS5LoadUnroll
       for (int li = r0; li < G::kReg; li += RP) {
         const int gi = i0 - kHalo + li;
         float2 v = make_float2(0.f, 0.f);
