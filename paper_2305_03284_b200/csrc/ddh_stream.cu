@@ -576,6 +576,9 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
   DDH_PDL_TRIGGER();
   load_tw_async<N>(tw, A.tw4, tid, NT);  // the oldest group: complete at the first wait_group 1
   DDH_PDL_WAIT();
+  double p1n = 0.0;  // the first item's partial (nb1 <= 32: one per lane, before the slab copies), then one item ahead
+  if (A.nb1 <= 32 && (int)blockIdx.x < total && (tid & 31) < A.nb1)
+    p1n = __ldg(A.part1 + (size_t)(blockIdx.x / NC) * A.nb1 + (tid & 31));
   if ((int)blockIdx.x < total) issue(blockIdx.x, 0);
   asm volatile("cp.async.commit_group;");
   if ((int)blockIdx.x + G < total) issue(blockIdx.x + G, 1);
@@ -587,14 +590,15 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
     const size_t off = (size_t)s * P;
     float2 *slab = reinterpret_cast<float2 *>(stage0 + st * Q::STAGE);  // [N][W]
     const float *rsl = reinterpret_cast<const float *>(stage0 + st * Q::STAGE + Q::CB);
-    // the stream's ||y - mu||^2 partials: loaded now, reduced after the column FFT (the
-    // same per-lane sums and shuffle tree as sum_part1; its L2 latency was 28 % of the
-    // kernel's stall samples when the reduction came first)
-    double p1 = 0.0;
-    if (A.nb1 <= 32) {  // one partial per lane: a plain load (0 + x = x), consumed after the FFT
+    // the stream's ||y - mu||^2 partials (one per lane at nb1 <= 32, loaded one item ahead:
+    // issued at the item start their L2 latency was 28-32 % of the kernel's stall samples,
+    // the compiler hoisting the reduction up to the load)
+    double p1 = p1n;
+    if (A.nb1 <= 32) {
       const int lane = tid & 31;
-      if (lane < A.nb1) p1 = __ldg(A.part1 + (size_t)s * A.nb1 + lane);
+      p1n = (item + G < total && lane < A.nb1) ? __ldg(A.part1 + (size_t)((item + G) / NC) * A.nb1 + lane) : 0.0;
     } else {
+      p1 = 0.0;
       for (int bb = tid & 31; bb < A.nb1; bb += 32) p1 += A.part1[(size_t)s * A.nb1 + bb];
     }
     asm volatile("cp.async.wait_group 1;" ::: "memory");  // item k's group (one newer may be pending)
