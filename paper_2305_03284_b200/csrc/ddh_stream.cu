@@ -1457,7 +1457,8 @@ cudaError_t launch_s4(const StepArgs &a, cudaStream_t st) {
 // single-stream latency, +20 % halo recomputation)
 template <int N>
 static bool small_tiles(int sc) {
-  return N >= 64 && (N / 64) * (N / 64) * sc < 2 * device_sms();
+  static const int on = getenv("DDH_SMALL_TILES") ? atoi(getenv("DDH_SMALL_TILES")) : 1;  // diagnostic
+  return on && N >= 64 && (N / 64) * (N / 64) * sc < 2 * device_sms();
 }
 // 16x16 tiles when even 32-tiles would leave most SMs idle (one stream at
 // N <= 256: 256 CTAs with one pass per colour phase; c2 step 26.3 -> 24.7 us
