@@ -43,6 +43,26 @@
 // buffer a predecessor produces or consumes before the wait.
 #define DDH_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 #define DDH_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+// DDH_PDL_NOTRIG (build knob, bits S0 1, S1 2, S2 4, S4 8, r-ICD 16, phi-ICD 32):
+// kernels whose bit is set issue no early launch_dependents, so their
+// dependent launches only as their CTAs exit (no dependent CTAs resident
+// and waiting beside them while other lanes' kernels need the slots).
+// Default: S2 only (its dependent S4 resident and waiting during the whole
+// persistent S2 cost the c3 step 1 %: 546.1-546.2 k -> 551.8-552.1 k frames/s,
+// profiles/r02h_pdl_ab.txt; every other kernel measured best with the early
+// trigger, e.g. S4 without it 546 -> 539 k)
+#ifndef DDH_PDL_NOTRIG
+#define DDH_PDL_NOTRIG 4
+#endif
+// DDH_PDL_LATE (bits S1 2, S2 4 of the persistent forms): launch_dependents
+// when a CTA starts its last item (with the bit also set in DDH_PDL_NOTRIG)
+#ifndef DDH_PDL_LATE
+#define DDH_PDL_LATE 0
+#endif
+#define DDH_PDL_TRIGGER_K(bit)                  \
+  do {                                          \
+    if (!(DDH_PDL_NOTRIG & (bit))) DDH_PDL_TRIGGER(); \
+  } while (0)
 
 namespace ddh {
 
@@ -199,7 +219,7 @@ __global__ void __launch_bounds__(kS0Threads) ks_stats(StepArgs A) {
   const size_t off = (size_t)s * P;
   double l0 = 0.0, lx = 0.0, ly = 0.0;
   double yr = 0.0, yi = 0.0;
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(1);
   DDH_PDL_WAIT();
   const float2 *Y = A.want_y ? call_y(A, A.y) : nullptr;
   for (size_t p0 = base + (size_t)threadIdx.x * 8; p0 < base + per; p0 += (size_t)kS0Threads * 8) {
@@ -260,7 +280,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 1024 / SCfg<N>::NTR) ks_rows_fwd
   const size_t row = off + (size_t)i * N;
   // issue the loads first (y: 8 B, phi: 4 B per pixel, comb t + TPV e); the
   // frames are read-only user input, so they may be read before the wait
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(2);
   const float2 *Y = call_y(A, A.y);
   float2 v[E];
 #pragma unroll
@@ -391,7 +411,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(2);
   // y is read-only user input: its copies may start before the wait; phi after
   if (tid == 0) {
     if (blockIdx.x < total) issue(blockIdx.x, 0, true, false);
@@ -408,6 +428,9 @@ __global__ void __launch_bounds__(SCfg<N>::NTR, 512 / SCfg<N>::NTR) ks_rows_fwd_
   __syncthreads();  // twiddles, first item's scalars
   int k = 0;
   for (int item = blockIdx.x; item < total; item += G, ++k) {
+#if DDH_PDL_LATE & 2
+    if (item + G >= total) DDH_PDL_TRIGGER();  // the dependent launches as the last items start
+#endif
     const int st = k & 1, bx = item % NR, s = item / NR;
     const int i = bx * H + b;
     const size_t row = (size_t)s * P + (size_t)i * N;
@@ -494,7 +517,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   const int b = tid % W, t = tid / W;
   const int col = blockIdx.x * W + b;
   const size_t off = (size_t)s * P;
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(4);
   load_tw_async<N>(tw, A.tw4, tid, NT);
   DDH_PDL_WAIT();
   float2 v[E];
@@ -573,7 +596,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
                    "l"(A.r_state + base + (size_t)row * N + 4 * part));
     }
   };
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(4);
   load_tw_async<N>(tw, A.tw4, tid, NT);  // the oldest group: complete at the first wait_group 1
   DDH_PDL_WAIT();
   double p1n = 0.0;  // the first item's partial (nb1 <= 32: one per lane, before the slab copies), then one item ahead
@@ -585,6 +608,9 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
   asm volatile("cp.async.commit_group;");
   int k = 0;
   for (int item = blockIdx.x; item < total; item += G, ++k) {
+#if DDH_PDL_LATE & 4
+    if (item + G >= total) DDH_PDL_TRIGGER();  // the dependent launches as the last items start
+#endif
     const int st = k & 1, bx = item % NC, s = item / NC;
     const int col = bx * W + b;
     const size_t off = (size_t)s * P;
@@ -656,7 +682,7 @@ __device__ __forceinline__ void rows_inv_body(const StepArgs &A, const int bx, c
   const int t = tid % TPV, b = tid / TPV;
   const int i = bx * H + b;
   const size_t row = (size_t)s * P + (size_t)i * N;
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(8);
   const int2 sp = __ldg(A.rowspan + i);  // constant: loaded before the wait, used in the epilogue
   load_tw_async<N>(tw, A.tw4, tid, NT);  // commit group 1 of 2
   {  // y is read-only user input: staged before the wait (commit group 2 of 2)
@@ -782,7 +808,7 @@ __global__ void __launch_bounds__(NTH, 2048 / NTH) ks_ricd(StepArgs A) {
   const size_t off = (size_t)s * P;
   const float *__restrict__ rin = A.icd_in + off;
   const float *__restrict__ qin = A.q + off;
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(16);
   DDH_PDL_WAIT();
   {  // thread = one pair column pj of the region, rows r0, r0 + RP, ...
     constexpr int RP = NTH / G::kSub;
@@ -975,7 +1001,7 @@ __global__ void __launch_bounds__(IcdT<TILE>::NTH, IcdT<TILE>::MINB) ks_phiicd(S
   const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
   const size_t off = (size_t)s * P;
   const float *__restrict__ pin = A.icd_in + off;
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(32);
   DDH_PDL_WAIT();
 
   const float *st = A.sstat + (size_t)s * kStatW;
@@ -1163,7 +1189,7 @@ __device__ __forceinline__ void ricd_pass_px(const StepArgs &A, int s, int p) {
 #endif
 template <int N, int C>
 __global__ void __launch_bounds__(256, DDH_RICD_MINB) ks_ricd_pass(StepArgs A) {
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(16);
   DDH_PDL_WAIT();
   ricd_pass_px<N, C>(A, blockIdx.y, blockIdx.x * 256 + threadIdx.x);
 }
@@ -1206,7 +1232,7 @@ __global__ void __launch_bounds__(RowsCfg<N>::NT, RowsCfg<N>::MINB) ks_ricd_rows
   const unsigned gm = (unsigned)(((i - 1) & (N - 1)) * N + 2 * p), g0 = (unsigned)(i * N + 2 * p),
                  gp = (unsigned)(((i + 1) & (N - 1)) * N + 2 * p);
   DDH_DBG(i < N && 2 * p + 1 < N && lr < RPC);
-  DDH_PDL_TRIGGER();
+  DDH_PDL_TRIGGER_K(16);
   DDH_PDL_WAIT();
   const float dflag = A.sstat[(size_t)s * kStatW + 6];
   const float2 M = __ldg(reinterpret_cast<const float2 *>(in + g0));
