@@ -259,13 +259,16 @@ def run_ours(args):
     gen_s = time.time() - t0
     ctx, y_dev, y_host, stream = unit.ctx, unit.y_dev, unit.y_host, unit.stream
     K, W = args.steps, args.warmup
-    unit.steps(W)
-    unit.prime_graphs()  # untimed: capture the call graphs the timed steps replay (both parities)
-    # parity sample (rank 0): one GPU step vs the oracle from the same FP32 state
+    # parity sample (rank 0): one GPU step vs the oracle from the same (warm) FP32 state.
+    # It runs BEFORE the warm-up: the oracle keeps the host busy for seconds with the GPU
+    # idle, which must not sit between the W warm-up steps and the timed region.
     parity = None
     if rank == 0 and not args.no_parity:
+        unit.steps(W)  # state preparation for the sample only (not the contract's warm-up)
         parity = quick_parity(ctx, y_dev, y_host, unit.pos, n, nv, dev)
         unit.pos = (unit.pos + 1) % F
+    unit.steps(W)  # the contract's W untimed warm-up steps, right before the timed region
+    unit.prime_graphs()  # untimed: capture the call graphs the timed steps replay (both parities)
     torch.cuda.synchronize()
     # ---- timed region: K steps, uninstrumented (the reported value)
     l0 = ctx.kernel_launches
