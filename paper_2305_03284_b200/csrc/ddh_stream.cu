@@ -43,7 +43,10 @@
 // buffer a predecessor produces or consumes before the wait.
 #define DDH_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 #define DDH_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
-// DDH_PDL_NOTRIG (build knob, bits S0 1, S1 2, S2 4, S4 8, r-ICD 16, phi-ICD 32):
+// DDH_PDL_NOTRIG (build knob, bits S0 1, S1 2, S2 4 (only launches with more items than
+// CTAs: with the bit applied to single-item launches too the single-stream latency rose
+// from 25.5 to 31.5 us p50, profiles/r02h_bench.json vs r02g_bench.json), S4 8, r-ICD 16,
+// phi-ICD 32, the large-launch S2 form `ks_cols` 64):
 // kernels whose bit is set issue no early launch_dependents, so their
 // dependent launches only as their CTAs exit (no dependent CTAs resident
 // and waiting beside them while other lanes' kernels need the slots).
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 1024 / SCfg<N>::NTC) ks_cols(Ste
   const int b = tid % W, t = tid / W;
   const int col = blockIdx.x * W + b;
   const size_t off = (size_t)s * P;
-  DDH_PDL_TRIGGER_K(4);
+  DDH_PDL_TRIGGER_K(64);  // the small-launch form keeps the early trigger (bit 64, not S2's 4): latency path
   load_tw_async<N>(tw, A.tw4, tid, NT);
   DDH_PDL_WAIT();
   float2 v[E];
@@ -596,7 +599,10 @@ __global__ void __launch_bounds__(SCfg<N>::NTC, 512 / SCfg<N>::NTC) ks_cols_p(St
                    "l"(A.r_state + base + (size_t)row * N + 4 * part));
     }
   };
-  DDH_PDL_TRIGGER_K(4);
+  // a launch of one item per CTA (single-stream latency mode) keeps the early trigger: S2's
+  // NOTRIG bit is about the dependent sitting beside a *persistent* S2 (c2 p50 31.5 -> 25.5 us)
+  if (total <= G) DDH_PDL_TRIGGER();
+  else DDH_PDL_TRIGGER_K(4);
   load_tw_async<N>(tw, A.tw4, tid, NT);  // the oldest group: complete at the first wait_group 1
   DDH_PDL_WAIT();
   double p1n = 0.0;  // the first item's partial (nb1 <= 32: one per lane, before the slab copies), then one item ahead
