@@ -79,6 +79,16 @@ typedef enum {
                                The first chunk of each key is captured (~ms of host
                                time); results are bit-identical either way         */
 
+#define DDH_F_NO_ADAPTIVE_GRAPHS 256u /* By default a multi-frame ddh_step on the streaming
+                               path switches to the chunk graphs of DDH_F_CALL_GRAPHS by
+                               itself at the second time it finds the ctx stream drained
+                               before a frame of a call with more than four chunks left
+                               (the device waits for the host; c3, 300 frames, a busy
+                               host: 330-350 k frames/s directly launched, 541 k from
+                               graphs), for the rest of that call and the next four long
+                               calls.  This flag keeps direct launches whatever the host
+                               does.  Results are bit-identical.                    */
+
 #define DDH_F_L2_PERSIST 64u /* opt-in (device-wide side effect): raise the device's
                                persisting-L2 carve-out to the ctx's spectrum buffer
                                (<= 48 MiB) and give the ctx's own lane streams an

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -148,6 +149,13 @@ struct ddh_ctx {
     int cur, pcur;  // state after the chunk (psum_valid is then true)
   };
   bool call_graphs = false;
+  // Adaptive call graphs (default; DDH_F_NO_ADAPTIVE_GRAPHS / DDH_ADAPTIVE_GRAPHS=0 turn it off):
+  // a long multi-frame call whose ctx stream is found drained before two frames of a call
+  // (the host, not the device, is the bound) finishes from chunk graphs.
+  // adapt: 0 off, 1 on, 2 test mode (every check counts as starved)
+  int adapt = 0, adapt_hot = 0, adapt_starved = 0;
+  double host_delay_us = 0.0;  // DDH_HOST_DELAY_US (diagnostic)
+  uint64_t adapt_switches = 0;
   int chunk = 8;
   bool rel_mode = false;  // capturing a call graph: pointers are stand-ins (StepArgs::rel)
   CallDesc *desc = nullptr;
@@ -1008,6 +1016,11 @@ ddh_status ddh_create(const ddh_params *pp, void *cuda_stream, ddh_ctx **out) {
     const char *ck = std::getenv("DDH_CHUNK");
     c->call_graphs = cg ? std::atoi(cg) != 0 : (p.flags & DDH_F_CALL_GRAPHS) && !(p.flags & DDH_F_SERIAL);
     c->chunk = std::max(2, ck ? std::atoi(ck) : 8);
+    if (const char *hd = std::getenv("DDH_HOST_DELAY_US")) c->host_delay_us = std::atof(hd);
+    const char *ad = std::getenv("DDH_ADAPTIVE_GRAPHS");  // 0 off, 1 on, 2 test mode
+    c->adapt = (p.flags & (DDH_F_SERIAL | DDH_F_GRAPHS)) ? 0
+               : ad ? std::atoi(ad)
+                    : ((p.flags & DDH_F_NO_ADAPTIVE_GRAPHS) || (cg && std::atoi(cg) == 0)) ? 0 : 1;
     A(cudaMalloc((void **)&c->desc, sizeof(CallDesc)));
     A(cudaMemset(c->desc, 0, sizeof(CallDesc)));
   }
@@ -1199,13 +1212,56 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
       c->frame += c->chunk;
     }
   }
-  for (; t < T; ++t) {
+  // Adaptive call graphs: directly launched frames need ~105 us of host time each at c3, a
+  // little less than the device needs, so a slow host makes a long call enqueue-bound (c3,
+  // 300 frames, the enqueue thread sharing its core: 552 k -> 330-350 k frames/s; from graphs
+  // 541 k either way, profiles/r02i_graphs_ab.txt).  The ctx stream found drained before two
+  // frames of a call (every lane joins it per frame) means the device waits for the host:
+  // the rest of the call then runs from chunk graphs (~2 % slower on the device, ~2 us of
+  // host time per frame).  Only with at least four chunks left (a capture costs ~ms once).
+  const bool can_adapt = c->adapt > 0 && c->streaming && !c->call_graphs && !use_chain(c, c->p.n_k) &&
+                         !c->profiling && c->sc == c->S;
+  // a ctx that switched keeps its next four long calls on graphs from their first frame
+  // (a busy host cannot be observed from a graph call), then probes again
+  bool graph_mode = can_adapt && c->adapt_hot > 0 && T > 4 * c->chunk;
+  if (graph_mode) --c->adapt_hot;
+  // drained-stream observations are kept in the ctx across calls (a host that runs in long
+  // bursts stalls once per call at most) and cleared by a long call that sees none
+  const bool probing = can_adapt && !graph_mode && T > 4 * c->chunk + 2;
+  int seen = 0;
+  while (t < T) {
+    if (graph_mode && !c->y_prefetched && t + c->chunk <= T) {
+      s = run_chunk(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
+                    r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr, c->chunk);
+      if (s != DDH_OK) return s;
+      c->frame += c->chunk;
+      t += c->chunk;
+      continue;
+    }
+    if (can_adapt && !graph_mode && t >= 2 && T - t > 4 * c->chunk) {
+      const cudaError_t q = c->adapt == 2 ? cudaSuccess : cudaStreamQuery(c->st);
+      if (q == cudaSuccess) {  // the second observation switches: consecutive (a slow host) or not (a host in bursts)
+        ++seen;
+        if (++c->adapt_starved >= 2) graph_mode = true, ++c->adapt_switches, c->adapt_hot = 4, c->adapt_starved = 0;
+      } else if (q != cudaErrorNotReady) {
+        DDH_CK(c, q);
+      }
+    }
+    if (c->host_delay_us > 0) {  // diagnostic (DDH_HOST_DELAY_US): a uniformly slower host, per directly launched frame
+      const auto t0 = std::chrono::steady_clock::now();
+      while (std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() < c->host_delay_us) {
+      }
+    }
+    // the frame before the first chunk prefetches nothing (chunks start with no cross-frame work pending)
+    const bool pf = t + 1 < T && !(graph_mode && t + 1 + c->chunk <= T);
     s = step_frame(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
                    r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr,
-                   t + 1 < T ? (const float2 *)y + (t + 1) * fs : nullptr);
+                   pf ? (const float2 *)y + (t + 1) * fs : nullptr);
     if (s != DDH_OK) return s;
     c->frame += 1;
+    ++t;
   }
+  if (probing && seen == 0) c->adapt_starved = 0;
   return DDH_OK;
 }
 

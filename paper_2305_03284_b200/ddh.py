@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("DDH_LIB") or os.path.join(_HERE, "lib", "libddh.so")
 
 DDH_F_NO_TIPTILT = 1
 DDH_F_CALL_GRAPHS = 128  # multi-frame calls replayed from chunk graphs (include/ddh.h)
+DDH_F_NO_ADAPTIVE_GRAPHS = 256  # never switch a long host-bound call to chunk graphs (include/ddh.h)
 
 _STATUS = {0: "DDH_OK", 1: "DDH_E_INVAL", 2: "DDH_E_CUDA", 3: "DDH_E_NOMEM", 4: "DDH_E_STATE"}
 

@@ -692,6 +692,40 @@ def test_call_graphs_bit_exact():
             assert a == b
 
 
+def test_adaptive_call_graphs_bit_exact(monkeypatch):
+    """A long multi-frame call that finds the device waiting for the host switches
+    to chunk graphs by itself (include/ddh.h DDH_F_NO_ADAPTIVE_GRAPHS).  Test mode
+    (DDH_ADAPTIVE_GRAPHS=2: every check counts as starved) forces the switch at
+    frame 3 of a 45-frame call: direct frames, a frame without prefetch, five chunk
+    graphs and a direct tail give the bits of direct launches, with fewer host
+    launches; with the feature off, or a call too short, nothing is replayed."""
+    n, S, T = 128, 24, 45
+    y, _, _ = frames(n, S, 5)
+    yt = torch.from_numpy(y).to(DEV).repeat(9, 1, 1, 1).contiguous()
+    res, launches = [], []
+    for mode in ("0", "2", "1"):
+        monkeypatch.setenv("DDH_ADAPTIVE_GRAPHS", mode)
+        ctx = DDH(n, S, noise_var=0.1, lanes=2)
+        po = torch.empty((T, S, n, n), device=DEV)
+        ro = torch.empty_like(po)
+        st = torch.empty((T, S), dtype=torch.uint8, device=DEV)
+        l0 = ctx.kernel_launches
+        ctx.step(yt, po, ro, st)
+        torch.cuda.synchronize()
+        launches.append(ctx.kernel_launches - l0)
+        short0 = ctx.kernel_launches
+        ctx.step(yt[:20], po[:20])  # too short to switch (at most four chunks left at frame 2)
+        short = ctx.kernel_launches - short0
+        po3 = torch.empty((T, S, n, n), device=DEV)
+        ctx.step(yt, po3)  # after a switch: the next long calls start on graphs at frame 0
+        r_, p_, f_ = ctx.get_state()
+        res.append((po, ro, st, po3, r_, p_, f_, short))
+    for other in res[1:]:
+        for a, b in zip(res[0], other):
+            assert torch.equal(a, b) if isinstance(a, torch.Tensor) else a == b
+    assert launches[1] != launches[0]  # five chunks came from graphs (+1 descriptor launch each)
+
+
 def test_sharding_and_launch_groups_bit_exact():
     """Streams are independent: the per-stream results do not depend on how
     streams are grouped into launches or split over contexts (G-GPU sharding
