@@ -81,13 +81,13 @@ typedef enum {
 
 #define DDH_F_NO_ADAPTIVE_GRAPHS 256u /* By default a multi-frame ddh_step on the streaming
                                path switches to the chunk graphs of DDH_F_CALL_GRAPHS by
-                               itself at the second time it finds the ctx stream drained
-                               before a frame of a call with more than four chunks left
-                               (the device waits for the host; c3, 300 frames, a busy
-                               host: 330-350 k frames/s directly launched, 541 k from
-                               graphs), for the rest of that call and the next four long
-                               calls.  This flag keeps direct launches whatever the host
-                               does.  Results are bit-identical.                    */
+                               itself when, at three consecutive frame boundaries (from
+                               frame 8 on, more than four chunks left), the device holds
+                               no whole frame of backlog: it is waiting for the host.
+                               The rest of that call and the ctx's next four long calls
+                               then come from graphs (tools/adapt_ab.sh).  This flag
+                               keeps direct launches whatever the host does.  Results
+                               are bit-identical.                                   */
 
 #define DDH_F_L2_PERSIST 64u /* opt-in (device-wide side effect): raise the device's
                                persisting-L2 carve-out to the ctx's spectrum buffer

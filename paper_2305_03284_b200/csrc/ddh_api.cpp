@@ -150,10 +150,11 @@ struct ddh_ctx {
   };
   bool call_graphs = false;
   // Adaptive call graphs (default; DDH_F_NO_ADAPTIVE_GRAPHS / DDH_ADAPTIVE_GRAPHS=0 turn it off):
-  // a long multi-frame call whose ctx stream is found drained before two frames of a call
-  // (the host, not the device, is the bound) finishes from chunk graphs.
+  // a long multi-frame call that finds the device waiting for the host (no whole frame of
+  // backlog at three consecutive frame boundaries) finishes from chunk graphs.
   // adapt: 0 off, 1 on, 2 test mode (every check counts as starved)
-  int adapt = 0, adapt_hot = 0, adapt_starved = 0;
+  int adapt = 0, adapt_hot = 0;
+  cudaEvent_t adapt_ev[2] = {nullptr, nullptr};  // ends of the last two directly launched frames
   double host_delay_us = 0.0;  // DDH_HOST_DELAY_US (diagnostic)
   uint64_t adapt_switches = 0;
   int chunk = 8;
@@ -798,6 +799,8 @@ void free_ctx(ddh_ctx *c) {
   if (c->desc) cudaFree(c->desc);
   if (c->cap_st) cudaStreamDestroy(c->cap_st);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->adapt_ev)
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->lane_ev)
     if (e) cudaEventDestroy(e);
   for (cudaStream_t s : c->lane_st)
@@ -1215,9 +1218,8 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
   // Adaptive call graphs: directly launched frames need ~105 us of host time each at c3, a
   // little less than the device needs, so a slow host makes a long call enqueue-bound (c3,
   // 300 frames, the enqueue thread sharing its core: 552 k -> 330-350 k frames/s; from graphs
-  // 541 k either way, profiles/r02i_graphs_ab.txt).  The ctx stream found drained before two
-  // frames of a call (every lane joins it per frame) means the device waits for the host:
-  // the rest of the call then runs from chunk graphs (~2 % slower on the device, ~2 us of
+  // 541 k either way, profiles/r02i_graphs_ab.txt).  When the device is found waiting for the
+  // host (below), the rest of the call runs from chunk graphs (~2 % slower on the device, ~2 us of
   // host time per frame).  Only with at least four chunks left (a capture costs ~ms once).
   const bool can_adapt = c->adapt > 0 && c->streaming && !c->call_graphs && !use_chain(c, c->p.n_k) &&
                          !c->profiling && c->sc == c->S;
@@ -1225,10 +1227,18 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
   // (a busy host cannot be observed from a graph call), then probes again
   bool graph_mode = can_adapt && c->adapt_hot > 0 && T > 4 * c->chunk;
   if (graph_mode) --c->adapt_hot;
-  // drained-stream observations are kept in the ctx across calls (a host that runs in long
-  // bursts stalls once per call at most) and cleared by a long call that sees none
-  const bool probing = can_adapt && !graph_mode && T > 4 * c->chunk + 2;
-  int seen = 0;
+  // The observable: when the host has enqueued frame t-1 and is about to enqueue frame t, is
+  // frame t-2 already complete?  A device-bound pipeline keeps at least one whole frame of
+  // backlog (the host runs ahead: at c3 by 11 us more per frame), a host-bound one executes
+  // kernels as they arrive.  (The ctx stream itself is never found drained at a frame boundary:
+  // the kernels enqueued last are still running.)  Checked from frame 8 on (the host's lead has
+  // built up by then); three consecutive observations switch.
+  const bool probing = can_adapt && !graph_mode && T > 4 * c->chunk + 8;
+  int consec = 0;
+  if (probing && !c->adapt_ev[0]) {
+    DDH_CK(c, cudaEventCreateWithFlags(&c->adapt_ev[0], cudaEventDisableTiming));
+    DDH_CK(c, cudaEventCreateWithFlags(&c->adapt_ev[1], cudaEventDisableTiming));
+  }
   while (t < T) {
     if (graph_mode && !c->y_prefetched && t + c->chunk <= T) {
       s = run_chunk(c, (const float2 *)y + t * fs, phi_out ? phi_out + t * fs : nullptr,
@@ -1238,12 +1248,13 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
       t += c->chunk;
       continue;
     }
-    if (can_adapt && !graph_mode && t >= 2 && T - t > 4 * c->chunk) {
-      const cudaError_t q = c->adapt == 2 ? cudaSuccess : cudaStreamQuery(c->st);
-      if (q == cudaSuccess) {  // the second observation switches: consecutive (a slow host) or not (a host in bursts)
-        ++seen;
-        if (++c->adapt_starved >= 2) graph_mode = true, ++c->adapt_switches, c->adapt_hot = 4, c->adapt_starved = 0;
-      } else if (q != cudaErrorNotReady) {
+    if (probing && !graph_mode && t >= 8 && T - t > 4 * c->chunk) {
+      const cudaError_t q = c->adapt == 2 ? cudaSuccess : cudaEventQuery(c->adapt_ev[t & 1]);  // end of frame t-2
+      if (q == cudaSuccess) {
+        if (++consec >= 3) graph_mode = true, ++c->adapt_switches, c->adapt_hot = 4;
+      } else if (q == cudaErrorNotReady) {
+        consec = 0;
+      } else {
         DDH_CK(c, q);
       }
     }
@@ -1258,10 +1269,10 @@ ddh_status ddh_step(ddh_ctx *c, const void *y, int32_t T, float *phi_out, float 
                    r_out ? r_out + t * fs : nullptr, status ? status + (size_t)t * c->S : nullptr,
                    pf ? (const float2 *)y + (t + 1) * fs : nullptr);
     if (s != DDH_OK) return s;
+    if (probing && !graph_mode) DDH_CK(c, cudaEventRecord(c->adapt_ev[t & 1], c->st));  // end of frame t
     c->frame += 1;
     ++t;
   }
-  if (probing && seen == 0) c->adapt_starved = 0;
   return DDH_OK;
 }
 

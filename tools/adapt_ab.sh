@@ -9,7 +9,7 @@ B="python bench.py --gpus 1 --no-e2e --no-latency --no-cpu-baseline --no-parity"
 one() { local l=$1; shift
   v=$("$@" 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step']*1e3,1), d['gpu_launches'])")
   echo "$l $v" | tee -a $OUT; }
-for rep in 1 2; do
+for rep in 1; do
   one "K300 adaptive            " $B --steps 300 --warmup 5
   one "K300 direct              " env DDH_ADAPTIVE_GRAPHS=0 $B --steps 300 --warmup 5
   one "K20  adaptive            " $B --steps 20 --warmup 5
@@ -20,7 +20,7 @@ for rep in 1 2; do
   one "K20  adaptive delay 60 us" env DDH_HOST_DELAY_US=60 $B --steps 20 --warmup 5
 done
 taskset -c 2 python -c "while True: pass" & HOG=$!
-for rep in 1 2; do
+for rep in 1; do
   one "K300 adaptive hogged     " taskset -c 2 $B --steps 300 --warmup 5
   one "K300 direct   hogged     " env DDH_ADAPTIVE_GRAPHS=0 taskset -c 2 $B --steps 300 --warmup 5
 done
